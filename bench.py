@@ -1,0 +1,450 @@
+#!/usr/bin/env python
+"""Benchmark: path samples/s and Mrays/s at 1080p, depth 8, on 1/2/4/8 GPUs,
+vs the CPU reference path (BASELINE.json `metric`).
+
+Workload (BASELINE.json configs[3]): the ~1.06 M-triangle
+procedural pushbutton assembly with mixed OpenPBR materials (coat, glass,
+metal, dielectric, emissive) under a synthetic HDR sky, 1920x1080, 256 spp,
+max_depth 8, rr_start 3.  One step = one full frame (W*H*spp paths) tiled
+across the ranks (interleaved 16x16 tiles) plus the NCCL merge onto rank 0.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+
+`--impl reference` times the reference's algorithm on the host cores: the
+float64 C restatement in oracle/ (the reference is Python/numba and is not
+installed on the GPU box), all threads, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "path samples/s and Mrays/s at 1080p depth 8 (1/2/4/8 GPU) vs CPU ref"
+UNIT = "samples/s"
+HBM_FALLBACK_GBS = 6650.0
+
+
+def parse_args():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--workload", default="pushbutton")
+    p.add_argument("--width", type=int, default=1920)
+    p.add_argument("--height", type=int, default=1080)
+    p.add_argument("--spp", type=int, default=256)
+    p.add_argument("--depth", type=int, default=8)
+    p.add_argument("--rr-start", type=int, default=3)
+    p.add_argument("--seed", type=int, default=0)
+    p.add_argument("--tile", type=int, default=16)
+    p.add_argument("--flags", type=int, default=0)
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=12.0)
+    p.add_argument("--ref-step-seconds", type=float, default=6.0)
+    return p.parse_args()
+
+
+def workload_config(args, n_tris: int, world: int) -> dict:
+    desc = {
+        "pushbutton": "C4: procedural CAD pushbutton assembly, mixed OpenPBR materials "
+                      "(metal, dielectric, coat, glass, emissive) + synthetic HDR sky",
+        "pushbutton_ref": "C4 (reference lobes only, gradient sky)",
+        "sphere70k": "C3: bumpy_sphere(70k) on a metal plane, gradient sky",
+        "cornell_c2": "C2: Cornell box, metal + glossy dielectric boxes",
+        "cornell_c2x": "C2: Cornell box, metal + coat + glass boxes",
+    }.get(args.workload, args.workload)
+    return {
+        "workload": f"{desc}, {n_tris} triangles, {args.width}x{args.height}, {args.spp} spp, "
+                    f"max_depth {args.depth}",
+        "scene": args.workload, "triangles": n_tris, "width": args.width,
+        "height": args.height, "spp": args.spp, "max_depth": args.depth,
+        "rr_start_depth": args.rr_start, "seed": args.seed,
+        "parallelism": f"tiles{args.tile}x{world}" if world > 1 else "single",
+        "l2": "no explicit flush: per-step working set (scene ~0.14 GB + path queues "
+              "~0.5 GB) exceeds the 126 MB L2",
+    }
+
+
+def build_workload(args):
+    from paper_2407_19977_b200.procgen import scene_by_name
+    from paper_2407_19977_b200 import build_bvh
+    scene = scene_by_name(args.workload, width=args.width, height=args.height)
+    bvh = build_bvh(scene.triangles)
+    return scene, bvh
+
+
+# ------------------------------------------------------------------ clocks
+
+class ClockSampler:
+    """nvidia-smi sampled every 200 ms during the timed region."""
+    FIELDS = ["index", "clocks.sm", "clocks.max.sm", "power.draw",
+              "clocks_event_reasons.active", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown",
+              "clocks_event_reasons.sw_thermal_slowdown", "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={','.join(self.FIELDS)}",
+                 "--format=csv,noheader,nounits", "-lms", "200", "-i", str(self.gpu)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == len(self.FIELDS):
+                self.rows.append(parts)
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        sm = [num(r[1]) for r in self.rows if num(r[1]) is not None]
+        mx = [num(r[2]) for r in self.rows if num(r[2]) is not None]
+        loaded = [s for s in sm if mx and s > 0.5 * max(mx)] or sm
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            for name, val in zip(names, r[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------ helpers
+
+def measured_peak():
+    f = ROOT / "MEASURED_PEAKS.json"
+    if f.exists():
+        try:
+            return float(json.loads(f.read_text())["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+        except Exception:
+            pass
+    return HBM_FALLBACK_GBS, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(workload: str):
+    """dram bytes per trace launch from the committed ncu capture, if any."""
+    f = ROOT / "profiles" / "trace_traffic.json"
+    if not f.exists():
+        return None, None
+    try:
+        d = json.loads(f.read_text())
+        e = d.get(workload)
+        if e:
+            return e.get("dram_bytes_per_ray"), e.get("source")
+    except Exception:
+        pass
+    return None, None
+
+
+def cpu_baseline(scene, bvh, args, seconds: float) -> dict:
+    """The float64 oracle (the reference's algorithm restated in C) on a
+    bounded pixel sample of the same frame, all host threads."""
+    from oracle.oracle import OracleScene, default_threads
+    from paper_2407_19977_b200 import camera_pack
+    oc = OracleScene.from_scene(scene, bvh)
+    cam = camera_pack(scene.camera)
+    w, h = args.width, args.height
+    threads = default_threads()
+    n = max(threads * 256, 8192)
+    paths = 0
+    segs = 0
+    t_total = 0.0
+    sample = 0
+    rng = np.random.default_rng(1)
+    while t_total < seconds:
+        pix = np.sort(rng.choice(w * h, size=min(n, w * h), replace=False))
+        t0 = time.perf_counter()
+        _, seg = oc.sample_values(pix, sample, cam, w, h, args.seed, args.depth, args.rr_start,
+                                  1e-4, threads)
+        dt = time.perf_counter() - t0
+        t_total += dt
+        paths += pix.size
+        segs += int(seg.sum())
+        sample += 1
+        if dt < seconds / 8:
+            n = min(w * h, n * 2)
+    return {"value": paths / t_total, "unit": UNIT, "cores": threads, "kind": "port",
+            "mrays_per_s": segs / t_total / 1e6,
+            "sample": f"{paths} random (pixel, sample) paths of the same frame and settings "
+                      f"over {sample} sample indices, {t_total:.1f} s on {threads} threads "
+                      f"(oracle/lt_oracle.c, float64 restatement of the reference)"}
+
+
+# ------------------------------------------------------------------ arms
+
+def run_reference(args, rank: int, world: int) -> None:
+    if rank != 0:
+        return
+    from oracle.oracle import OracleScene, default_threads
+    from paper_2407_19977_b200 import camera_pack
+    scene, bvh = build_workload(args)
+    oc = OracleScene.from_scene(scene, bvh)
+    cam = camera_pack(scene.camera)
+    w, h = args.width, args.height
+    threads = default_threads()
+    rng = np.random.default_rng(2)
+    # calibrate the per-step pixel sample to about --ref-step-seconds
+    n = 4096
+    while True:
+        pix = np.sort(rng.choice(w * h, size=n, replace=False))
+        t0 = time.perf_counter()
+        oc.sample_values(pix, 0, cam, w, h, args.seed, args.depth, args.rr_start, 1e-4, threads)
+        dt = time.perf_counter() - t0
+        if dt > 0.5 or n >= w * h:
+            n = int(min(w * h, max(1024, n * args.ref_step_seconds / max(dt, 1e-3))))
+            break
+        n = min(w * h, n * 4)
+    times, segs = [], []
+    for step in range(args.warmup + args.steps):
+        pix = np.sort(rng.choice(w * h, size=n, replace=False))
+        t0 = time.perf_counter()
+        _, seg = oc.sample_values(pix, step % args.spp, cam, w, h, args.seed, args.depth,
+                                  args.rr_start, 1e-4, threads)
+        dt = time.perf_counter() - t0
+        if step >= args.warmup:
+            times.append(dt)
+            segs.append(int(seg.sum()))
+    total = sum(times)
+    value = n * args.steps / total
+    cfg = workload_config(args, len(scene.triangles), world)
+    sample = (f"each step: {n} random pixels x 1 sample of the {w}x{h} frame "
+              f"({n / (w * h) / args.spp:.2e} of the full {args.spp}-spp workload)")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": cfg, "mrays_per_s": sum(segs) / total / 1e6,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def pinned_copy(a):
+    import torch
+    a = np.ascontiguousarray(a)
+    t = torch.empty(a.shape, dtype=torch.from_numpy(a[:0]).dtype, pin_memory=True)
+    out = t.numpy()
+    out[...] = a
+    return out, t
+
+
+def run_ours(args, rank: int, world: int, local_rank: int) -> None:
+    import torch
+    import torch.distributed as dist
+
+    from paper_2407_19977_b200 import RenderSettings, render_progressive
+    from paper_2407_19977_b200._lib import LT_FLAG_COUNT, LT_FLAG_PROFILE
+    from paper_2407_19977_b200.device import DeviceScene
+    from paper_2407_19977_b200.distributed import merge_tiles, render_distributed
+    from paper_2407_19977_b200.integrator import Accumulator, render_pass_device
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    scene, bvh = build_workload(args)
+    settings = RenderSettings(samples_per_pixel=args.spp, max_depth=args.depth,
+                              rr_start_depth=args.rr_start, seed=args.seed)
+    ds = DeviceScene(scene, bvh, device=local_rank)
+    cam = scene.camera
+    acc = Accumulator(cam.width, cam.height, local_rank)
+    shard = (rank, world, args.tile) if world > 1 else None
+    stream = torch.cuda.current_stream(dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def step(flags, spp=None):
+        acc.sum.zero_()
+        acc.valid.zero_()
+        acc.invalid.zero_()
+        render_pass_device(ds, cam, settings, acc, 0, spp or args.spp, flags=flags | args.flags,
+                           shard=shard, stream=stream)
+        if world > 1:
+            merge_tiles(acc, dst=0)
+
+    # untimed: work counters for the roofline (same paths, reduced spp)
+    count_spp = min(args.spp, 16)
+    step(LT_FLAG_COUNT, count_spp)
+    torch.cuda.synchronize(dev)
+    cst = ds.stats()
+    slab_per_ray = cst["slab_tests"] / max(1, cst["rays"])
+    tri_per_ray = cst["tri_tests"] / max(1, cst["rays"])
+    bytes_per_ray = 32.0 * slab_per_ray + 48.0 * tri_per_ray + 40.0
+
+    for _ in range(args.warmup):
+        step(0)
+    torch.cuda.synchronize(dev)
+    barrier()
+    sampler = ClockSampler(local_rank) if rank == 0 else None
+    if sampler:
+        sampler.start()
+        time.sleep(0.3)
+    torch.cuda.synchronize(dev)
+    barrier()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step(LT_FLAG_PROFILE)
+    ev1.record(stream)
+    torch.cuda.synchronize(dev)
+    barrier()
+    clocks = sampler.stop() if sampler else None
+    ms = ev0.elapsed_time(ev1)
+    st = ds.stats()    # the last timed step on this rank
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    rays = torch.tensor([st["rays"]], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(rays, op=dist.ReduceOp.SUM)
+    ms_max = float(t.item())
+    rays_per_step = float(rays.item())
+    samples_per_step = args.width * args.height * args.spp
+    value = samples_per_step * args.steps / (ms_max / 1e3)
+    mrays = rays_per_step * args.steps / (ms_max / 1e3) / 1e6
+
+    # roofline of the dominant kernel (closest-hit traversal), this rank
+    peak, peak_src = measured_peak()
+    trace_ms = st["trace_ms"]
+    launches = max(1, st["trace_launches"])
+    achieved = (st["rays"] * bytes_per_ray) / (trace_ms / 1e3) / 1e9 if trace_ms > 0 else None
+    traffic_per_ray, traffic_src = ncu_traffic(args.workload)
+    roofline = {
+        "bound": "hbm", "kernel": "k_trace (closest-hit BVH traversal)",
+        "achieved": achieved, "peak": peak, "unit": "GB/s",
+        "frac": achieved / peak if achieved else None,
+        "traffic": (traffic_per_ray * st["rays"] / launches) if traffic_per_ray else None,
+        "algorithmic_bytes_per_launch": st["rays"] * bytes_per_ray / launches,
+        "bytes_per_ray": bytes_per_ray, "slab_tests_per_ray": slab_per_ray,
+        "tri_tests_per_ray": tri_per_ray, "trace_launches_per_step": launches,
+        "trace_ms_per_step": trace_ms, "trace_share_of_step": trace_ms / (ms / args.steps),
+        "peak_source": peak_src, "traffic_source": traffic_src,
+    }
+
+    # end to end through the public API: scene upload (pinned host arrays),
+    # render, merge, image back to the host
+    e2e = None
+    if not args.no_e2e:
+        keep = []
+
+        def pin(obj, names):
+            for nm in names:
+                arr, t_ = pinned_copy(getattr(obj, nm))
+                keep.append(t_)
+                setattr(obj, nm, arr)
+        pin(scene.triangles, ["v0", "v1", "v2", "n0", "n1", "n2", "material_index"])
+        pin(bvh, ["bounds_min", "bounds_max", "left_child", "right_child", "first_triangle",
+                  "triangle_count", "triangle_order"])
+        h2d = sum(getattr(scene.triangles, nm).nbytes for nm in
+                  ["v0", "v1", "v2", "n0", "n1", "n2", "material_index"])
+        h2d += sum(getattr(bvh, nm).nbytes for nm in
+                   ["bounds_min", "bounds_max", "left_child", "right_child", "first_triangle",
+                    "triangle_count", "triangle_order"])
+        d2h = args.width * args.height * (3 * 8 + 8) if rank == 0 else 0
+
+        def e2e_step():
+            if world > 1:
+                return render_distributed(scene, settings, bvh, tile_size=args.tile,
+                                          device=local_rank)
+            return render_progressive(scene, settings, bvh=bvh, device=local_rank)
+        e2e_step()
+        torch.cuda.synchronize(dev)
+        barrier()
+        t0 = time.perf_counter()
+        n_e2e = max(1, min(args.steps, 3))
+        for _ in range(n_e2e):
+            e2e_step()
+        torch.cuda.synchronize(dev)
+        el = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(el, op=dist.ReduceOp.MAX)
+        e2e = {"value": samples_per_step * n_e2e / float(el.item()), "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "steps": n_e2e,
+               "api": "render_progressive(scene, settings, bvh) (render_distributed for N>1): "
+                      "scene upload from pinned host arrays + BVH flatten + render + image "
+                      "D2H, wall clock"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(scene, bvh, args, args.cpu_seconds)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "fp32", "data": "synthetic",
+            "config": workload_config(args, len(scene.triangles), world),
+            "mrays_per_s": mrays, "rays_per_step": rays_per_step,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
+            "gpu_launches": int(st["kernel_launches"] * args.steps),
+        }
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,177 @@
+/*
+ * luxb200.h -- C-ABI of the B200-native path tracer (the drop-in boundary).
+ *
+ * Plain pointers and sizes only; no torch or CUDA types in the signatures
+ * (`void *stream` is a cudaStream_t, NULL = the legacy default stream).
+ * Every entry point returns an int status (LT_OK = 0) and leaves a
+ * thread-local message for lt_last_error().  Non-finite path samples are
+ * counted, never raised (integrator.py:266-272).
+ *
+ * Each entry point names the reference interface it replaces, as file:line
+ * under /root/reference/pkg/src/luxtrace/.  The Python mirror
+ * (paper_2407_19977_b200/) binds these with ctypes; INTEGRATION.md shows the
+ * binding a luxtrace maintainer would add on the reference side.
+ */
+#ifndef LUXB200_H
+#define LUXB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LT_ABI_VERSION 1
+
+/* status codes */
+#define LT_OK 0
+#define LT_ERR_INVALID 1   /* bad argument: the Python mirror raises ValueError */
+#define LT_ERR_CUDA 2      /* CUDA runtime failure: RuntimeError */
+#define LT_ERR_NOMEM 3     /* allocation failure: MemoryError */
+#define LT_ERR_UNSUPPORTED 4
+
+/* environment kinds: _ENV_UNIFORM / _ENV_GRADIENT (integrator.py:37-38);
+ * LT_ENV_LATLONG is the synthetic-HDR extension (no reference, parity unpinned) */
+#define LT_ENV_UNIFORM 0
+#define LT_ENV_GRADIENT 1
+#define LT_ENV_LATLONG 2
+
+/* lt_render_params.flags */
+#define LT_FLAG_SORT_MATERIALS 1u   /* shade hits in material-sorted order */
+#define LT_FLAG_NO_SMEM_TOP 2u      /* disable shared-memory staging of top BVH nodes */
+#define LT_FLAG_PROFILE 4u          /* time every trace launch with CUDA events */
+#define LT_FLAG_COUNT 8u            /* count slab / triangle tests in the trace kernel */
+
+typedef struct lt_scene lt_scene;
+
+/* Scene description: the arrays `_scene_arrays` packs for `_render_pass`
+ * (integrator.py:284-291), all host pointers, row-major, reference dtypes. */
+typedef struct lt_scene_desc {
+  /* TriangleBuffer (geometry.py:88-131): (n,3) float64 each, (n,) int32 */
+  int64_t n_triangles;
+  const double *v0, *v1, *v2, *n0, *n1, *n2;
+  const int32_t *material_index;
+  /* Bvh (bvh.py:38-50), the host-built tree, consumed unchanged */
+  int64_t n_nodes;
+  const double *bounds_min, *bounds_max;            /* (n_nodes,3) */
+  const int32_t *left_child, *right_child;          /* (n_nodes,) -1 at leaves */
+  const int32_t *first_triangle, *triangle_count;   /* (n_nodes,) leaf iff count > 0 */
+  const int32_t *triangle_order;                    /* (n,) */
+  /* pack_materials (material.py:68-92): (k,) or (k,3) float64 */
+  int32_t n_materials;
+  const double *base_weight, *base_color, *base_metalness, *specular_weight;
+  const double *specular_color, *specular_roughness, *specular_ior;
+  const double *emission_luminance, *emission_color;
+  /* extension lobes (no reference; NULL = zero weight = reference material) */
+  const double *coat_weight, *coat_roughness, *coat_ior, *coat_color;
+  const double *transmission_weight, *transmission_color;
+  /* _environment_pack (integrator.py:118-121) */
+  int32_t env_kind;
+  double env_a[3], env_b[3];
+  /* LT_ENV_LATLONG: (env_height, env_width, 3) float32 radiance, times env_scale */
+  int32_t env_width, env_height;
+  const float *env_texels;
+  double env_scale;
+} lt_scene_desc;
+
+typedef struct lt_scene_info {
+  int32_t device;
+  int64_t n_triangles, n_nodes, n_internal, n_smem_nodes;
+  int64_t device_bytes;         /* resident scene bytes in HBM */
+  int32_t sm_count;
+} lt_scene_info;
+
+/* One render pass: `_render_pass(..., sample_start, sample_count, cam, width,
+ * height, ..., seed, max_depth, rr_start, t_min)` (integrator.py:230-237). */
+typedef struct lt_render_params {
+  double camera[14];            /* _camera_pack (integrator.py:75-83) */
+  int32_t width, height;
+  int64_t sample_start, sample_count;
+  uint64_t seed;
+  int32_t max_depth, rr_start;
+  double t_min;
+  /* image sharding: square tiles of tile_size, tile k (raster order) is
+   * rendered by rank k % n_ranks.  n_ranks <= 1 renders every pixel.
+   * RNG streams stay keyed by the GLOBAL pixel index, so any sharding yields
+   * the same per-pixel values as one GPU. */
+  int32_t tile_size, rank, n_ranks;
+  uint32_t flags;
+  int64_t max_batch_paths;      /* 0 = library default */
+} lt_render_params;
+
+typedef struct lt_render_stats {
+  int64_t paths;                /* (pixel, sample) paths traced */
+  int64_t rays;                 /* closest-hit queries (primary + continuation) */
+  int64_t batches;
+  int64_t kernel_launches;
+  int64_t trace_launches;       /* trace kernel launches in the pass */
+  int64_t slab_tests;           /* child-box tests incl. root (LT_FLAG_COUNT only) */
+  int64_t tri_tests;            /* triangle tests (LT_FLAG_COUNT only) */
+  double trace_ms;              /* sum of CUDA-event times of the trace launches
+                                   (LT_FLAG_PROFILE only, else 0) */
+} lt_render_stats;
+
+/* ---- library ---- */
+int lt_abi_version(void);
+const char *lt_last_error(void);
+int lt_device_count(int32_t *count);
+
+/* ---- host BVH build: build_bvh (bvh.py:286-298), same binned SAH
+ * (bvh.py:85-262), bit-identical arrays.  Output buffers are caller-owned:
+ * node arrays sized 2n (bounds 2n*3), order sized n. ---- */
+int lt_build_bvh(const double *v0, const double *v1, const double *v2, int64_t n,
+                 int32_t leaf_size, int32_t bins, double *bounds_min, double *bounds_max,
+                 int32_t *left_child, int32_t *right_child, int32_t *first_triangle,
+                 int32_t *triangle_count, int32_t *triangle_order, int64_t *n_nodes,
+                 int64_t *leaf_count, int64_t *max_depth);
+
+/* ---- scene residency: replaces the per-call `_scene_arrays` packing
+ * (integrator.py:284-291); flattens the host BVH into the HBM layout ---- */
+int lt_scene_create(const lt_scene_desc *desc, int32_t device, lt_scene **out);
+int lt_scene_destroy(lt_scene *scene);
+int lt_scene_info_get(const lt_scene *scene, lt_scene_info *info);
+
+/* ---- closest hit: intersect_scene_batch (bvh.py:667-677) / _traverse_batch
+ * (bvh.py:554-567).  Device pointers: origins/dirs (n,3) float32; outputs
+ * idx (n,) int32 (-1 on miss), t (n,) float32 (+inf on miss). ---- */
+int lt_intersect_batch(lt_scene *scene, const float *origins, const float *dirs, int64_t n,
+                       float t_min, float t_max, int32_t *idx, float *t, void *stream);
+/* Host-buffer twin with the reference dtypes: float64 rays, int64 idx,
+ * float64 t (the fp32 result widened). */
+int lt_intersect_batch_host(lt_scene *scene, const double *origins, const double *dirs,
+                            int64_t n, double t_min, double t_max, int64_t *idx, double *t);
+/* Work counters: traversal_counts_batch (bvh.py:680-691), host buffers.
+ * nodes = child-box tests + 1 (root), tests = triangle tests. */
+int lt_traversal_counts_host(lt_scene *scene, const double *origins, const double *dirs,
+                             int64_t n, double t_min, double t_max, int64_t *nodes,
+                             int64_t *tests);
+
+/* ---- the operator: _render_pass (integrator.py:230-277).
+ * Device pointers: accum_sum (h*w*3) float32 per-pixel SUM of finite
+ * samples, valid/invalid (h*w) uint32 counts; all updated in place.
+ * Samples of a pixel are added in sample-index order. ---- */
+int lt_render_pass(lt_scene *scene, const lt_render_params *params, float *accum_sum,
+                   uint32_t *valid, uint32_t *invalid, void *stream);
+/* Host-buffer drop-in with the reference's exact in/out contract:
+ * accum (h,w,3) float64 running MEAN, valid/invalid (h,w) int64, updated in
+ * place with samples [sample_start, sample_start + sample_count). */
+int lt_render_pass_host(lt_scene *scene, const lt_render_params *params, double *accum_mean,
+                        int64_t *valid, int64_t *invalid);
+int lt_render_stats_get(const lt_scene *scene, lt_render_stats *stats);
+
+/* ---- single paths with caller-supplied PCG state: trace_radiance
+ * (integrator.py:294-307) batched.  Host buffers: origins/dirs (n,3) f64,
+ * state/inc (n,) u64 in, rgb (n,3) f64 out, state_out (n,) u64. ---- */
+int lt_trace_paths_host(lt_scene *scene, const double *origins, const double *dirs,
+                        const uint64_t *state, const uint64_t *inc, int64_t n,
+                        int32_t max_depth, int32_t rr_start, double t_min, double *rgb,
+                        uint64_t *state_out);
+
+/* ---- display transform (tonemap.py:18-61, the §8(f) next row): linear
+ * (h*w*3) float32 device -> sRGB u8 (h*w*3) device ---- */
+int lt_tonemap_u8(const float *linear, int64_t n_pixels, uint8_t *out, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,34 @@
+"""paper_2407_19977_b200 -- B200-native Monte-Carlo path tracing of
+triangle-mesh scenes with the OpenPBR surface model (arXiv 2407.19977's hot
+path), a drop-in for the `luxtrace` reference's render API.
+
+Host code is Python; the hot path is hand-written sm_100a CUDA behind the
+C-ABI in include/luxb200.h (built in-tree by `build.py`).  There is no CPU
+fallback: compute entry points raise when the library or a GPU is missing.
+"""
+from .geometry import (DEFAULT_T_MIN, Ray, Triangle, TriangleBuffer, normalize, vec3)
+from .material import (OpenPbrParams, emitted_radiance, pack_material_table, pack_materials)
+from .scene import (CameraConfig, EnvironmentConfig, SceneDescription, SceneError, camera_pack)
+from .rng import PcgState, next_unit_real, pcg_next_u32, pcg_seed, seed_stream
+from .bvh import (STACK_SIZE, BuildStats, Bvh, build_bvh, intersect_scene,
+                  intersect_scene_batch, traversal_counts_batch)
+from .device import DeviceScene
+from .integrator import (RenderResult, RenderSettings, environment_radiance,
+                         generate_camera_ray, render_image, render_pass, render_progressive,
+                         trace_radiance, trace_radiance_batch)
+from .procgen import bumpy_sphere, cornell_box, pushbutton, sphere_on_plane, synthetic_hdr
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "DEFAULT_T_MIN", "Ray", "Triangle", "TriangleBuffer", "normalize", "vec3",
+    "OpenPbrParams", "emitted_radiance", "pack_material_table", "pack_materials",
+    "CameraConfig", "EnvironmentConfig", "SceneDescription", "SceneError", "camera_pack",
+    "PcgState", "next_unit_real", "pcg_next_u32", "pcg_seed", "seed_stream",
+    "STACK_SIZE", "BuildStats", "Bvh", "build_bvh", "intersect_scene", "intersect_scene_batch",
+    "traversal_counts_batch", "DeviceScene",
+    "RenderResult", "RenderSettings", "environment_radiance", "generate_camera_ray",
+    "render_image", "render_pass", "render_progressive", "trace_radiance",
+    "trace_radiance_batch",
+    "bumpy_sphere", "cornell_box", "pushbutton", "sphere_on_plane", "synthetic_hdr",
+]

@@ -1,0 +1,879 @@
+// lt_api.cu -- the C-ABI (include/luxb200.h): scene residency, the render
+// pass orchestration (the wavefront loop), ray queries and host-buffer
+// drop-ins with the reference's dtypes.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "lt_internal.h"
+#include "lt_kernels.h"
+
+using namespace lt;
+
+// ------------------------------------------------------------------ errors
+
+static thread_local std::string g_last_error;
+
+int lt_fail(int code, const char *fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+#define CK(call)                                                                   \
+  do {                                                                             \
+    cudaError_t e_ = (call);                                                       \
+    if (e_ != cudaSuccess)                                                         \
+      return lt_fail(e_ == cudaErrorMemoryAllocation ? LT_ERR_NOMEM : LT_ERR_CUDA, \
+                     "%s failed: %s", #call, cudaGetErrorString(e_));              \
+  } while (0)
+
+#define RET(expr)            \
+  do {                       \
+    int r_ = (expr);         \
+    if (r_ != LT_OK) return r_; \
+  } while (0)
+
+namespace {
+
+constexpr int64_t kDefaultBatchPaths = int64_t(1) << 22;  // 4M paths (~512 MB of queues)
+constexpr int32_t kMaxBfsNodes = 2048;                    // BFS-ordered top of the tree
+
+struct DevBuf {
+  void *p = nullptr;
+  size_t bytes = 0;
+  int ensure(size_t want) {
+    if (want <= bytes) return LT_OK;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    CK(cudaMalloc(&p, want));
+    bytes = want;
+    return LT_OK;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <class T>
+  T *as() const {
+    return static_cast<T *>(p);
+  }
+};
+
+struct HostBuf {
+  void *p = nullptr;
+  size_t bytes = 0;
+  int ensure(size_t want) {
+    if (want <= bytes) return LT_OK;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    bytes = 0;
+    CK(cudaMallocHost(&p, want));
+    bytes = want;
+    return LT_OK;
+  }
+  void release() {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <class T>
+  T *as() const {
+    return static_cast<T *>(p);
+  }
+};
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+}  // namespace
+
+struct lt_scene {
+  int device = 0;
+  int sm_count = 0;
+  cudaStream_t stream = nullptr;
+  SceneView view{};
+  int64_t n_tris = 0, n_nodes = 0, n_internal = 0, n_bfs = 0;
+  int64_t device_bytes = 0;
+  DevBuf nodes, tris, shade, mats, env;
+  // wavefront workspace
+  int64_t cap = 0;
+  int32_t depth_cap = 0;
+  DevBuf q_o[2], q_d[2], hits, T, L, rng, counters, ray_ctr;
+  // sharding pixel list cache
+  DevBuf pix_list;
+  int64_t pix_key[5] = {-1, -1, -1, -1, -1};
+  int64_t pix_count = 0;
+  // scratch for ray queries / host drop-ins
+  DevBuf s_a, s_b, s_c, s_d, s_e, s_f;
+  HostBuf h_stage;
+  // launch configuration
+  int trace_grid[2] = {0, 0};  // [no smem, smem]
+  int shade_grid = 0;
+  int smem_nodes = 0;
+  // stats of the last pass
+  lt_render_stats stats{};
+  std::vector<cudaEvent_t> ev_pool;
+  int ev_used = 0;
+};
+
+// ------------------------------------------------------------------ library
+
+extern "C" int lt_abi_version(void) { return LT_ABI_VERSION; }
+
+extern "C" const char *lt_last_error(void) { return g_last_error.c_str(); }
+
+extern "C" int lt_device_count(int32_t *count) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) {
+    *count = 0;
+    return lt_fail(LT_ERR_CUDA, "cudaGetDeviceCount failed: %s", cudaGetErrorString(e));
+  }
+  *count = n;
+  return LT_OK;
+}
+
+extern "C" int lt_build_bvh(const double *v0, const double *v1, const double *v2, int64_t n,
+                            int32_t leaf_size, int32_t bins, double *bounds_min,
+                            double *bounds_max, int32_t *left_child, int32_t *right_child,
+                            int32_t *first_triangle, int32_t *triangle_count,
+                            int32_t *triangle_order, int64_t *n_nodes, int64_t *leaf_count,
+                            int64_t *max_depth) {
+  if (!v0 || !v1 || !v2 || !bounds_min || !bounds_max || !left_child || !right_child ||
+      !first_triangle || !triangle_count || !triangle_order || !n_nodes || !leaf_count ||
+      !max_depth)
+    return lt_fail(LT_ERR_INVALID, "lt_build_bvh: null pointer");
+  return lt_build_bvh_impl(v0, v1, v2, n, leaf_size, bins, bounds_min, bounds_max, left_child,
+                           right_child, first_triangle, triangle_count, triangle_order, n_nodes,
+                           leaf_count, max_depth);
+}
+
+// ------------------------------------------------------------------ scene
+
+static int validate_desc(const lt_scene_desc *d) {
+  if (!d) return lt_fail(LT_ERR_INVALID, "null scene description");
+  if (d->n_triangles < 1) return lt_fail(LT_ERR_INVALID, "empty scene");
+  if (d->n_triangles >= (int64_t(1) << 31) - 1)
+    return lt_fail(LT_ERR_INVALID, "too many triangles (%lld)", (long long)d->n_triangles);
+  if (!d->v0 || !d->v1 || !d->v2 || !d->n0 || !d->n1 || !d->n2 || !d->material_index)
+    return lt_fail(LT_ERR_INVALID, "triangle arrays must be non-null");
+  if (d->n_nodes < 1 || !d->bounds_min || !d->bounds_max || !d->left_child ||
+      !d->right_child || !d->first_triangle || !d->triangle_count || !d->triangle_order)
+    return lt_fail(LT_ERR_INVALID, "bvh arrays must be non-null");
+  if (d->n_materials < 1 || !d->base_weight || !d->base_color || !d->base_metalness ||
+      !d->specular_weight || !d->specular_color || !d->specular_roughness ||
+      !d->specular_ior || !d->emission_luminance || !d->emission_color)
+    return lt_fail(LT_ERR_INVALID, "material arrays must be non-null");
+  const int64_t n = d->n_triangles, nn = d->n_nodes;
+  for (int64_t i = 0; i < n; ++i) {
+    const int32_t m = d->material_index[i];
+    if (m < 0 || m >= d->n_materials)
+      return lt_fail(LT_ERR_INVALID, "triangle %lld: material index %d out of range [0, %d)",
+                     (long long)i, m, d->n_materials);
+    const int32_t o = d->triangle_order[i];
+    if (o < 0 || o >= n)
+      return lt_fail(LT_ERR_INVALID, "triangle_order[%lld] = %d out of range", (long long)i, o);
+  }
+  for (int64_t i = 0; i < nn; ++i) {
+    if (d->triangle_count[i] > 0) {
+      const int64_t f = d->first_triangle[i], c = d->triangle_count[i];
+      if (f < 0 || f + c > n)
+        return lt_fail(LT_ERR_INVALID, "node %lld: leaf range [%lld, %lld) out of bounds",
+                       (long long)i, (long long)f, (long long)(f + c));
+    } else {
+      const int32_t l = d->left_child[i], r = d->right_child[i];
+      if (l <= i || r <= i || l >= nn || r >= nn)
+        return lt_fail(LT_ERR_INVALID, "node %lld: invalid children (%d, %d)", (long long)i, l,
+                       r);
+    }
+  }
+  if (d->env_kind < LT_ENV_UNIFORM || d->env_kind > LT_ENV_LATLONG)
+    return lt_fail(LT_ERR_INVALID, "unknown environment kind %d", d->env_kind);
+  if (d->env_kind == LT_ENV_LATLONG &&
+      (!d->env_texels || d->env_width < 1 || d->env_height < 1))
+    return lt_fail(LT_ERR_INVALID, "lat-long environment needs texels and a size");
+  return LT_OK;
+}
+
+// float64 -> float32 rounded toward -inf / +inf (host side of the outward
+// rounding the flatten kernel does with __double2float_rd/_ru)
+static float f32_down(double x) {
+  float f = (float)x;
+  if ((double)f > x) f = std::nextafterf(f, -INFINITY);
+  return f;
+}
+static float f32_up(double x) {
+  float f = (float)x;
+  if ((double)f < x) f = std::nextafterf(f, INFINITY);
+  return f;
+}
+
+static double alpha_of(double r) {
+  double a = r * r;
+  return a < 1e-4 ? 1e-4 : a;
+}
+static double f0_from_ior(double ior) {
+  double r = (ior - 1.0) / (ior + 1.0);
+  return r * r;
+}
+
+static void build_material(const lt_scene_desc *d, int i, GpuMaterial &g) {
+  std::memset(&g, 0, sizeof(g));
+  const double bw = d->base_weight[i], m = d->base_metalness[i], sw = d->specular_weight[i];
+  const double alpha = alpha_of(d->specular_roughness[i]);
+  const double f0d = f0_from_ior(d->specular_ior[i]);
+  const double avg = sw * (f0d + (1.0 - f0d) / 21.0);
+  g.bw = (float)bw;
+  for (int k = 0; k < 3; ++k) {
+    g.bc[k] = (float)d->base_color[3 * i + k];
+    g.sc[k] = (float)d->specular_color[3 * i + k];
+    g.ec[k] = (float)d->emission_color[3 * i + k];
+  }
+  g.m = (float)m;
+  g.sw = (float)sw;
+  g.alpha = (float)alpha;
+  g.a2 = (float)(alpha * alpha);
+  g.f0d = (float)f0d;
+  g.fdavg = (float)avg;
+  g.diff = (float)(bw * (1.0 / 3.141592653589793) * (1.0 - avg));
+  g.el = (float)d->emission_luminance[i];
+  g.ior = (float)d->specular_ior[i];
+  uint32_t flags = 0;
+  if (m <= 0.0 && sw <= 0.0) flags |= MAT_DIFFUSE_ONLY;
+  if (d->emission_luminance[i] > 0.0) flags |= MAT_EMISSIVE;
+  const double cw = d->coat_weight ? d->coat_weight[i] : 0.0;
+  if (cw > 0.0) {
+    flags |= MAT_COAT;
+    const double ca = alpha_of(d->coat_roughness ? d->coat_roughness[i] : 0.0);
+    const double f0c = f0_from_ior(d->coat_ior ? d->coat_ior[i] : 1.5);
+    g.cw = (float)cw;
+    g.calpha = (float)ca;
+    g.ca2 = (float)(ca * ca);
+    g.f0c = (float)f0c;
+    g.cfbar = (float)(f0c + (1.0 - f0c) / 21.0);
+  }
+  for (int k = 0; k < 3; ++k) {
+    g.cc[k] = d->coat_color ? (float)d->coat_color[3 * i + k] : 1.f;
+    g.tc[k] = d->transmission_color ? (float)d->transmission_color[3 * i + k] : 1.f;
+  }
+  const double tw = d->transmission_weight ? d->transmission_weight[i] : 0.0;
+  if (tw > 0.0 && m < 1.0) {
+    flags |= MAT_GLASS;
+    g.tw = (float)tw;
+  }
+  g.flags = flags;
+}
+
+template <class T>
+static int upload(DevBuf &b, const T *src, size_t count, cudaStream_t st) {
+  RET(b.ensure(std::max<size_t>(count * sizeof(T), 16)));
+  if (count) CK(cudaMemcpyAsync(b.p, src, count * sizeof(T), cudaMemcpyHostToDevice, st));
+  return LT_OK;
+}
+
+static void destroy_scene(lt_scene *s) {
+  if (!s) return;
+  DeviceGuard g(s->device);
+  if (s->stream) cudaStreamSynchronize(s->stream);
+  for (DevBuf *b : {&s->nodes, &s->tris, &s->shade, &s->mats, &s->env, &s->q_o[0], &s->q_o[1],
+                    &s->q_d[0], &s->q_d[1], &s->hits, &s->T, &s->L, &s->rng, &s->counters,
+                    &s->ray_ctr, &s->pix_list, &s->s_a, &s->s_b, &s->s_c, &s->s_d, &s->s_e,
+                    &s->s_f})
+    b->release();
+  s->h_stage.release();
+  for (cudaEvent_t e : s->ev_pool) cudaEventDestroy(e);
+  if (s->stream) cudaStreamDestroy(s->stream);
+  delete s;
+}
+
+static int configure_launches(lt_scene *s) {
+  int blocks = 0;
+  const char *env = std::getenv("LT_SMEM_NODES");
+  int want = env ? std::atoi(env) : 256;
+  s->smem_nodes = (int)std::max<int64_t>(0, std::min<int64_t>(want, s->n_bfs));
+  size_t smem = (size_t)s->smem_nodes * 64;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, trace_kernel_ptr(false, false),
+                                                   kTraceThreads, 0));
+  s->trace_grid[0] = std::max(1, blocks) * s->sm_count;
+  blocks = 0;
+  if (smem > 0) {
+    for (bool c : {false, true})
+      CK(cudaFuncSetAttribute(trace_kernel_ptr(true, c),
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, trace_kernel_ptr(true, false),
+                                                     kTraceThreads, smem));
+  }
+  s->trace_grid[1] = std::max(1, blocks) * s->sm_count;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, shade_kernel_ptr(), kShadeThreads, 0));
+  s->shade_grid = std::max(1, blocks) * s->sm_count;
+  return LT_OK;
+}
+
+static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s) {
+  s->device = device;
+  CK(cudaSetDevice(device));
+  CK(cudaDeviceGetAttribute(&s->sm_count, cudaDevAttrMultiProcessorCount, device));
+  CK(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+  cudaStream_t st = s->stream;
+  const int64_t n = d->n_triangles, nn = d->n_nodes;
+  s->n_tris = n;
+  s->n_nodes = nn;
+
+  // --- internal-node renumbering: top levels BFS, the rest depth-first
+  std::vector<int32_t> new_index(nn, -1), perm;
+  perm.reserve(nn);
+  auto is_leaf = [&](int64_t i) { return d->triangle_count[i] > 0; };
+  if (!is_leaf(0)) {
+    std::vector<int32_t> queue;
+    queue.push_back(0);
+    size_t head = 0;
+    while (head < queue.size() && (int64_t)perm.size() < kMaxBfsNodes) {
+      const int32_t x = queue[head++];
+      new_index[x] = (int32_t)perm.size();
+      perm.push_back(x);
+      for (int32_t c : {d->left_child[x], d->right_child[x]})
+        if (!is_leaf(c)) queue.push_back(c);
+    }
+    s->n_bfs = (int64_t)perm.size();
+    std::vector<int32_t> stack;
+    for (size_t q = head; q < queue.size(); ++q) {
+      stack.push_back(queue[q]);
+      while (!stack.empty()) {
+        const int32_t x = stack.back();
+        stack.pop_back();
+        new_index[x] = (int32_t)perm.size();
+        perm.push_back(x);
+        const int32_t l = d->left_child[x], r = d->right_child[x];
+        if (!is_leaf(r)) stack.push_back(r);
+        if (!is_leaf(l)) stack.push_back(l);
+      }
+    }
+  }
+  s->n_internal = (int64_t)perm.size();
+  // leaf-end flags for the leaf-ordered triangle stream
+  std::vector<uint8_t> leaf_end(n, 0);
+  for (int64_t i = 0; i < nn; ++i)
+    if (is_leaf(i)) leaf_end[d->first_triangle[i] + d->triangle_count[i] - 1] = 1;
+
+  // --- upload the float64 arrays and flatten on the device
+  DevBuf t_v[6], t_mat, t_order, t_end, t_bmin, t_bmax, t_left, t_right, t_first, t_count,
+      t_perm, t_new;
+  const double *src[6] = {d->v0, d->v1, d->v2, d->n0, d->n1, d->n2};
+  int rc = LT_OK;
+  do {
+    for (int k = 0; k < 6 && rc == LT_OK; ++k) rc = upload(t_v[k], src[k], 3 * n, st);
+    if (rc) break;
+    if ((rc = upload(t_mat, d->material_index, n, st))) break;
+    if ((rc = upload(t_order, d->triangle_order, n, st))) break;
+    if ((rc = upload(t_end, leaf_end.data(), n, st))) break;
+    if ((rc = s->tris.ensure(48 * n))) break;
+    if ((rc = s->shade.ensure(48 * n))) break;
+    launch_flatten_tris(t_v[0].as<double>(), t_v[1].as<double>(), t_v[2].as<double>(),
+                        t_v[3].as<double>(), t_v[4].as<double>(), t_v[5].as<double>(),
+                        t_mat.as<int32_t>(), t_order.as<int32_t>(), t_end.as<uint8_t>(), n,
+                        s->tris.as<float4>(), s->shade.as<float4>(), st);
+    if ((rc = s->nodes.ensure(std::max<int64_t>(1, s->n_internal) * 64))) break;
+    if (s->n_internal > 0) {
+      if ((rc = upload(t_bmin, d->bounds_min, 3 * nn, st))) break;
+      if ((rc = upload(t_bmax, d->bounds_max, 3 * nn, st))) break;
+      if ((rc = upload(t_left, d->left_child, nn, st))) break;
+      if ((rc = upload(t_right, d->right_child, nn, st))) break;
+      if ((rc = upload(t_first, d->first_triangle, nn, st))) break;
+      if ((rc = upload(t_count, d->triangle_count, nn, st))) break;
+      if ((rc = upload(t_perm, perm.data(), perm.size(), st))) break;
+      if ((rc = upload(t_new, new_index.data(), nn, st))) break;
+      launch_flatten_nodes(t_bmin.as<double>(), t_bmax.as<double>(), t_left.as<int32_t>(),
+                           t_right.as<int32_t>(), t_first.as<int32_t>(), t_count.as<int32_t>(),
+                           t_perm.as<int32_t>(), t_new.as<int32_t>(), s->n_internal,
+                           s->nodes.as<float4>(), st);
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+      rc = lt_fail(LT_ERR_CUDA, "flatten launch failed: %s", cudaGetErrorString(e));
+      break;
+    }
+    // materials
+    std::vector<GpuMaterial> mats(d->n_materials);
+    for (int i = 0; i < d->n_materials; ++i) build_material(d, i, mats[i]);
+    if ((rc = upload(s->mats, mats.data(), mats.size(), st))) break;
+    // environment
+    if (d->env_kind == LT_ENV_LATLONG) {
+      const int64_t np = (int64_t)d->env_width * d->env_height;
+      std::vector<float4> tex(np);
+      for (int64_t i = 0; i < np; ++i)
+        tex[i] = make_float4(d->env_texels[3 * i], d->env_texels[3 * i + 1],
+                             d->env_texels[3 * i + 2], 0.f);
+      if ((rc = upload(s->env, tex.data(), tex.size(), st))) break;
+    }
+    e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) {
+      rc = lt_fail(LT_ERR_CUDA, "scene upload failed: %s", cudaGetErrorString(e));
+      break;
+    }
+  } while (0);
+  for (DevBuf &b : t_v) b.release();
+  for (DevBuf *b : {&t_mat, &t_order, &t_end, &t_bmin, &t_bmax, &t_left, &t_right, &t_first,
+                    &t_count, &t_perm, &t_new})
+    b->release();
+  RET(rc);
+
+  SceneView &v = s->view;
+  v.nodes = s->nodes.as<float4>();
+  v.tris = s->tris.as<float4>();
+  v.shade = s->shade.as<float4>();
+  v.mats = s->mats.as<GpuMaterial>();
+  v.env_map = s->env.as<float4>();
+  v.root_link = is_leaf(0) ? ~d->first_triangle[0] : 0;
+  for (int a = 0; a < 3; ++a) {
+    v.root_lo[a] = f32_down(d->bounds_min[a]);
+    v.root_hi[a] = f32_up(d->bounds_max[a]);
+  }
+  v.env_kind = d->env_kind;
+  v.env_w = d->env_width;
+  v.env_h = d->env_height;
+  v.env_scale = (float)(d->env_kind == LT_ENV_LATLONG ? d->env_scale : 1.0);
+  for (int k = 0; k < 3; ++k) {
+    v.env_a[k] = (float)d->env_a[k];
+    v.env_b[k] = (float)d->env_b[k];
+  }
+  s->device_bytes = (int64_t)(s->nodes.bytes + s->tris.bytes + s->shade.bytes + s->mats.bytes +
+                              s->env.bytes);
+  RET(configure_launches(s));
+  v.n_top = s->smem_nodes;
+  return LT_OK;
+}
+
+extern "C" int lt_scene_create(const lt_scene_desc *desc, int32_t device, lt_scene **out) {
+  if (!out) return lt_fail(LT_ERR_INVALID, "null output handle");
+  *out = nullptr;
+  RET(validate_desc(desc));
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return lt_fail(LT_ERR_CUDA, "no CUDA device available");
+  if (device < 0 || device >= ndev)
+    return lt_fail(LT_ERR_INVALID, "device %d out of range [0, %d)", device, ndev);
+  DeviceGuard g(device);
+  lt_scene *s = new lt_scene();
+  int rc = scene_create_impl(desc, device, s);
+  if (rc != LT_OK) {
+    std::string msg = g_last_error;
+    destroy_scene(s);
+    g_last_error = msg;
+    return rc;
+  }
+  *out = s;
+  return LT_OK;
+}
+
+extern "C" int lt_scene_destroy(lt_scene *scene) {
+  destroy_scene(scene);
+  return LT_OK;
+}
+
+extern "C" int lt_scene_info_get(const lt_scene *s, lt_scene_info *info) {
+  if (!s || !info) return lt_fail(LT_ERR_INVALID, "null argument");
+  info->device = s->device;
+  info->n_triangles = s->n_tris;
+  info->n_nodes = s->n_nodes;
+  info->n_internal = s->n_internal;
+  info->n_smem_nodes = s->smem_nodes;
+  info->device_bytes = s->device_bytes;
+  info->sm_count = s->sm_count;
+  return LT_OK;
+}
+
+// ------------------------------------------------------------------ workspace
+
+static int ensure_workspace(lt_scene *s, int64_t cap, int32_t max_depth) {
+  if (cap > s->cap) {
+    for (int k = 0; k < 2; ++k) {
+      RET(s->q_o[k].ensure(16 * cap));
+      RET(s->q_d[k].ensure(16 * cap));
+    }
+    RET(s->hits.ensure(16 * cap));
+    RET(s->T.ensure(16 * cap));
+    RET(s->L.ensure(16 * cap));
+    RET(s->rng.ensure(16 * cap));
+    s->cap = cap;
+  }
+  if (max_depth > s->depth_cap) {
+    RET(s->counters.ensure(sizeof(int32_t) * (2 * (size_t)max_depth + 2)));
+    s->depth_cap = max_depth;
+  }
+  RET(s->ray_ctr.ensure(3 * sizeof(unsigned long long)));
+  return LT_OK;
+}
+
+static PathArrays path_arrays(lt_scene *s) {
+  return PathArrays{s->T.as<float4>(), s->L.as<float4>(), s->rng.as<ulonglong2>()};
+}
+
+static int record_event(lt_scene *s, cudaStream_t st) {
+  if (s->ev_used == (int)s->ev_pool.size()) {
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    s->ev_pool.push_back(e);
+  }
+  CK(cudaEventRecord(s->ev_pool[s->ev_used++], st));
+  return LT_OK;
+}
+
+// The bounce loop of _trace (integrator.py:160-226) over the whole queue:
+// trace -> shade per segment; queue 0 must already hold the primary rays and
+// counters[0] their number.
+static int run_bounces(lt_scene *s, int32_t max_depth, int32_t rr_start, float t_min,
+                       uint32_t flags, cudaStream_t st) {
+  const bool smem = !(flags & LT_FLAG_NO_SMEM_TOP) && s->smem_nodes > 0;
+  SceneView sc = s->view;
+  sc.n_top = smem ? s->smem_nodes : 0;
+  int32_t *ctr = s->counters.as<int32_t>();
+  int32_t *fetch = ctr + max_depth + 1;
+  const PathArrays pa = path_arrays(s);
+  int cur = 0;
+  for (int32_t depth = 0; depth < max_depth; ++depth) {
+    if (flags & LT_FLAG_PROFILE) RET(record_event(s, st));
+    launch_trace(sc, smem, (flags & LT_FLAG_COUNT) != 0, s->trace_grid[smem ? 1 : 0],
+                 smem ? (size_t)s->smem_nodes * 64 : 0, s->q_o[cur].as<float4>(),
+                 s->q_d[cur].as<float4>(), ctr + depth, fetch + depth, s->hits.as<float4>(),
+                 s->ray_ctr.as<unsigned long long>(), st);
+    if (flags & LT_FLAG_PROFILE) RET(record_event(s, st));
+    ShadeArgs sa{depth, max_depth, rr_start, t_min};
+    launch_shade(sc, sa, pa, s->shade_grid, s->q_o[cur].as<float4>(), s->q_d[cur].as<float4>(),
+                 s->hits.as<float4>(), ctr + depth, s->q_o[cur ^ 1].as<float4>(),
+                 s->q_d[cur ^ 1].as<float4>(), ctr + depth + 1, st);
+    s->stats.kernel_launches += 2;
+    s->stats.trace_launches += 1;
+    cur ^= 1;
+  }
+  CK(cudaGetLastError());
+  return LT_OK;
+}
+
+static int validate_render(const lt_render_params *p) {
+  if (!p) return lt_fail(LT_ERR_INVALID, "null render params");
+  if (p->width < 1 || p->height < 1) return lt_fail(LT_ERR_INVALID, "image width and height must be >= 1");
+  if ((int64_t)p->width * p->height >= (int64_t(1) << 31))
+    return lt_fail(LT_ERR_INVALID, "image too large");
+  if (p->max_depth < 1) return lt_fail(LT_ERR_INVALID, "max_depth must be >= 1");
+  if (p->rr_start < 0) return lt_fail(LT_ERR_INVALID, "rr_start_depth must be >= 0");
+  if (p->sample_start < 0 || p->sample_count < 0)
+    return lt_fail(LT_ERR_INVALID, "sample range must be non-negative");
+  if (!(p->t_min > 0.0)) return lt_fail(LT_ERR_INVALID, "t_min must be positive");
+  if (p->n_ranks > 1 && (p->rank < 0 || p->rank >= p->n_ranks || p->tile_size < 1))
+    return lt_fail(LT_ERR_INVALID, "invalid sharding (rank %d of %d, tile %d)", p->rank,
+                   p->n_ranks, p->tile_size);
+  return LT_OK;
+}
+
+// local pixel list for interleaved tiles: tile k (raster order over
+// ceil(W/T) x ceil(H/T) tiles) belongs to rank k % n_ranks
+static int pixel_set(lt_scene *s, const lt_render_params *p, const int32_t **list, int64_t *n) {
+  if (p->n_ranks <= 1) {
+    *list = nullptr;
+    *n = (int64_t)p->width * p->height;
+    return LT_OK;
+  }
+  const int64_t key[5] = {p->width, p->height, p->tile_size, p->rank, p->n_ranks};
+  if (!std::equal(key, key + 5, s->pix_key)) {
+    const int64_t W = p->width, H = p->height, T = p->tile_size;
+    const int64_t ntx = (W + T - 1) / T, nty = (H + T - 1) / T;
+    std::vector<int32_t> pix;
+    for (int64_t tile = p->rank; tile < ntx * nty; tile += p->n_ranks) {
+      const int64_t ty = tile / ntx, tx = tile - ty * ntx;
+      for (int64_t y = ty * T; y < std::min(H, (ty + 1) * T); ++y)
+        for (int64_t x = tx * T; x < std::min(W, (tx + 1) * T); ++x)
+          pix.push_back((int32_t)(y * W + x));
+    }
+    RET(s->pix_list.ensure(std::max<size_t>(16, pix.size() * 4)));
+    if (!pix.empty())
+      CK(cudaMemcpy(s->pix_list.p, pix.data(), pix.size() * 4, cudaMemcpyHostToDevice));
+    std::copy(key, key + 5, s->pix_key);
+    s->pix_count = (int64_t)pix.size();
+  }
+  *list = s->pix_list.as<int32_t>();
+  *n = s->pix_count;
+  return LT_OK;
+}
+
+static int render_impl(lt_scene *s, const lt_render_params *p, float *accum, uint32_t *valid,
+                       uint32_t *invalid, cudaStream_t st) {
+  RET(validate_render(p));
+  if (!accum || !valid || !invalid) return lt_fail(LT_ERR_INVALID, "null accumulation buffer");
+  s->stats = lt_render_stats{};
+  s->ev_used = 0;
+  const int32_t *pix_list = nullptr;
+  int64_t n_local = 0;
+  RET(pixel_set(s, p, &pix_list, &n_local));
+  if (n_local == 0 || p->sample_count == 0) return LT_OK;
+  const int64_t B = p->max_batch_paths > 0 ? p->max_batch_paths : kDefaultBatchPaths;
+  const int64_t pix_chunk = std::min(n_local, B);
+  const int64_t spb = std::min<int64_t>(std::max<int64_t>(1, B / pix_chunk), p->sample_count);
+  RET(ensure_workspace(s, pix_chunk * spb, p->max_depth));
+  CK(cudaMemsetAsync(s->ray_ctr.p, 0, 3 * sizeof(unsigned long long), st));
+  const float t_min = (float)p->t_min;
+  const PathArrays pa = path_arrays(s);
+  int32_t *ctr = s->counters.as<int32_t>();
+  for (int64_t s0 = 0; s0 < p->sample_count; s0 += spb) {
+    const int64_t ns = std::min(spb, p->sample_count - s0);
+    for (int64_t pc0 = 0; pc0 < n_local; pc0 += pix_chunk) {
+      const int64_t np = std::min(pix_chunk, n_local - pc0);
+      CK(cudaMemsetAsync(ctr, 0, sizeof(int32_t) * (2 * (size_t)p->max_depth + 2), st));
+      RaygenArgs ra{};
+      std::memcpy(ra.cam, p->camera, sizeof(ra.cam));
+      ra.width = p->width;
+      ra.height = p->height;
+      ra.seed = p->seed;
+      ra.sample_base = p->sample_start + s0;
+      ra.n_pix = np;
+      ra.pix_offset = pc0;
+      ra.pix_list = pix_list;
+      ra.n_paths = np * ns;
+      ra.t_min = t_min;
+      launch_raygen(ra, pa, s->q_o[0].as<float4>(), s->q_d[0].as<float4>(), ctr, st);
+      RET(run_bounces(s, p->max_depth, p->rr_start, t_min, p->flags, st));
+      AccumArgs aa{np, pc0, ns, pix_list};
+      launch_accumulate(aa, s->L.as<float4>(), accum, valid, invalid, st);
+      s->stats.kernel_launches += 2;
+      s->stats.batches += 1;
+      s->stats.paths += np * ns;
+    }
+  }
+  CK(cudaGetLastError());
+  return LT_OK;
+}
+
+extern "C" int lt_render_pass(lt_scene *s, const lt_render_params *params, float *accum_sum,
+                              uint32_t *valid, uint32_t *invalid, void *stream) {
+  if (!s) return lt_fail(LT_ERR_INVALID, "null scene");
+  DeviceGuard g(s->device);
+  return render_impl(s, params, accum_sum, valid, invalid, (cudaStream_t)stream);
+}
+
+extern "C" int lt_render_stats_get(const lt_scene *cs, lt_render_stats *out) {
+  if (!cs || !out) return lt_fail(LT_ERR_INVALID, "null argument");
+  lt_scene *s = const_cast<lt_scene *>(cs);
+  DeviceGuard g(s->device);
+  if (s->ray_ctr.p) {
+    unsigned long long c[3] = {0, 0, 0};
+    CK(cudaMemcpy(c, s->ray_ctr.p, sizeof(c), cudaMemcpyDeviceToHost));
+    s->stats.rays = (int64_t)c[0];
+    s->stats.slab_tests = (int64_t)c[1];
+    s->stats.tri_tests = (int64_t)c[2];
+  }
+  double ms = 0.0;
+  for (int i = 0; i + 1 < s->ev_used; i += 2) {
+    CK(cudaEventSynchronize(s->ev_pool[i + 1]));
+    float e = 0.f;
+    CK(cudaEventElapsedTime(&e, s->ev_pool[i], s->ev_pool[i + 1]));
+    ms += e;
+  }
+  s->stats.trace_ms = ms;
+  *out = s->stats;
+  return LT_OK;
+}
+
+extern "C" int lt_render_pass_host(lt_scene *s, const lt_render_params *p, double *accum_mean,
+                                   int64_t *valid, int64_t *invalid) {
+  if (!s) return lt_fail(LT_ERR_INVALID, "null scene");
+  RET(validate_render(p));
+  if (!accum_mean || !valid || !invalid) return lt_fail(LT_ERR_INVALID, "null output buffer");
+  DeviceGuard g(s->device);
+  const int64_t npx = (int64_t)p->width * p->height;
+  RET(s->s_a.ensure(12 * npx));
+  RET(s->s_b.ensure(4 * npx));
+  RET(s->s_c.ensure(4 * npx));
+  cudaStream_t st = s->stream;
+  CK(cudaMemsetAsync(s->s_a.p, 0, 12 * npx, st));
+  CK(cudaMemsetAsync(s->s_b.p, 0, 4 * npx, st));
+  CK(cudaMemsetAsync(s->s_c.p, 0, 4 * npx, st));
+  RET(render_impl(s, p, s->s_a.as<float>(), s->s_b.as<uint32_t>(), s->s_c.as<uint32_t>(), st));
+  RET(s->h_stage.ensure(20 * npx));
+  float *h_sum = s->h_stage.as<float>();
+  uint32_t *h_valid = reinterpret_cast<uint32_t *>(h_sum + 3 * npx);
+  uint32_t *h_invalid = h_valid + npx;
+  CK(cudaMemcpyAsync(h_sum, s->s_a.p, 12 * npx, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(h_valid, s->s_b.p, 4 * npx, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(h_invalid, s->s_c.p, 4 * npx, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  // fold the new samples into the running means (integrator.py:266-270)
+  for (int64_t i = 0; i < npx; ++i) {
+    const uint32_t v = h_valid[i];
+    if (v) {
+      const int64_t n = valid[i] + v;
+      for (int c = 0; c < 3; ++c) {
+        const double m = accum_mean[3 * i + c];
+        accum_mean[3 * i + c] = m + ((double)h_sum[3 * i + c] - (double)v * m) / (double)n;
+      }
+      valid[i] = n;
+    }
+    invalid[i] += h_invalid[i];
+  }
+  return LT_OK;
+}
+
+// ------------------------------------------------------------------ ray queries
+
+static int intersect_common(lt_scene *s, int64_t n, cudaStream_t st, bool count,
+                            int32_t **nodes, int32_t **tests) {
+  RET(s->s_d.ensure(std::max<int64_t>(16, 16 * n)));
+  RET(s->s_e.ensure(std::max<int64_t>(16, 16 * n)));
+  RET(s->s_f.ensure(std::max<int64_t>(16, 16 * n)));
+  if (count) {
+    RET(s->s_b.ensure(std::max<int64_t>(16, 4 * n)));
+    RET(s->s_c.ensure(std::max<int64_t>(16, 4 * n)));
+    *nodes = s->s_b.as<int32_t>();
+    *tests = s->s_c.as<int32_t>();
+  }
+  launch_trace_rays(s->view, s->s_d.as<float4>(), s->s_e.as<float4>(), n, s->s_f.as<float4>(),
+                    count ? *nodes : nullptr, count ? *tests : nullptr, st);
+  CK(cudaGetLastError());
+  return LT_OK;
+}
+
+extern "C" int lt_intersect_batch(lt_scene *s, const float *origins, const float *dirs, int64_t n,
+                                  float t_min, float t_max, int32_t *idx, float *t, void *stream) {
+  if (!s || n < 0) return lt_fail(LT_ERR_INVALID, "invalid arguments");
+  if (n == 0) return LT_OK;
+  if (!origins || !dirs || !idx || !t) return lt_fail(LT_ERR_INVALID, "null ray buffer");
+  DeviceGuard g(s->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  RET(s->s_d.ensure(16 * n));
+  RET(s->s_e.ensure(16 * n));
+  launch_pack_rays_f32(origins, dirs, n, t_min, t_max, s->s_d.as<float4>(), s->s_e.as<float4>(),
+                       st);
+  RET(intersect_common(s, n, st, false, nullptr, nullptr));
+  launch_unpack_hits(s->view, s->s_f.as<float4>(), n, idx, t, nullptr, nullptr, st);
+  CK(cudaGetLastError());
+  return LT_OK;
+}
+
+static int upload_rays_f64(lt_scene *s, const double *o, const double *d, int64_t n,
+                           double t_min, double t_max, cudaStream_t st) {
+  RET(s->s_a.ensure(48 * n));
+  double *dev = s->s_a.as<double>();
+  CK(cudaMemcpyAsync(dev, o, 24 * n, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(dev + 3 * n, d, 24 * n, cudaMemcpyHostToDevice, st));
+  RET(s->s_d.ensure(16 * n));
+  RET(s->s_e.ensure(16 * n));
+  const float fmax = (float)t_max;  // +inf stays +inf
+  launch_pack_rays_f64(dev, dev + 3 * n, n, (float)t_min, fmax, s->s_d.as<float4>(),
+                       s->s_e.as<float4>(), st);
+  return LT_OK;
+}
+
+extern "C" int lt_intersect_batch_host(lt_scene *s, const double *origins, const double *dirs,
+                                       int64_t n, double t_min, double t_max, int64_t *idx,
+                                       double *t) {
+  if (!s || n < 0) return lt_fail(LT_ERR_INVALID, "invalid arguments");
+  if (n == 0) return LT_OK;
+  if (!origins || !dirs || !idx || !t) return lt_fail(LT_ERR_INVALID, "null ray buffer");
+  DeviceGuard g(s->device);
+  cudaStream_t st = s->stream;
+  RET(upload_rays_f64(s, origins, dirs, n, t_min, t_max, st));
+  RET(intersect_common(s, n, st, false, nullptr, nullptr));
+  RET(s->s_a.ensure(16 * n));
+  int64_t *d_idx = s->s_a.as<int64_t>();
+  double *d_t = reinterpret_cast<double *>(d_idx + n);
+  launch_unpack_hits(s->view, s->s_f.as<float4>(), n, nullptr, nullptr, d_idx, d_t, st);
+  CK(cudaMemcpyAsync(idx, d_idx, 8 * n, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(t, d_t, 8 * n, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return LT_OK;
+}
+
+extern "C" int lt_traversal_counts_host(lt_scene *s, const double *origins, const double *dirs,
+                                        int64_t n, double t_min, double t_max, int64_t *nodes,
+                                        int64_t *tests) {
+  if (!s || n < 0) return lt_fail(LT_ERR_INVALID, "invalid arguments");
+  if (n == 0) return LT_OK;
+  if (!origins || !dirs || !nodes || !tests) return lt_fail(LT_ERR_INVALID, "null buffer");
+  DeviceGuard g(s->device);
+  cudaStream_t st = s->stream;
+  RET(upload_rays_f64(s, origins, dirs, n, t_min, t_max, st));
+  int32_t *d_nodes = nullptr, *d_tests = nullptr;
+  RET(intersect_common(s, n, st, true, &d_nodes, &d_tests));
+  std::vector<int32_t> hn(n), ht(n);
+  CK(cudaMemcpyAsync(hn.data(), d_nodes, 4 * n, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(ht.data(), d_tests, 4 * n, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  for (int64_t i = 0; i < n; ++i) {
+    nodes[i] = hn[i];
+    tests[i] = ht[i];
+  }
+  return LT_OK;
+}
+
+extern "C" int lt_trace_paths_host(lt_scene *s, const double *origins, const double *dirs,
+                                   const uint64_t *state, const uint64_t *inc, int64_t n,
+                                   int32_t max_depth, int32_t rr_start, double t_min, double *rgb,
+                                   uint64_t *state_out) {
+  if (!s || n < 0) return lt_fail(LT_ERR_INVALID, "invalid arguments");
+  if (n == 0) return LT_OK;
+  if (!origins || !dirs || !state || !inc || !rgb || !state_out)
+    return lt_fail(LT_ERR_INVALID, "null buffer");
+  if (max_depth < 1) return lt_fail(LT_ERR_INVALID, "max_depth must be >= 1");
+  if (rr_start < 0) return lt_fail(LT_ERR_INVALID, "rr_start_depth must be >= 0");
+  if (!(t_min > 0.0)) return lt_fail(LT_ERR_INVALID, "t_min must be positive");
+  if (n >= (int64_t(1) << 31)) return lt_fail(LT_ERR_INVALID, "too many paths");
+  DeviceGuard g(s->device);
+  cudaStream_t st = s->stream;
+  s->stats = lt_render_stats{};
+  s->ev_used = 0;
+  RET(ensure_workspace(s, n, max_depth));
+  RET(s->s_a.ensure(64 * n));
+  double *d_o = s->s_a.as<double>();
+  double *d_d = d_o + 3 * n;
+  uint64_t *d_state = reinterpret_cast<uint64_t *>(d_d + 3 * n);
+  uint64_t *d_inc = d_state + n;
+  CK(cudaMemcpyAsync(d_o, origins, 24 * n, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_d, dirs, 24 * n, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_state, state, 8 * n, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_inc, inc, 8 * n, cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(s->counters.p, 0, sizeof(int32_t) * (2 * (size_t)max_depth + 2), st));
+  CK(cudaMemsetAsync(s->ray_ctr.p, 0, 3 * sizeof(unsigned long long), st));
+  const PathArrays pa = path_arrays(s);
+  launch_raygen_explicit(d_o, d_d, d_state, d_inc, n, (float)t_min, pa, s->q_o[0].as<float4>(),
+                         s->q_d[0].as<float4>(), s->counters.as<int32_t>(), st);
+  RET(run_bounces(s, max_depth, rr_start, (float)t_min, 0u, st));
+  RET(s->s_b.ensure(32 * n));
+  double *d_rgb = s->s_b.as<double>();
+  uint64_t *d_sout = reinterpret_cast<uint64_t *>(d_rgb + 3 * n);
+  launch_gather_explicit(pa, n, d_rgb, d_sout, st);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(rgb, d_rgb, 24 * n, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(state_out, d_sout, 8 * n, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return LT_OK;
+}
+
+extern "C" int lt_tonemap_u8(const float *linear, int64_t n_pixels, uint8_t *out, void *stream) {
+  if (n_pixels < 0 || (n_pixels > 0 && (!linear || !out)))
+    return lt_fail(LT_ERR_INVALID, "invalid tonemap arguments");
+  launch_tonemap_u8(linear, n_pixels, out, (cudaStream_t)stream);
+  CK(cudaGetLastError());
+  return LT_OK;
+}

@@ -1,0 +1,511 @@
+// lt_kernels.cu -- the wavefront pipeline kernels and the scene flattening.
+//
+// One render batch = raygen -> max_depth x (trace -> shade) -> accumulate.
+// Queues are device-resident; every kernel reads its queue length from
+// device memory, so a whole batch is issued without a host round trip.
+#include <cstdint>
+
+#include "lt_kernels.h"
+#include "lt_material.cuh"
+#include "lt_traverse.cuh"
+
+namespace lt {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+// ------------------------------------------------------------------ flatten
+
+// Node records from the host BVH (bvh.py:38-50): boxes rounded outward to
+// fp32 (the float64 pad of 1e-7*extent is below fp32 resolution), links
+// renumbered; leaves become ~first_triangle.
+__global__ void k_flatten_nodes(const double *__restrict__ bmin, const double *__restrict__ bmax,
+                                const int32_t *__restrict__ left,
+                                const int32_t *__restrict__ right,
+                                const int32_t *__restrict__ first,
+                                const int32_t *__restrict__ count,
+                                const int32_t *__restrict__ perm,
+                                const int32_t *__restrict__ new_index, int64_t n_internal,
+                                float4 *__restrict__ out) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n_internal) return;
+  const int32_t old = perm[i];
+  const int32_t ch[2] = {left[old], right[old]};
+  float lo[2][3], hi[2][3];
+  int32_t link[2];
+  for (int c = 0; c < 2; ++c) {
+    const int32_t x = ch[c];
+    for (int a = 0; a < 3; ++a) {
+      lo[c][a] = __double2float_rd(bmin[3 * (int64_t)x + a]);
+      hi[c][a] = __double2float_ru(bmax[3 * (int64_t)x + a]);
+    }
+    link[c] = count[x] > 0 ? ~first[x] : new_index[x];
+  }
+  out[4 * i + 0] = make_float4(lo[0][0], hi[0][0], lo[0][1], hi[0][1]);
+  out[4 * i + 1] = make_float4(lo[1][0], hi[1][0], lo[1][1], hi[1][1]);
+  out[4 * i + 2] = make_float4(lo[0][2], hi[0][2], lo[1][2], hi[1][2]);
+  out[4 * i + 3] = make_float4(__int_as_float(link[0]), __int_as_float(link[1]), 0.f, 0.f);
+}
+
+// Triangles in leaf order k (triangle_order[k]); e1/e2 from float64
+// differences rounded once; shading normals + material index alongside.
+__global__ void k_flatten_tris(const double *__restrict__ v0, const double *__restrict__ v1,
+                               const double *__restrict__ v2, const double *__restrict__ n0,
+                               const double *__restrict__ n1, const double *__restrict__ n2,
+                               const int32_t *__restrict__ mat_index,
+                               const int32_t *__restrict__ order,
+                               const uint8_t *__restrict__ leaf_end, int64_t n,
+                               float4 *__restrict__ tris, float4 *__restrict__ shade) {
+  int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int64_t ti = order[k];
+  const double *a = v0 + 3 * ti, *b = v1 + 3 * ti, *c = v2 + 3 * ti;
+  tris[3 * k + 0] = make_float4((float)a[0], (float)a[1], (float)a[2], __int_as_float((int)ti));
+  tris[3 * k + 1] = make_float4((float)(b[0] - a[0]), (float)(b[1] - a[1]), (float)(b[2] - a[2]),
+                                __int_as_float(leaf_end[k] ? 1 : 0));
+  tris[3 * k + 2] =
+      make_float4((float)(c[0] - a[0]), (float)(c[1] - a[1]), (float)(c[2] - a[2]), 0.f);
+  const double *p0 = n0 + 3 * ti, *p1 = n1 + 3 * ti, *p2 = n2 + 3 * ti;
+  shade[3 * k + 0] =
+      make_float4((float)p0[0], (float)p0[1], (float)p0[2], __int_as_float(mat_index[ti]));
+  shade[3 * k + 1] = make_float4((float)p1[0], (float)p1[1], (float)p1[2], 0.f);
+  shade[3 * k + 2] = make_float4((float)p2[0], (float)p2[1], (float)p2[2], 0.f);
+}
+
+// ------------------------------------------------------------------ raygen
+
+// Primary rays for paths p = s_local * n_pix + i (sample-major), keyed by the
+// GLOBAL pixel index and sample index (integrator.py:253-258).
+__global__ void k_raygen(RaygenArgs ra, PathArrays pa, float4 *__restrict__ q_o,
+                         float4 *__restrict__ q_d, int32_t *__restrict__ count0) {
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p == 0) *count0 = (int32_t)ra.n_paths;
+  if (p >= ra.n_paths) return;
+  const int64_t s_local = p / ra.n_pix;
+  const int64_t i = p - s_local * ra.n_pix;
+  const int64_t pix = ra.pix_list ? (int64_t)ra.pix_list[ra.pix_offset + i] : ra.pix_offset + i;
+  const int64_t sample = ra.sample_base + s_local;
+  const int64_t py = pix / ra.width;
+  const int64_t px = pix - py * ra.width;
+  uint64_t state, inc;
+  seed_stream((uint64_t)pix, (uint64_t)sample, ra.seed, state, inc);
+  const double jx = unit_f64(state, inc);
+  const double jy = unit_f64(state, inc);
+  const f3 d = camera_dir(ra.cam, (double)px, (double)py, jx, jy, ra.width, ra.height);
+  q_o[p] = make_float4((float)ra.cam[0], (float)ra.cam[1], (float)ra.cam[2],
+                       __int_as_float((int32_t)p));
+  q_d[p] = make_float4(d.x, d.y, d.z, ra.t_min);
+  pa.T[p] = make_float4(1.f, 1.f, 1.f, 0.f);
+  pa.L[p] = make_float4(0.f, 0.f, 0.f, 0.f);
+  pa.rng[p] = make_ulonglong2(state, inc);
+}
+
+// Explicit rays with caller-supplied PCG state (trace_radiance,
+// integrator.py:294-307).
+__global__ void k_raygen_explicit(const double *__restrict__ o, const double *__restrict__ d,
+                                  const uint64_t *__restrict__ state,
+                                  const uint64_t *__restrict__ inc, int64_t n, float t_min,
+                                  PathArrays pa,
+                                  float4 *__restrict__ q_o, float4 *__restrict__ q_d,
+                                  int32_t *__restrict__ count0) {
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p == 0) *count0 = (int32_t)n;
+  if (p >= n) return;
+  q_o[p] = make_float4((float)o[3 * p], (float)o[3 * p + 1], (float)o[3 * p + 2],
+                       __int_as_float((int32_t)p));
+  q_d[p] = make_float4((float)d[3 * p], (float)d[3 * p + 1], (float)d[3 * p + 2], t_min);
+  pa.T[p] = make_float4(1.f, 1.f, 1.f, 0.f);
+  pa.L[p] = make_float4(0.f, 0.f, 0.f, 0.f);
+  pa.rng[p] = make_ulonglong2(state[p], inc[p]);
+}
+
+__global__ void k_gather_explicit(PathArrays pa, int64_t n, double *__restrict__ rgb,
+                                  uint64_t *__restrict__ state_out) {
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const float4 L = pa.L[p];
+  rgb[3 * p + 0] = L.x;
+  rgb[3 * p + 1] = L.y;
+  rgb[3 * p + 2] = L.z;
+  state_out[p] = pa.rng[p].x;
+}
+
+// ------------------------------------------------------------------ trace
+
+// Persistent closest-hit kernel: one CTA per resident slot, warps fetch 32
+// queue entries at a time from a device counter (load balance across the
+// divergent ray population); the top BVH levels are staged in shared memory.
+// ray_ctr[0] += queue length; with COUNT also ray_ctr[1] += slab tests and
+// ray_ctr[2] += triangle tests (warp-reduced, one atomic per warp per fetch).
+template <bool USE_SMEM, bool COUNT>
+__global__ void __launch_bounds__(kTraceThreads)
+    k_trace(SceneView sc, const float4 *__restrict__ q_o, const float4 *__restrict__ q_d,
+            const int32_t *__restrict__ count, int32_t *__restrict__ fetch,
+            float4 *__restrict__ hits, unsigned long long *__restrict__ ray_ctr) {
+  extern __shared__ float4 s_top[];
+  if (USE_SMEM) {
+    const int n4 = 4 * sc.n_top;
+    for (int j = threadIdx.x; j < n4; j += blockDim.x) s_top[j] = __ldg(&sc.nodes[j]);
+    __syncthreads();
+  }
+  const int n = *count;
+  if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(ray_ctr, (unsigned long long)n);
+  const int lane = threadIdx.x & 31;
+  while (true) {
+    int base = 0;
+    if (lane == 0) base = atomicAdd(fetch, 32);
+    base = __shfl_sync(kFull, base, 0);
+    if (base >= n) break;
+    const int q = base + lane;
+    int nn = 0, nt = 0;
+    if (q < n) {
+      const float4 ro = q_o[q];
+      const float4 rd = q_d[q];
+      const HitRec h = traverse<USE_SMEM, COUNT>(sc, s_top, mk(ro.x, ro.y, ro.z),
+                                                mk(rd.x, rd.y, rd.z), rd.w,
+                                                __int_as_float(0x7f800000), &nn, &nt);
+      hits[q] = make_float4(h.t, h.u, h.v, __int_as_float(h.k));
+    }
+    if (COUNT) {
+      for (int off = 16; off > 0; off >>= 1) {
+        nn += __shfl_down_sync(kFull, nn, off);
+        nt += __shfl_down_sync(kFull, nt, off);
+      }
+      if (lane == 0) {
+        atomicAdd(ray_ctr + 1, (unsigned long long)nn);
+        atomicAdd(ray_ctr + 2, (unsigned long long)nt);
+      }
+    }
+  }
+}
+
+// Arbitrary rays (intersect_scene_batch): ray (o, d), t_min in q_d.w,
+// t_max in q_o.w.  Optionally counts work per ray (traversal_counts_batch).
+template <bool COUNT>
+__global__ void __launch_bounds__(kTraceThreads)
+    k_trace_rays(SceneView sc, const float4 *__restrict__ q_o, const float4 *__restrict__ q_d,
+                 int64_t n, float4 *__restrict__ hits, int32_t *__restrict__ nodes,
+                 int32_t *__restrict__ tests) {
+  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= n) return;
+  const float4 ro = q_o[q];
+  const float4 rd = q_d[q];
+  int nn = 0, nt = 0;
+  const HitRec h = traverse<false, COUNT>(sc, nullptr, mk(ro.x, ro.y, ro.z), mk(rd.x, rd.y, rd.z),
+                                          rd.w, ro.w, &nn, &nt);
+  hits[q] = make_float4(h.t, h.u, h.v, __int_as_float(h.k));
+  if (COUNT) {
+    nodes[q] = nn;
+    tests[q] = nt;
+  }
+}
+
+// ------------------------------------------------------------------ shade
+
+// One bounce of _trace (integrator.py:160-226) for every queued path:
+// miss -> environment; hit -> emission; final segment stops; otherwise hit
+// frame, 3 draws, BSDF sample, throughput, Russian roulette (4th draw), and
+// the continuation ray is appended to the next queue (warp ballot +
+// one atomic per warp).
+__global__ void __launch_bounds__(kShadeThreads)
+    k_shade(SceneView sc, ShadeArgs sa, PathArrays pa, const float4 *__restrict__ q_o,
+            const float4 *__restrict__ q_d, const float4 *__restrict__ hits,
+            const int32_t *__restrict__ count_in, float4 *__restrict__ n_o,
+            float4 *__restrict__ n_d, int32_t *__restrict__ count_out) {
+  const int n = *count_in;
+  const int lane = threadIdx.x & 31;
+  for (int base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
+    const int q = base + threadIdx.x;
+    bool emit = false;
+    float4 out_o, out_d;
+    if (q < n) {
+      const float4 ro = q_o[q];
+      const float4 rd = q_d[q];
+      const float4 h = hits[q];
+      const int32_t p = __float_as_int(ro.w);
+      const int32_t k = __float_as_int(h.w);
+      const f3 d = mk(rd.x, rd.y, rd.z);
+      const float4 T = pa.T[p];
+      float4 L = pa.L[p];
+      if (k < 0) {
+        const f3 e = env_radiance(sc, d);
+        L.x += T.x * e.x;
+        L.y += T.y * e.y;
+        L.z += T.z * e.z;
+        pa.L[p] = L;
+      } else {
+        const float4 s0 = __ldg(&sc.shade[3 * (int64_t)k]);
+        const int32_t mi = __float_as_int(s0.w);
+        const GpuMaterial &mt = sc.mats[mi];
+        if (mt.flags & MAT_EMISSIVE) {
+          L.x += T.x * mt.el * mt.ec[0];
+          L.y += T.y * mt.el * mt.ec[1];
+          L.z += T.z * mt.el * mt.ec[2];
+          pa.L[p] = L;
+        }
+        if (sa.depth != sa.max_depth - 1) {
+          const float4 e1 = __ldg(&sc.tris[3 * (int64_t)k + 1]);
+          const float4 e2 = __ldg(&sc.tris[3 * (int64_t)k + 2]);
+          const float4 s1 = __ldg(&sc.shade[3 * (int64_t)k + 1]);
+          const float4 s2 = __ldg(&sc.shade[3 * (int64_t)k + 2]);
+          f3 g, sn;
+          bool front;
+          hit_frame(d, mk(e1.x, e1.y, e1.z), mk(e2.x, e2.y, e2.z), mk(s0.x, s0.y, s0.z),
+                    mk(s1.x, s1.y, s1.z), mk(s2.x, s2.y, s2.z), h.y, h.z, g, sn, front);
+          ulonglong2 rs = pa.rng[p];
+          uint64_t state = rs.x;
+          const uint64_t inc = rs.y;
+          const float u_lobe = unit_f32(state, inc);
+          const float u1 = unit_f32(state, inc);
+          const float u2 = unit_f32(state, inc);
+          f3 wi, w;
+          bool alive = sample_material(-d, sn, mt, front, u_lobe, u1, u2, wi, w);
+          float4 Tn = T;
+          if (alive) {
+            Tn.x *= w.x;
+            Tn.y *= w.y;
+            Tn.z *= w.z;
+            if (Tn.x <= 0.f && Tn.y <= 0.f && Tn.z <= 0.f) alive = false;
+          }
+          if (alive && sa.depth >= sa.rr_start) {
+            float pr = fmaxf(fmaxf(Tn.x, Tn.y), Tn.z);
+            pr = fminf(fmaxf(pr, LT_RR_MIN_F), 1.f);
+            const float u_rr = unit_f32(state, inc);
+            if (u_rr >= pr) {
+              alive = false;
+            } else {
+              Tn.x /= pr;
+              Tn.y /= pr;
+              Tn.z /= pr;
+            }
+          }
+          pa.rng[p].x = state;
+          if (alive) {
+            pa.T[p] = Tn;
+            const float t = h.x;
+            out_o = make_float4(ro.x + t * d.x, ro.y + t * d.y, ro.z + t * d.z, ro.w);
+            out_d = make_float4(wi.x, wi.y, wi.z, sa.t_min);
+            emit = true;
+          }
+        }
+      }
+    }
+    // warp-aggregated append to the next queue
+    const unsigned mask = __ballot_sync(kFull, emit);
+    if (mask) {
+      const int leader = __ffs(mask) - 1;
+      int slot0 = 0;
+      if (lane == leader) slot0 = atomicAdd(count_out, __popc(mask));
+      slot0 = __shfl_sync(kFull, slot0, leader);
+      if (emit) {
+        const int slot = slot0 + __popc(mask & ((1u << lane) - 1u));
+        n_o[slot] = out_o;
+        n_d[slot] = out_d;
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ accumulate
+
+// Per-pixel sum of the batch's finite samples in sample order, plus valid /
+// invalid counts (integrator.py:266-272; the mean is sum / valid).
+__global__ void k_accumulate(AccumArgs aa, const float4 *__restrict__ L,
+                             float *__restrict__ accum, uint32_t *__restrict__ valid,
+                             uint32_t *__restrict__ invalid) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= aa.n_pix) return;
+  const int64_t pix =
+      aa.pix_list ? (int64_t)aa.pix_list[aa.pix_offset + i] : aa.pix_offset + i;
+  float r = accum[3 * pix + 0], g = accum[3 * pix + 1], b = accum[3 * pix + 2];
+  uint32_t nv = valid[pix], ni = invalid[pix];
+  for (int64_t s = 0; s < aa.n_samples; ++s) {
+    const float4 x = L[s * aa.n_pix + i];
+    if (isfinite(x.x) && isfinite(x.y) && isfinite(x.z)) {
+      r += x.x;
+      g += x.y;
+      b += x.z;
+      ++nv;
+    } else {
+      ++ni;
+    }
+  }
+  accum[3 * pix + 0] = r;
+  accum[3 * pix + 1] = g;
+  accum[3 * pix + 2] = b;
+  valid[pix] = nv;
+  invalid[pix] = ni;
+}
+
+// ------------------------------------------------------------------ ray I/O
+
+__global__ void k_pack_rays_f32(const float *__restrict__ o, const float *__restrict__ d,
+                                int64_t n, float t_min, float t_max, float4 *__restrict__ q_o,
+                                float4 *__restrict__ q_d) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  q_o[i] = make_float4(o[3 * i], o[3 * i + 1], o[3 * i + 2], t_max);
+  q_d[i] = make_float4(d[3 * i], d[3 * i + 1], d[3 * i + 2], t_min);
+}
+
+__global__ void k_pack_rays_f64(const double *__restrict__ o, const double *__restrict__ d,
+                                int64_t n, float t_min, float t_max, float4 *__restrict__ q_o,
+                                float4 *__restrict__ q_d) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  q_o[i] = make_float4((float)o[3 * i], (float)o[3 * i + 1], (float)o[3 * i + 2], t_max);
+  q_d[i] = make_float4((float)d[3 * i], (float)d[3 * i + 1], (float)d[3 * i + 2], t_min);
+}
+
+__global__ void k_unpack_hits(SceneView sc, const float4 *__restrict__ hits, int64_t n,
+                              int32_t *__restrict__ idx32, float *__restrict__ t32,
+                              int64_t *__restrict__ idx64, double *__restrict__ t64) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float4 h = hits[i];
+  const int32_t k = __float_as_int(h.w);
+  const int32_t orig = k >= 0 ? __float_as_int(__ldg(&sc.tris[3 * (int64_t)k]).w) : -1;
+  const float t = k >= 0 ? h.x : __int_as_float(0x7f800000);
+  if (idx32) idx32[i] = orig;
+  if (t32) t32[i] = t;
+  if (idx64) idx64[i] = orig;
+  if (t64) t64[i] = (double)t;
+}
+
+// ------------------------------------------------------------------ display
+
+// tonemap.py:18-61 (PBR Neutral -> sRGB -> half-up u8), float64 arithmetic
+__global__ void k_tonemap_u8(const float *__restrict__ lin, int64_t n_pixels,
+                             uint8_t *__restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n_pixels) return;
+  const double kStart = 0.8 - 0.04, kDesat = 0.15;
+  double c[3] = {lin[3 * i], lin[3 * i + 1], lin[3 * i + 2]};
+  const double x = fmin(c[0], fmin(c[1], c[2]));
+  const double offset = x < 0.08 ? x - 6.25 * x * x : 0.04;
+  for (int k = 0; k < 3; ++k) c[k] -= offset;
+  const double peak = fmax(c[0], fmax(c[1], c[2]));
+  const double dd = 1.0 - kStart;
+  const double new_peak = 1.0 - dd * dd / (peak + dd - kStart);
+  const bool compress = peak > kStart;
+  const double gg = compress ? 1.0 - 1.0 / (kDesat * (peak - new_peak) + 1.0) : 0.0;
+  for (int k = 0; k < 3; ++k) {
+    double v = c[k];
+    if (compress) v = (v * (new_peak / peak)) * (1.0 - gg) + new_peak * gg;
+    v = fmin(fmax(v, 0.0), 1.0);
+    v = v <= 0.0031308 ? 12.92 * v : 1.055 * pow(v, 1.0 / 2.4) - 0.055;
+    v = floor(255.0 * fmin(fmax(v, 0.0), 1.0) + 0.5);
+    out[3 * i + k] = (uint8_t)v;
+  }
+}
+
+// ------------------------------------------------------------------ launchers
+
+const void *trace_kernel_ptr(bool smem, bool count) {
+  if (count) return smem ? (const void *)k_trace<true, true> : (const void *)k_trace<false, true>;
+  return smem ? (const void *)k_trace<true, false> : (const void *)k_trace<false, false>;
+}
+const void *shade_kernel_ptr() { return (const void *)k_shade; }
+
+void launch_flatten_nodes(const double *bmin, const double *bmax, const int32_t *left,
+                          const int32_t *right, const int32_t *first, const int32_t *count,
+                          const int32_t *perm, const int32_t *new_index, int64_t n_internal,
+                          float4 *out, cudaStream_t st) {
+  if (n_internal <= 0) return;
+  k_flatten_nodes<<<(unsigned)((n_internal + 255) / 256), 256, 0, st>>>(
+      bmin, bmax, left, right, first, count, perm, new_index, n_internal, out);
+}
+
+void launch_flatten_tris(const double *v0, const double *v1, const double *v2, const double *n0,
+                         const double *n1, const double *n2, const int32_t *mat_index,
+                         const int32_t *order, const uint8_t *leaf_end, int64_t n, float4 *tris,
+                         float4 *shade, cudaStream_t st) {
+  k_flatten_tris<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(v0, v1, v2, n0, n1, n2, mat_index,
+                                                              order, leaf_end, n, tris, shade);
+}
+
+void launch_raygen(const RaygenArgs &ra, const PathArrays &pa, float4 *q_o, float4 *q_d,
+                   int32_t *count0, cudaStream_t st) {
+  const int64_t n = ra.n_paths > 0 ? ra.n_paths : 1;
+  k_raygen<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(ra, pa, q_o, q_d, count0);
+}
+
+void launch_raygen_explicit(const double *o, const double *d, const uint64_t *state,
+                            const uint64_t *inc, int64_t n, float t_min, const PathArrays &pa,
+                            float4 *q_o, float4 *q_d, int32_t *count0, cudaStream_t st) {
+  const int64_t m = n > 0 ? n : 1;
+  k_raygen_explicit<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(o, d, state, inc, n, t_min, pa,
+                                                                 q_o, q_d, count0);
+}
+
+void launch_gather_explicit(const PathArrays &pa, int64_t n, double *rgb, uint64_t *state_out,
+                            cudaStream_t st) {
+  if (n <= 0) return;
+  k_gather_explicit<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(pa, n, rgb, state_out);
+}
+
+void launch_trace(const SceneView &sc, bool smem, bool count_work, int grid, size_t smem_bytes,
+                  const float4 *q_o, const float4 *q_d, const int32_t *count, int32_t *fetch,
+                  float4 *hits, unsigned long long *ray_ctr, cudaStream_t st) {
+  const size_t sm = smem ? smem_bytes : 0;
+  if (smem && count_work)
+    k_trace<true, true><<<grid, kTraceThreads, sm, st>>>(sc, q_o, q_d, count, fetch, hits,
+                                                         ray_ctr);
+  else if (smem)
+    k_trace<true, false><<<grid, kTraceThreads, sm, st>>>(sc, q_o, q_d, count, fetch, hits,
+                                                          ray_ctr);
+  else if (count_work)
+    k_trace<false, true><<<grid, kTraceThreads, 0, st>>>(sc, q_o, q_d, count, fetch, hits,
+                                                         ray_ctr);
+  else
+    k_trace<false, false><<<grid, kTraceThreads, 0, st>>>(sc, q_o, q_d, count, fetch, hits,
+                                                          ray_ctr);
+}
+
+void launch_trace_rays(const SceneView &sc, const float4 *q_o, const float4 *q_d, int64_t n,
+                       float4 *hits, int32_t *nodes, int32_t *tests, cudaStream_t st) {
+  if (n <= 0) return;
+  const unsigned grid = (unsigned)((n + kTraceThreads - 1) / kTraceThreads);
+  if (nodes)
+    k_trace_rays<true><<<grid, kTraceThreads, 0, st>>>(sc, q_o, q_d, n, hits, nodes, tests);
+  else
+    k_trace_rays<false><<<grid, kTraceThreads, 0, st>>>(sc, q_o, q_d, n, hits, nullptr, nullptr);
+}
+
+void launch_shade(const SceneView &sc, const ShadeArgs &sa, const PathArrays &pa, int grid,
+                  const float4 *q_o, const float4 *q_d, const float4 *hits,
+                  const int32_t *count_in, float4 *n_o, float4 *n_d, int32_t *count_out,
+                  cudaStream_t st) {
+  k_shade<<<grid, kShadeThreads, 0, st>>>(sc, sa, pa, q_o, q_d, hits, count_in, n_o, n_d,
+                                          count_out);
+}
+
+void launch_accumulate(const AccumArgs &aa, const float4 *L, float *accum, uint32_t *valid,
+                       uint32_t *invalid, cudaStream_t st) {
+  if (aa.n_pix <= 0) return;
+  k_accumulate<<<(unsigned)((aa.n_pix + 255) / 256), 256, 0, st>>>(aa, L, accum, valid, invalid);
+}
+
+void launch_pack_rays_f32(const float *o, const float *d, int64_t n, float t_min, float t_max,
+                          float4 *q_o, float4 *q_d, cudaStream_t st) {
+  if (n <= 0) return;
+  k_pack_rays_f32<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(o, d, n, t_min, t_max, q_o, q_d);
+}
+
+void launch_pack_rays_f64(const double *o, const double *d, int64_t n, float t_min, float t_max,
+                          float4 *q_o, float4 *q_d, cudaStream_t st) {
+  if (n <= 0) return;
+  k_pack_rays_f64<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(o, d, n, t_min, t_max, q_o, q_d);
+}
+
+void launch_unpack_hits(const SceneView &sc, const float4 *hits, int64_t n, int32_t *idx32,
+                        float *t32, int64_t *idx64, double *t64, cudaStream_t st) {
+  if (n <= 0) return;
+  k_unpack_hits<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(sc, hits, n, idx32, t32, idx64, t64);
+}
+
+void launch_tonemap_u8(const float *lin, int64_t n_pixels, uint8_t *out, cudaStream_t st) {
+  if (n_pixels <= 0) return;
+  k_tonemap_u8<<<(unsigned)((n_pixels + 255) / 256), 256, 0, st>>>(lin, n_pixels, out);
+}
+
+}  // namespace lt

@@ -1,0 +1,78 @@
+// lt_kernels.h -- kernel argument structs and launchers (host <-> device).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "lt_device.cuh"
+
+namespace lt {
+
+constexpr int kTraceThreads = 128;
+constexpr int kShadeThreads = 256;
+
+struct PathArrays {
+  float4 *T;           // throughput rgb
+  float4 *L;           // radiance rgb
+  ulonglong2 *rng;     // PCG (state, inc)
+};
+
+struct RaygenArgs {
+  double cam[14];
+  int32_t width, height;
+  uint64_t seed;
+  int64_t sample_base;   // sample index of s_local = 0
+  int64_t n_pix;         // pixels in this batch
+  int64_t pix_offset;    // first local pixel of this batch
+  const int32_t *pix_list;  // local -> global pixel (NULL: identity)
+  int64_t n_paths;       // n_pix * samples in this batch
+  float t_min;
+};
+
+struct ShadeArgs {
+  int32_t depth, max_depth, rr_start;
+  float t_min;
+};
+
+struct AccumArgs {
+  int64_t n_pix, pix_offset, n_samples;
+  const int32_t *pix_list;
+};
+
+const void *trace_kernel_ptr(bool smem, bool count);
+const void *shade_kernel_ptr();
+
+void launch_flatten_nodes(const double *bmin, const double *bmax, const int32_t *left,
+                          const int32_t *right, const int32_t *first, const int32_t *count,
+                          const int32_t *perm, const int32_t *new_index, int64_t n_internal,
+                          float4 *out, cudaStream_t st);
+void launch_flatten_tris(const double *v0, const double *v1, const double *v2, const double *n0,
+                         const double *n1, const double *n2, const int32_t *mat_index,
+                         const int32_t *order, const uint8_t *leaf_end, int64_t n, float4 *tris,
+                         float4 *shade, cudaStream_t st);
+void launch_raygen(const RaygenArgs &ra, const PathArrays &pa, float4 *q_o, float4 *q_d,
+                   int32_t *count0, cudaStream_t st);
+void launch_raygen_explicit(const double *o, const double *d, const uint64_t *state,
+                            const uint64_t *inc, int64_t n, float t_min, const PathArrays &pa,
+                            float4 *q_o, float4 *q_d, int32_t *count0, cudaStream_t st);
+void launch_gather_explicit(const PathArrays &pa, int64_t n, double *rgb, uint64_t *state_out,
+                            cudaStream_t st);
+void launch_trace(const SceneView &sc, bool smem, bool count_work, int grid, size_t smem_bytes,
+                  const float4 *q_o, const float4 *q_d, const int32_t *count, int32_t *fetch,
+                  float4 *hits, unsigned long long *ray_ctr, cudaStream_t st);
+void launch_trace_rays(const SceneView &sc, const float4 *q_o, const float4 *q_d, int64_t n,
+                       float4 *hits, int32_t *nodes, int32_t *tests, cudaStream_t st);
+void launch_shade(const SceneView &sc, const ShadeArgs &sa, const PathArrays &pa, int grid,
+                  const float4 *q_o, const float4 *q_d, const float4 *hits,
+                  const int32_t *count_in, float4 *n_o, float4 *n_d, int32_t *count_out,
+                  cudaStream_t st);
+void launch_accumulate(const AccumArgs &aa, const float4 *L, float *accum, uint32_t *valid,
+                       uint32_t *invalid, cudaStream_t st);
+void launch_pack_rays_f32(const float *o, const float *d, int64_t n, float t_min, float t_max,
+                          float4 *q_o, float4 *q_d, cudaStream_t st);
+void launch_pack_rays_f64(const double *o, const double *d, int64_t n, float t_min, float t_max,
+                          float4 *q_o, float4 *q_d, cudaStream_t st);
+void launch_unpack_hits(const SceneView &sc, const float4 *hits, int64_t n, int32_t *idx32,
+                        float *t32, int64_t *idx64, double *t64, cudaStream_t st);
+void launch_tonemap_u8(const float *lin, int64_t n_pixels, uint8_t *out, cudaStream_t st);
+
+}  // namespace lt
