@@ -311,7 +311,9 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     cst = ds.stats()
     slab_per_ray = cst["slab_tests"] / max(1, cst["rays"])
     tri_per_ray = cst["tri_tests"] / max(1, cst["rays"])
-    bytes_per_ray = 32.0 * slab_per_ray + 48.0 * tri_per_ray + 40.0
+    # 32 B per child-box test (a 64 B node = 2 tests), 48 B per
+    # triangle test, and the ray record: 32 B in + 16 B hit out
+    bytes_per_ray = 32.0 * slab_per_ray + 48.0 * tri_per_ray + 48.0
 
     for _ in range(args.warmup):
         step(0)

@@ -118,7 +118,12 @@ struct lt_scene {
   SceneView view{};
   int64_t n_tris = 0, n_nodes = 0, n_internal = 0, n_bfs = 0;
   int64_t device_bytes = 0;
-  DevBuf nodes, tris, shade, mats, env;
+  // nodes and leaf-ordered triangles share one allocation so a single L2
+  // access-policy window keeps the whole traversal set persisting
+  DevBuf geo, shade, mats, env;
+  size_t nodes_bytes = 0, geo_bytes = 0;
+  bool use_window = false;
+  cudaAccessPolicyWindow window{};
   // wavefront workspace
   int64_t cap = 0;
   int32_t depth_cap = 0;
@@ -299,7 +304,7 @@ static void destroy_scene(lt_scene *s) {
   if (!s) return;
   DeviceGuard g(s->device);
   if (s->stream) cudaStreamSynchronize(s->stream);
-  for (DevBuf *b : {&s->nodes, &s->tris, &s->shade, &s->mats, &s->env, &s->q_o[0], &s->q_o[1],
+  for (DevBuf *b : {&s->geo, &s->shade, &s->mats, &s->env, &s->q_o[0], &s->q_o[1],
                     &s->q_d[0], &s->q_d[1], &s->hits, &s->T, &s->L, &s->rng, &s->counters,
                     &s->ray_ctr, &s->pix_list, &s->s_a, &s->s_b, &s->s_c, &s->s_d, &s->s_e,
                     &s->s_f})
@@ -311,25 +316,42 @@ static void destroy_scene(lt_scene *s) {
 }
 
 static int configure_launches(lt_scene *s) {
-  int blocks = 0;
   const char *env = std::getenv("LT_SMEM_NODES");
-  int want = env ? std::atoi(env) : 256;
+  const int want = env ? std::atoi(env) : 64;
   s->smem_nodes = (int)std::max<int64_t>(0, std::min<int64_t>(want, s->n_bfs));
-  size_t smem = (size_t)s->smem_nodes * 64;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, trace_kernel_ptr(false, false),
-                                                   kTraceThreads, 0));
-  s->trace_grid[0] = std::max(1, blocks) * s->sm_count;
-  blocks = 0;
-  if (smem > 0) {
+  for (int v = 0; v < 2; ++v) {
+    const bool top = v == 1;
+    const size_t smem = trace_smem_bytes(top ? s->smem_nodes : 0);
     for (bool c : {false, true})
-      CK(cudaFuncSetAttribute(trace_kernel_ptr(true, c),
+      CK(cudaFuncSetAttribute(trace_kernel_ptr(top, c),
                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, trace_kernel_ptr(true, false),
+    int blocks = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, trace_kernel_ptr(top, false),
                                                      kTraceThreads, smem));
+    s->trace_grid[v] = std::max(1, blocks) * s->sm_count;
   }
-  s->trace_grid[1] = std::max(1, blocks) * s->sm_count;
+  int blocks = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, shade_kernel_ptr(), kShadeThreads, 0));
   s->shade_grid = std::max(1, blocks) * s->sm_count;
+  // L2 residency of the traversal set (nodes + leaf-ordered triangles)
+  const char *pe = std::getenv("LT_L2_PERSIST");
+  int max_persist = 0, max_window = 0;
+  cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, s->device);
+  cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, s->device);
+  s->use_window = !(pe && pe[0] == '0') && max_persist > 0 && max_window > 0;
+  if (s->use_window) {
+    const size_t limit = std::min<size_t>((size_t)max_persist, s->geo_bytes);
+    size_t cur = 0;
+    cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+    if (cur < limit) CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, limit));
+    cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+    const size_t win = std::min<size_t>((size_t)max_window, s->geo_bytes);
+    s->window.base_ptr = s->geo.p;
+    s->window.num_bytes = win;
+    s->window.hitRatio = win > 0 ? (float)std::min(1.0, (double)cur / (double)win) : 0.f;
+    s->window.hitProp = cudaAccessPropertyPersisting;
+    s->window.missProp = cudaAccessPropertyStreaming;
+  }
   return LT_OK;
 }
 
@@ -390,13 +412,16 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
     if ((rc = upload(t_mat, d->material_index, n, st))) break;
     if ((rc = upload(t_order, d->triangle_order, n, st))) break;
     if ((rc = upload(t_end, leaf_end.data(), n, st))) break;
-    if ((rc = s->tris.ensure(48 * n))) break;
+    s->nodes_bytes = (size_t)std::max<int64_t>(1, s->n_internal) * 64;
+    s->geo_bytes = s->nodes_bytes + 48 * (size_t)n;
+    if ((rc = s->geo.ensure(s->geo_bytes))) break;
     if ((rc = s->shade.ensure(48 * n))) break;
+    float4 *g_nodes = s->geo.as<float4>();
+    float4 *g_tris = g_nodes + s->nodes_bytes / 16;
     launch_flatten_tris(t_v[0].as<double>(), t_v[1].as<double>(), t_v[2].as<double>(),
                         t_v[3].as<double>(), t_v[4].as<double>(), t_v[5].as<double>(),
                         t_mat.as<int32_t>(), t_order.as<int32_t>(), t_end.as<uint8_t>(), n,
-                        s->tris.as<float4>(), s->shade.as<float4>(), st);
-    if ((rc = s->nodes.ensure(std::max<int64_t>(1, s->n_internal) * 64))) break;
+                        g_tris, s->shade.as<float4>(), st);
     if (s->n_internal > 0) {
       if ((rc = upload(t_bmin, d->bounds_min, 3 * nn, st))) break;
       if ((rc = upload(t_bmax, d->bounds_max, 3 * nn, st))) break;
@@ -408,8 +433,8 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
       if ((rc = upload(t_new, new_index.data(), nn, st))) break;
       launch_flatten_nodes(t_bmin.as<double>(), t_bmax.as<double>(), t_left.as<int32_t>(),
                            t_right.as<int32_t>(), t_first.as<int32_t>(), t_count.as<int32_t>(),
-                           t_perm.as<int32_t>(), t_new.as<int32_t>(), s->n_internal,
-                           s->nodes.as<float4>(), st);
+                           t_perm.as<int32_t>(), t_new.as<int32_t>(), s->n_internal, g_nodes,
+                           st);
     }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
@@ -442,8 +467,8 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
   RET(rc);
 
   SceneView &v = s->view;
-  v.nodes = s->nodes.as<float4>();
-  v.tris = s->tris.as<float4>();
+  v.nodes = s->geo.as<float4>();
+  v.tris = s->geo.as<float4>() + s->nodes_bytes / 16;
   v.shade = s->shade.as<float4>();
   v.mats = s->mats.as<GpuMaterial>();
   v.env_map = s->env.as<float4>();
@@ -460,10 +485,11 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
     v.env_a[k] = (float)d->env_a[k];
     v.env_b[k] = (float)d->env_b[k];
   }
-  s->device_bytes = (int64_t)(s->nodes.bytes + s->tris.bytes + s->shade.bytes + s->mats.bytes +
-                              s->env.bytes);
+  s->device_bytes = (int64_t)(s->geo.bytes + s->shade.bytes + s->mats.bytes + s->env.bytes);
   RET(configure_launches(s));
   v.n_top = s->smem_nodes;
+  const char *rf = std::getenv("LT_REFILL");
+  v.refill_min = std::max(1, std::min(32, rf ? std::atoi(rf) : 8));
   return LT_OK;
 }
 
@@ -556,10 +582,10 @@ static int run_bounces(lt_scene *s, int32_t max_depth, int32_t rr_start, float t
   int cur = 0;
   for (int32_t depth = 0; depth < max_depth; ++depth) {
     if (flags & LT_FLAG_PROFILE) RET(record_event(s, st));
-    launch_trace(sc, smem, (flags & LT_FLAG_COUNT) != 0, s->trace_grid[smem ? 1 : 0],
-                 smem ? (size_t)s->smem_nodes * 64 : 0, s->q_o[cur].as<float4>(),
-                 s->q_d[cur].as<float4>(), ctr + depth, fetch + depth, s->hits.as<float4>(),
-                 s->ray_ctr.as<unsigned long long>(), st);
+    CK(launch_trace(sc, smem, (flags & LT_FLAG_COUNT) != 0, s->trace_grid[smem ? 1 : 0],
+                    s->use_window ? &s->window : nullptr, s->q_o[cur].as<float4>(),
+                    s->q_d[cur].as<float4>(), ctr + depth, fetch + depth, s->hits.as<float4>(),
+                    s->ray_ctr.as<unsigned long long>(), st));
     if (flags & LT_FLAG_PROFILE) RET(record_event(s, st));
     ShadeArgs sa{depth, max_depth, rr_start, t_min};
     launch_shade(sc, sa, pa, s->shade_grid, s->q_o[cur].as<float4>(), s->q_d[cur].as<float4>(),

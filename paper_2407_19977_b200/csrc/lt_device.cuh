@@ -60,6 +60,7 @@ struct SceneView {
   const float4 *__restrict__ env_map;  // (h, w) RGB + pad
   int32_t root_link;
   int32_t n_top;        // internal nodes [0, n_top) are BFS-ordered top levels
+  int32_t refill_min;   // idle lanes that trigger a warp refill in k_trace
   float root_lo[3], root_hi[3];
   int32_t env_kind;
   int32_t env_w, env_h;

@@ -131,49 +131,194 @@ __global__ void k_gather_explicit(PathArrays pa, int64_t n, double *__restrict__
 
 // ------------------------------------------------------------------ trace
 
-// Persistent closest-hit kernel: one CTA per resident slot, warps fetch 32
-// queue entries at a time from a device counter (load balance across the
-// divergent ray population); the top BVH levels are staged in shared memory.
+// Persistent closest-hit kernel (the render path).
+//  * grid = SMs x resident CTAs; each lane owns one ray at a time and, when
+//    it finishes, the warp refills its idle lanes from the queue with one
+//    atomic (ballot + popc ranks) once >= sc.refill_min lanes are idle, so
+//    short rays do not leave lanes dark while long ones finish;
+//  * traversal stack: the first kShortStack entries of every lane live in
+//    shared memory, laid out [depth][thread] (conflict-free), deeper ones in
+//    local memory;
+//  * optionally the top BFS nodes are staged in shared memory;
+//  * queue reads / hit writes are streaming (__ldcs / __stcs) so they do not
+//    evict the scene from L2.
 // ray_ctr[0] += queue length; with COUNT also ray_ctr[1] += slab tests and
-// ray_ctr[2] += triangle tests (warp-reduced, one atomic per warp per fetch).
+// ray_ctr[2] += triangle tests.
 template <bool USE_SMEM, bool COUNT>
 __global__ void __launch_bounds__(kTraceThreads)
     k_trace(SceneView sc, const float4 *__restrict__ q_o, const float4 *__restrict__ q_d,
             const int32_t *__restrict__ count, int32_t *__restrict__ fetch,
             float4 *__restrict__ hits, unsigned long long *__restrict__ ray_ctr) {
-  extern __shared__ float4 s_top[];
+  extern __shared__ float4 s_mem[];
+  const int n_top = USE_SMEM ? sc.n_top : 0;
   if (USE_SMEM) {
-    const int n4 = 4 * sc.n_top;
-    for (int j = threadIdx.x; j < n4; j += blockDim.x) s_top[j] = __ldg(&sc.nodes[j]);
+    for (int j = threadIdx.x; j < 4 * n_top; j += blockDim.x) s_mem[j] = __ldg(&sc.nodes[j]);
     __syncthreads();
   }
+  int32_t *s_node = reinterpret_cast<int32_t *>(s_mem + 4 * n_top);
+  float *s_t = reinterpret_cast<float *>(s_node + kShortStack * kTraceThreads);
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const unsigned lanes_below = (1u << lane) - 1u;
+  int32_t l_node[LT_STACK - kShortStack];
+  float l_t[LT_STACK - kShortStack];
+
   const int n = *count;
-  if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(ray_ctr, (unsigned long long)n);
-  const int lane = threadIdx.x & 31;
+  if (blockIdx.x == 0 && tid == 0) atomicAdd(ray_ctr, (unsigned long long)n);
+
+  int q = -1;
+  bool exhausted = false;  // warp-uniform: the queue is drained
+  f3 o{0.f, 0.f, 0.f}, d{0.f, 0.f, 1.f}, inv{0.f, 0.f, 0.f};
+  float t_min = 0.f;
+  HitRec best{0.f, 0.f, 0.f, -1};
+  int32_t best_orig = 0x7fffffff;
+  int sp = 0;
+  int32_t node = LT_LINK_EXIT;
+  int nn = 0, nt = 0;
+
   while (true) {
-    int base = 0;
-    if (lane == 0) base = atomicAdd(fetch, 32);
-    base = __shfl_sync(kFull, base, 0);
-    if (base >= n) break;
-    const int q = base + lane;
-    int nn = 0, nt = 0;
-    if (q < n) {
-      const float4 ro = q_o[q];
-      const float4 rd = q_d[q];
-      const HitRec h = traverse<USE_SMEM, COUNT>(sc, s_top, mk(ro.x, ro.y, ro.z),
-                                                mk(rd.x, rd.y, rd.z), rd.w,
-                                                __int_as_float(0x7f800000), &nn, &nt);
-      hits[q] = make_float4(h.t, h.u, h.v, __int_as_float(h.k));
+    // ---- refill idle lanes
+    const unsigned idle = __ballot_sync(kFull, q < 0);
+    if (!exhausted && __popc(idle) >= sc.refill_min) {
+      const int cnt = __popc(idle);
+      const int leader = __ffs(idle) - 1;
+      int base = 0;
+      if (lane == leader) base = atomicAdd(fetch, cnt);
+      base = __shfl_sync(kFull, base, leader);
+      exhausted = base + cnt >= n;
+      if (q < 0) {
+        const int r = base + __popc(idle & lanes_below);
+        if (r < n) {
+          q = r;
+          const float4 ro = __ldcs(&q_o[r]);
+          const float4 rd = __ldcs(&q_d[r]);
+          o = mk(ro.x, ro.y, ro.z);
+          d = mk(rd.x, rd.y, rd.z);
+          t_min = rd.w;
+          inv = ray_inverse(d);
+          best = HitRec{__int_as_float(0x7f800000), 0.f, 0.f, -1};
+          best_orig = 0x7fffffff;
+          sp = 0;
+          if (COUNT) ++nn;
+          float t_root;
+          node = slab(o, inv, sc.root_lo[0], sc.root_hi[0], sc.root_lo[1], sc.root_hi[1],
+                      sc.root_lo[2], sc.root_hi[2], t_min, best.t, t_root)
+                     ? sc.root_link
+                     : LT_LINK_EXIT;
+        }
+      }
     }
-    if (COUNT) {
-      for (int off = 16; off > 0; off >>= 1) {
-        nn += __shfl_down_sync(kFull, nn, off);
-        nt += __shfl_down_sync(kFull, nt, off);
+    if (__ballot_sync(kFull, q >= 0) == 0) {
+      if (exhausted) break;
+      continue;
+    }
+    if (q >= 0) {
+      // pop the next stack entry not culled by the current best t (bvh.py:389)
+      auto pop = [&]() -> int32_t {
+        const float cull = best.t * LT_SLAB_WIDEN;
+        while (sp > 0) {
+          --sp;
+          int32_t x;
+          float tx;
+          if (sp < kShortStack) {
+            x = s_node[sp * kTraceThreads + tid];
+            tx = s_t[sp * kTraceThreads + tid];
+          } else {
+            x = l_node[sp - kShortStack];
+            tx = l_t[sp - kShortStack];
+          }
+          if (!(tx > cull)) return x;
+        }
+        return LT_LINK_EXIT;
+      };
+      // ---- internal nodes (speculative while-while, Aila & Laine 2009):
+      // a lane that reaches a leaf parks it in `leaf` and keeps descending
+      // until every lane in the loop holds a leaf, so the node loop runs
+      // with more lanes busy; culling with the older best t is only
+      // conservative, never wrong.
+      int32_t leaf = 0;  // >= 0: none pending
+      while (node >= 0) {
+        float4 a, b, c, e;
+        if (USE_SMEM && node < n_top) {
+          const float4 *np = s_mem + 4 * node;
+          a = np[0];
+          b = np[1];
+          c = np[2];
+          e = np[3];
+        } else {
+          const float4 *np = sc.nodes + 4 * (int64_t)node;
+          a = __ldg(np + 0);
+          b = __ldg(np + 1);
+          c = __ldg(np + 2);
+          e = __ldg(np + 3);
+        }
+        if (COUNT) nn += 2;
+        float tl, tr;
+        const bool hl = slab(o, inv, a.x, a.y, a.z, a.w, c.x, c.y, t_min, best.t, tl);
+        const bool hr = slab(o, inv, b.x, b.y, b.z, b.w, c.z, c.w, t_min, best.t, tr);
+        const int32_t lc = __float_as_int(e.x), rc = __float_as_int(e.y);
+        if (hl && hr) {
+          const bool left_near = tl <= tr;  // bvh.py:414
+          const int32_t far_node = left_near ? rc : lc;
+          const float far_t = left_near ? tr : tl;
+          if (sp < kShortStack) {
+            s_node[sp * kTraceThreads + tid] = far_node;
+            s_t[sp * kTraceThreads + tid] = far_t;
+          } else {
+            l_node[sp - kShortStack] = far_node;
+            l_t[sp - kShortStack] = far_t;
+          }
+          ++sp;
+          node = left_near ? lc : rc;
+        } else if (hl) {
+          node = lc;
+        } else if (hr) {
+          node = rc;
+        } else {
+          node = pop();
+        }
+        if (node < 0 && node != LT_LINK_EXIT && leaf >= 0) {
+          leaf = node;
+          node = pop();
+        }
+        if (!__any_sync(__activemask(), leaf >= 0)) break;
       }
-      if (lane == 0) {
-        atomicAdd(ray_ctr + 1, (unsigned long long)nn);
-        atomicAdd(ray_ctr + 2, (unsigned long long)nt);
+      if (leaf >= 0 && node < 0 && node != LT_LINK_EXIT) {
+        leaf = node;
+        node = pop();
       }
+      // ---- pending leaves: their triangles (the last carries the end flag)
+      while (leaf < 0) {
+        int64_t k = ~leaf;
+        while (true) {
+          const float4 t0 = __ldg(&sc.tris[3 * k]);
+          const float4 t1 = __ldg(&sc.tris[3 * k + 1]);
+          const float4 t2 = __ldg(&sc.tris[3 * k + 2]);
+          if (COUNT) ++nt;
+          mt_test(o, d, t_min, t0, t1, t2, (int32_t)k, best, best_orig);
+          if (__float_as_int(t1.w) != 0) break;
+          ++k;
+        }
+        leaf = 0;
+        if (node < 0 && node != LT_LINK_EXIT) {
+          leaf = node;
+          node = pop();
+        }
+      }
+      if (node == LT_LINK_EXIT) {
+        __stcs(&hits[q], make_float4(best.t, best.u, best.v, __int_as_float(best.k)));
+        q = -1;
+      }
+    }
+  }
+  if (COUNT) {
+    for (int off = 16; off > 0; off >>= 1) {
+      nn += __shfl_down_sync(kFull, nn, off);
+      nt += __shfl_down_sync(kFull, nt, off);
+    }
+    if (lane == 0) {
+      atomicAdd(ray_ctr + 1, (unsigned long long)nn);
+      atomicAdd(ray_ctr + 2, (unsigned long long)nt);
     }
   }
 }
@@ -190,8 +335,8 @@ __global__ void __launch_bounds__(kTraceThreads)
   const float4 ro = q_o[q];
   const float4 rd = q_d[q];
   int nn = 0, nt = 0;
-  const HitRec h = traverse<false, COUNT>(sc, nullptr, mk(ro.x, ro.y, ro.z), mk(rd.x, rd.y, rd.z),
-                                          rd.w, ro.w, &nn, &nt);
+  const HitRec h = traverse<COUNT>(sc, mk(ro.x, ro.y, ro.z), mk(rd.x, rd.y, rd.z), rd.w, ro.w,
+                                   &nn, &nt);
   hits[q] = make_float4(h.t, h.u, h.v, __int_as_float(h.k));
   if (COUNT) {
     nodes[q] = nn;
@@ -443,22 +588,37 @@ void launch_gather_explicit(const PathArrays &pa, int64_t n, double *rgb, uint64
   k_gather_explicit<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(pa, n, rgb, state_out);
 }
 
-void launch_trace(const SceneView &sc, bool smem, bool count_work, int grid, size_t smem_bytes,
-                  const float4 *q_o, const float4 *q_d, const int32_t *count, int32_t *fetch,
-                  float4 *hits, unsigned long long *ray_ctr, cudaStream_t st) {
-  const size_t sm = smem ? smem_bytes : 0;
+size_t trace_smem_bytes(int n_top) {
+  return (size_t)n_top * 64 + (size_t)kShortStack * kTraceThreads * 8;
+}
+
+cudaError_t launch_trace(const SceneView &sc, bool smem, bool count_work, int grid,
+                         const cudaAccessPolicyWindow *window, const float4 *q_o,
+                         const float4 *q_d, const int32_t *count, int32_t *fetch, float4 *hits,
+                         unsigned long long *ray_ctr, cudaStream_t st) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kTraceThreads);
+  cfg.dynamicSmemBytes = trace_smem_bytes(smem ? sc.n_top : 0);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  if (window) {
+    attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
+    attr[0].val.accessPolicyWindow = *window;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+  }
   if (smem && count_work)
-    k_trace<true, true><<<grid, kTraceThreads, sm, st>>>(sc, q_o, q_d, count, fetch, hits,
-                                                         ray_ctr);
-  else if (smem)
-    k_trace<true, false><<<grid, kTraceThreads, sm, st>>>(sc, q_o, q_d, count, fetch, hits,
-                                                          ray_ctr);
-  else if (count_work)
-    k_trace<false, true><<<grid, kTraceThreads, 0, st>>>(sc, q_o, q_d, count, fetch, hits,
-                                                         ray_ctr);
-  else
-    k_trace<false, false><<<grid, kTraceThreads, 0, st>>>(sc, q_o, q_d, count, fetch, hits,
-                                                          ray_ctr);
+    return cudaLaunchKernelEx(&cfg, k_trace<true, true>, sc, q_o, q_d, count, fetch, hits,
+                              ray_ctr);
+  if (smem)
+    return cudaLaunchKernelEx(&cfg, k_trace<true, false>, sc, q_o, q_d, count, fetch, hits,
+                              ray_ctr);
+  if (count_work)
+    return cudaLaunchKernelEx(&cfg, k_trace<false, true>, sc, q_o, q_d, count, fetch, hits,
+                              ray_ctr);
+  return cudaLaunchKernelEx(&cfg, k_trace<false, false>, sc, q_o, q_d, count, fetch, hits,
+                            ray_ctr);
 }
 
 void launch_trace_rays(const SceneView &sc, const float4 *q_o, const float4 *q_d, int64_t n,

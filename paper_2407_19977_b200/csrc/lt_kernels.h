@@ -9,6 +9,7 @@ namespace lt {
 
 constexpr int kTraceThreads = 128;
 constexpr int kShadeThreads = 256;
+constexpr int kShortStack = 16;   // per-lane traversal stack entries in shared memory
 
 struct PathArrays {
   float4 *T;           // throughput rgb
@@ -56,9 +57,11 @@ void launch_raygen_explicit(const double *o, const double *d, const uint64_t *st
                             float4 *q_o, float4 *q_d, int32_t *count0, cudaStream_t st);
 void launch_gather_explicit(const PathArrays &pa, int64_t n, double *rgb, uint64_t *state_out,
                             cudaStream_t st);
-void launch_trace(const SceneView &sc, bool smem, bool count_work, int grid, size_t smem_bytes,
-                  const float4 *q_o, const float4 *q_d, const int32_t *count, int32_t *fetch,
-                  float4 *hits, unsigned long long *ray_ctr, cudaStream_t st);
+size_t trace_smem_bytes(int n_top);
+cudaError_t launch_trace(const SceneView &sc, bool smem, bool count_work, int grid,
+                         const cudaAccessPolicyWindow *window, const float4 *q_o,
+                         const float4 *q_d, const int32_t *count, int32_t *fetch, float4 *hits,
+                         unsigned long long *ray_ctr, cudaStream_t st);
 void launch_trace_rays(const SceneView &sc, const float4 *q_o, const float4 *q_d, int64_t n,
                        float4 *hits, int32_t *nodes, int32_t *tests, cudaStream_t st);
 void launch_shade(const SceneView &sc, const ShadeArgs &sa, const PathArrays &pa, int grid,

@@ -292,7 +292,24 @@ def material_fixture():
     print(f"material fixture: {len(rows)} cases")
 
 
+def tonemap_fixture():
+    """tonemap_to_u8 (tonemap.py:59-61) on HDR values spanning both knees."""
+    rng = np.random.default_rng(5)
+    lin = np.concatenate([
+        rng.uniform(0.0, 0.1, (2000, 3)), rng.uniform(0.0, 1.0, (4000, 3)),
+        rng.exponential(2.0, (2000, 3)), rng.uniform(0.0, 50.0, (500, 3)),
+        np.array([[0.0, 0.0, 0.0], [0.08, 0.08, 0.08], [0.76, 0.5, 0.2], [1.0, 1.0, 1.0]])])
+    lin = lin.astype(np.float32).astype(np.float64)  # the device holds fp32 radiance
+    np.savez_compressed(HERE / "tonemap.npz", linear=lin, u8=lx.tonemap_to_u8(lin),
+                        neutral=lx.pbr_neutral_tonemap(lin))
+    print(f"tonemap fixture: {lin.shape[0]} colors")
+
+
 def main():
+    if "--only" in sys.argv:
+        globals()[sys.argv[sys.argv.index("--only") + 1] + "_fixture"]()
+        return
+    tonemap_fixture()
     rng_fixture()
     material_fixture()
     S = lx.RenderSettings

@@ -285,26 +285,30 @@ def test_per_sample_parity_at_scale():
 
 
 def test_converged_image_within_monte_carlo_ci():
-    """Independent seeds: GPU and oracle means agree within 4 sigma for all
-    but a small fraction of pixels (Cornell C2 materials)."""
+    """Independent seeds: GPU and oracle means agree within 4 sigma (pooled
+    per-pixel standard error of the difference) for all but a small fraction
+    of pixels (Cornell C2 materials).  The GPU image is the full render;
+    its per-pixel variance comes from the same samples rendered one at a
+    time."""
     from oracle.oracle import OracleScene
     m = lb()
     sc = m.cornell_box(48, 48, "mixed")
     bvh = m.build_bvh(sc.triangles)
     spp = 256
-    gpu = m.render_progressive(sc, m.RenderSettings(samples_per_pixel=spp, max_depth=8,
-                                                    seed=101), bvh=bvh).image
+    st = m.RenderSettings(samples_per_pixel=spp, max_depth=8, seed=101)
+    ds = m.DeviceScene(sc, bvh)
+    gpu = m.render_progressive(ds, st).image.reshape(-1, 3)
+    gvals = np.stack([gpu_sample_values(ds, sc.camera, st, s) for s in range(spp)])
+    assert np.allclose(np.nanmean(gvals, axis=0), gpu, rtol=1e-5, atol=1e-6)
     oc = OracleScene.from_scene(sc, bvh)
     cam = m.camera_pack(sc.camera)
     pix = np.arange(48 * 48)
     vals = np.stack([oc.sample_values(pix, s, cam, 48, 48, 202, 8, 3)[0] for s in range(spp)])
-    mean = vals.mean(axis=0).reshape(48, 48, 3)
-    var = vals.var(axis=0, ddof=1).reshape(48, 48, 3)
-    sigma = np.sqrt(2.0 * var / spp) + 1e-6
-    z = np.abs(gpu - mean) / sigma
-    frac = float((z > 4.0).any(axis=2).mean())
+    sigma = np.sqrt((np.nanvar(gvals, axis=0, ddof=1) + vals.var(axis=0, ddof=1)) / spp) + 1e-6
+    z = np.abs(gpu - vals.mean(axis=0)) / sigma
+    frac = float((z > 4.0).any(axis=1).mean())
     print(f"pixels beyond 4 sigma: {frac:.4f}")
-    assert frac <= 0.01
+    assert frac <= 0.005
 
 
 # ------------------------------------------------------------------ extensions
@@ -363,3 +367,26 @@ def test_latlong_environment_matches_oracle():
                               st.t_min)
     got = gpu_sample_values(ds, sc.camera, st, 0)
     assert close_fraction(got, ref, rel=2e-3) >= 0.97
+
+
+# ------------------------------------------------------------------ display
+
+def test_tonemap_matches_reference():
+    """k_tonemap_u8 vs the reference's tonemap_to_u8 on 8.5k HDR colors
+    (golden): identical 8-bit output."""
+    from conftest import GOLDEN
+    from paper_2407_19977_b200.tonemap import tonemap_to_u8
+    z = np.load(GOLDEN / "tonemap.npz")
+    got = tonemap_to_u8(z["linear"])
+    assert np.array_equal(got, z["u8"])
+
+
+def test_accumulator_to_u8():
+    from paper_2407_19977_b200.tonemap import accumulator_to_u8, tonemap_to_u8
+    m = lb()
+    g = golden_scene("glossy")
+    acc = m.render_progressive(g.scene, g.settings, return_device=True)
+    img = accumulator_to_u8(acc).cpu().numpy()
+    ref = tonemap_to_u8(acc.mean().cpu().numpy())
+    assert img.shape == (g.camera.height, g.camera.width, 3)
+    assert np.array_equal(img, ref)
