@@ -51,6 +51,8 @@ def parse_args():
     p.add_argument("--seed", type=int, default=0)
     p.add_argument("--tile", type=int, default=16)
     p.add_argument("--flags", type=int, default=0)
+    p.add_argument("--batch-paths", type=int, default=0,
+                   help="paths per wavefront batch (0 = library default)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -300,7 +302,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         acc.valid.zero_()
         acc.invalid.zero_()
         render_pass_device(ds, cam, settings, acc, 0, spp or args.spp, flags=flags | args.flags,
-                           shard=shard, stream=stream)
+                           shard=shard, max_batch_paths=args.batch_paths, stream=stream)
         if world > 1:
             merge_tiles(acc, dst=0)
 

@@ -12,7 +12,8 @@ from pathlib import Path
 
 import numpy as np
 
-LIB_PATH = Path(__file__).resolve().parent / "_build" / "libluxb200.so"
+LIB_PATH = Path(os.environ.get("LUXB200_LIB",
+                               Path(__file__).resolve().parent / "_build" / "libluxb200.so"))
 
 LT_OK = 0
 LT_ERR_INVALID = 1

@@ -51,27 +51,34 @@ def _stale(target: Path, deps: list[Path]) -> bool:
     return any(d.stat().st_mtime > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    OUT.mkdir(parents=True, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, variant: str | None = None,
+          defines: tuple[str, ...] = ()) -> Path:
+    """Build the library; `variant` builds an experimental copy with extra
+    -D `defines` into _build/variant_<name>/ (select it with LUXB200_LIB)."""
+    out = OUT if variant is None else OUT / f"variant_{variant}"
+    lib = out / "libluxb200.so"
+    out.mkdir(parents=True, exist_ok=True)
     headers = [CSRC / h for h in HEADERS] + [INCLUDE / "luxb200.h", Path(__file__)]
-    log_path = OUT / "build.log"
+    log_path = out / "build.log"
+    dflags = [f"-D{d}" for d in defines]
     objs = []
     with open(log_path, "a") as log:
         for src in CU_SOURCES:
-            obj = OUT / (Path(src).stem + ".o")
+            obj = out / (Path(src).stem + ".o")
             objs.append(obj)
             if force or _stale(obj, [CSRC / src] + headers):
-                _run([NVCC, *ARCH, *NVCC_FLAGS, "-c", str(CSRC / src), "-o", str(obj)], log)
+                _run([NVCC, *ARCH, *NVCC_FLAGS, *dflags, "-c", str(CSRC / src), "-o", str(obj)],
+                     log)
         for src in CPP_SOURCES:
-            obj = OUT / (Path(src).stem + ".o")
+            obj = out / (Path(src).stem + ".o")
             objs.append(obj)
             if force or _stale(obj, [CSRC / src] + headers):
                 _run([CXX, *CXX_FLAGS, "-c", str(CSRC / src), "-o", str(obj)], log)
-        if force or _stale(LIB, objs):
-            _run([NVCC, *ARCH, "-shared", "-o", str(LIB), *map(str, objs)], log)
+        if force or _stale(lib, objs):
+            _run([NVCC, *ARCH, "-shared", "-o", str(lib), *map(str, objs)], log)
     if verbose:
         print(log_path.read_text()[-4000:])
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

@@ -120,8 +120,9 @@ struct lt_scene {
   int64_t device_bytes = 0;
   // nodes and leaf-ordered triangles share one allocation so a single L2
   // access-policy window keeps the whole traversal set persisting
-  DevBuf geo, shade, mats, env;
+  DevBuf geo, shade, mats, env, nodes2;
   size_t nodes_bytes = 0, geo_bytes = 0;
+  int64_t n_wide = 0;
   bool use_window = false;
   cudaAccessPolicyWindow window{};
   // wavefront workspace
@@ -304,7 +305,7 @@ static void destroy_scene(lt_scene *s) {
   if (!s) return;
   DeviceGuard g(s->device);
   if (s->stream) cudaStreamSynchronize(s->stream);
-  for (DevBuf *b : {&s->geo, &s->shade, &s->mats, &s->env, &s->q_o[0], &s->q_o[1],
+  for (DevBuf *b : {&s->geo, &s->nodes2, &s->shade, &s->mats, &s->env, &s->q_o[0], &s->q_o[1],
                     &s->q_d[0], &s->q_d[1], &s->hits, &s->T, &s->L, &s->rng, &s->counters,
                     &s->ray_ctr, &s->pix_list, &s->s_a, &s->s_b, &s->s_c, &s->s_d, &s->s_e,
                     &s->s_f})
@@ -317,7 +318,7 @@ static void destroy_scene(lt_scene *s) {
 
 static int configure_launches(lt_scene *s) {
   const char *env = std::getenv("LT_SMEM_NODES");
-  const int want = env ? std::atoi(env) : 64;
+  const int want = env ? std::atoi(env) : 0;
   s->smem_nodes = (int)std::max<int64_t>(0, std::min<int64_t>(want, s->n_bfs));
   for (int v = 0; v < 2; ++v) {
     const bool top = v == 1;
@@ -396,6 +397,45 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
     }
   }
   s->n_internal = (int64_t)perm.size();
+  // --- 4-wide collapse of the same tree (render / closest-hit layout): a
+  // wide node starts from its binary node's two children and repeatedly
+  // replaces the internal child with the largest surface area by its two
+  // children, up to four; wide nodes are numbered depth-first.
+  std::vector<int32_t> wide_children, wide_of(nn, -1);
+  if (!is_leaf(0)) {
+    auto area = [&](int32_t x) {
+      const double *lo = d->bounds_min + 3 * (int64_t)x, *hi = d->bounds_max + 3 * (int64_t)x;
+      const double dx = hi[0] - lo[0], dy = hi[1] - lo[1], dz = hi[2] - lo[2];
+      return dx * dy + dy * dz + dz * dx;
+    };
+    std::vector<int32_t> stack{0};
+    while (!stack.empty()) {
+      const int32_t r = stack.back();
+      stack.pop_back();
+      wide_of[r] = (int32_t)(wide_children.size() / 4);
+      int32_t ch[4] = {d->left_child[r], d->right_child[r], -1, -1};
+      int nc = 2;
+      while (nc < 4) {
+        int pick = -1;
+        double best_area = -1.0;
+        for (int i = 0; i < nc; ++i)
+          if (!is_leaf(ch[i]) && area(ch[i]) > best_area) {
+            best_area = area(ch[i]);
+            pick = i;
+          }
+        if (pick < 0) break;
+        const int32_t x = ch[pick];
+        for (int j = nc; j > pick + 1; --j) ch[j] = ch[j - 1];
+        ch[pick] = d->left_child[x];
+        ch[pick + 1] = d->right_child[x];
+        ++nc;
+      }
+      for (int i = 0; i < 4; ++i) wide_children.push_back(i < nc ? ch[i] : -1);
+      for (int i = nc - 1; i >= 0; --i)
+        if (!is_leaf(ch[i])) stack.push_back(ch[i]);
+    }
+  }
+  s->n_wide = (int64_t)(wide_children.size() / 4);
   // leaf-end flags for the leaf-ordered triangle stream
   std::vector<uint8_t> leaf_end(n, 0);
   for (int64_t i = 0; i < nn; ++i)
@@ -403,7 +443,7 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
 
   // --- upload the float64 arrays and flatten on the device
   DevBuf t_v[6], t_mat, t_order, t_end, t_bmin, t_bmax, t_left, t_right, t_first, t_count,
-      t_perm, t_new;
+      t_perm, t_new, t_wch, t_wof;
   const double *src[6] = {d->v0, d->v1, d->v2, d->n0, d->n1, d->n2};
   int rc = LT_OK;
   do {
@@ -412,12 +452,14 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
     if ((rc = upload(t_mat, d->material_index, n, st))) break;
     if ((rc = upload(t_order, d->triangle_order, n, st))) break;
     if ((rc = upload(t_end, leaf_end.data(), n, st))) break;
-    s->nodes_bytes = (size_t)std::max<int64_t>(1, s->n_internal) * 64;
+    s->nodes_bytes = (size_t)std::max<int64_t>(1, s->n_wide) * 128;
     s->geo_bytes = s->nodes_bytes + 48 * (size_t)n;
     if ((rc = s->geo.ensure(s->geo_bytes))) break;
     if ((rc = s->shade.ensure(48 * n))) break;
-    float4 *g_nodes = s->geo.as<float4>();
-    float4 *g_tris = g_nodes + s->nodes_bytes / 16;
+    if ((rc = s->nodes2.ensure((size_t)std::max<int64_t>(1, s->n_internal) * 64))) break;
+    float4 *g_wide = s->geo.as<float4>();
+    float4 *g_tris = g_wide + s->nodes_bytes / 16;
+    float4 *g_nodes = s->nodes2.as<float4>();
     launch_flatten_tris(t_v[0].as<double>(), t_v[1].as<double>(), t_v[2].as<double>(),
                         t_v[3].as<double>(), t_v[4].as<double>(), t_v[5].as<double>(),
                         t_mat.as<int32_t>(), t_order.as<int32_t>(), t_end.as<uint8_t>(), n,
@@ -435,6 +477,11 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
                            t_right.as<int32_t>(), t_first.as<int32_t>(), t_count.as<int32_t>(),
                            t_perm.as<int32_t>(), t_new.as<int32_t>(), s->n_internal, g_nodes,
                            st);
+      if ((rc = upload(t_wch, wide_children.data(), wide_children.size(), st))) break;
+      if ((rc = upload(t_wof, wide_of.data(), wide_of.size(), st))) break;
+      launch_flatten_wide(t_bmin.as<double>(), t_bmax.as<double>(), t_first.as<int32_t>(),
+                          t_count.as<int32_t>(), t_wch.as<int32_t>(), t_wof.as<int32_t>(),
+                          s->n_wide, g_wide, st);
     }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
@@ -462,12 +509,14 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
   } while (0);
   for (DevBuf &b : t_v) b.release();
   for (DevBuf *b : {&t_mat, &t_order, &t_end, &t_bmin, &t_bmax, &t_left, &t_right, &t_first,
-                    &t_count, &t_perm, &t_new})
+                    &t_count, &t_perm, &t_new, &t_wch, &t_wof})
     b->release();
   RET(rc);
 
   SceneView &v = s->view;
-  v.nodes = s->geo.as<float4>();
+  v.wnodes = s->geo.as<float4>();
+  v.wroot_link = is_leaf(0) ? ~d->first_triangle[0] : 0;
+  v.nodes = s->nodes2.as<float4>();
   v.tris = s->geo.as<float4>() + s->nodes_bytes / 16;
   v.shade = s->shade.as<float4>();
   v.mats = s->mats.as<GpuMaterial>();
@@ -485,7 +534,8 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
     v.env_a[k] = (float)d->env_a[k];
     v.env_b[k] = (float)d->env_b[k];
   }
-  s->device_bytes = (int64_t)(s->geo.bytes + s->shade.bytes + s->mats.bytes + s->env.bytes);
+  s->device_bytes = (int64_t)(s->geo.bytes + s->nodes2.bytes + s->shade.bytes + s->mats.bytes +
+                              s->env.bytes);
   RET(configure_launches(s));
   v.n_top = s->smem_nodes;
   const char *rf = std::getenv("LT_REFILL");

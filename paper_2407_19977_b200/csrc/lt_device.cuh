@@ -1,6 +1,13 @@
 // lt_device.cuh -- device data layout and scalar device functions.
 //
 // HBM layout (all 16-byte aligned):
+//   wnodes : 8 x float4 (128 B, one cache line) per node of the host BVH
+//            collapsed to 4-wide (each wide node absorbs the largest-area
+//            internal children of its binary node until it has 4 children):
+//              f4[0..5] = lo.x[4], hi.x[4], lo.y[4], hi.y[4], lo.z[4], hi.z[4]
+//              f4[6]    = 4 child links (>= 0 wide node, < 0 leaf = ~first,
+//                         INT_MIN empty slot); f4[7] unused
+//            Boxes are the reference's float64 boxes rounded outward.
 //   nodes  : 4 x float4 per INTERNAL node of the host BVH; a node holds the
 //            fp32 boxes of both children (rounded outward) and their links.
 //              n0 = (L.lo.x, L.hi.x, L.lo.y, L.hi.y)
@@ -53,7 +60,9 @@ struct __align__(16) GpuMaterial {
 static_assert(sizeof(GpuMaterial) == 128, "material record is 128 bytes");
 
 struct SceneView {
-  const float4 *__restrict__ nodes;
+  const float4 *__restrict__ wnodes;   // BVH4: 8 x float4 per node (render / queries)
+  int32_t wroot_link;
+  const float4 *__restrict__ nodes;    // BVH2 (reference counters)
   const float4 *__restrict__ tris;
   const float4 *__restrict__ shade;
   const GpuMaterial *__restrict__ mats;

@@ -46,6 +46,42 @@ __global__ void k_flatten_nodes(const double *__restrict__ bmin, const double *_
   out[4 * i + 3] = make_float4(__int_as_float(link[0]), __int_as_float(link[1]), 0.f, 0.f);
 }
 
+// BVH4 records: node i gathers the reference nodes children[4 i .. 4 i + 3]
+// (-1 = empty slot) chosen by the host collapse; boxes rounded outward,
+// links: leaf -> ~first_triangle, internal -> its wide index.
+__global__ void k_flatten_wide(const double *__restrict__ bmin, const double *__restrict__ bmax,
+                               const int32_t *__restrict__ first,
+                               const int32_t *__restrict__ count,
+                               const int32_t *__restrict__ children,
+                               const int32_t *__restrict__ wide_of, int64_t n_wide,
+                               float4 *__restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n_wide) return;
+  float lo[3][4], hi[3][4];
+  int32_t link[4];
+  for (int c = 0; c < 4; ++c) {
+    const int32_t x = children[4 * i + c];
+    if (x < 0) {
+      for (int a = 0; a < 3; ++a) lo[a][c] = hi[a][c] = 0.f;
+      link[c] = LT_LINK_EXIT;
+      continue;
+    }
+    for (int a = 0; a < 3; ++a) {
+      lo[a][c] = __double2float_rd(bmin[3 * (int64_t)x + a]);
+      hi[a][c] = __double2float_ru(bmax[3 * (int64_t)x + a]);
+    }
+    link[c] = count[x] > 0 ? ~first[x] : wide_of[x];
+  }
+  float4 *o = out + 8 * i;
+  for (int a = 0; a < 3; ++a) {
+    o[2 * a] = make_float4(lo[a][0], lo[a][1], lo[a][2], lo[a][3]);
+    o[2 * a + 1] = make_float4(hi[a][0], hi[a][1], hi[a][2], hi[a][3]);
+  }
+  o[6] = make_float4(__int_as_float(link[0]), __int_as_float(link[1]), __int_as_float(link[2]),
+                     __int_as_float(link[3]));
+  o[7] = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
 // Triangles in leaf order k (triangle_order[k]); e1/e2 from float64
 // differences rounded once; shading normals + material index alongside.
 __global__ void k_flatten_tris(const double *__restrict__ v0, const double *__restrict__ v1,
@@ -145,17 +181,14 @@ __global__ void k_gather_explicit(PathArrays pa, int64_t n, double *__restrict__
 // ray_ctr[0] += queue length; with COUNT also ray_ctr[1] += slab tests and
 // ray_ctr[2] += triangle tests.
 template <bool USE_SMEM, bool COUNT>
-__global__ void __launch_bounds__(kTraceThreads)
+__global__ void __launch_bounds__(kTraceThreads, LT_TRACE_MIN_BLOCKS)
     k_trace(SceneView sc, const float4 *__restrict__ q_o, const float4 *__restrict__ q_d,
             const int32_t *__restrict__ count, int32_t *__restrict__ fetch,
             float4 *__restrict__ hits, unsigned long long *__restrict__ ray_ctr) {
+  // (USE_SMEM: the top-level staging variant measured slower than L1
+  // caching -- profiles/r01_sweep -- and is kept only as a launch option.)
   extern __shared__ float4 s_mem[];
-  const int n_top = USE_SMEM ? sc.n_top : 0;
-  if (USE_SMEM) {
-    for (int j = threadIdx.x; j < 4 * n_top; j += blockDim.x) s_mem[j] = __ldg(&sc.nodes[j]);
-    __syncthreads();
-  }
-  int32_t *s_node = reinterpret_cast<int32_t *>(s_mem + 4 * n_top);
+  int32_t *s_node = reinterpret_cast<int32_t *>(s_mem);
   float *s_t = reinterpret_cast<float *>(s_node + kShortStack * kTraceThreads);
   const int tid = threadIdx.x;
   const int lane = tid & 31;
@@ -168,7 +201,8 @@ __global__ void __launch_bounds__(kTraceThreads)
 
   int q = -1;
   bool exhausted = false;  // warp-uniform: the queue is drained
-  f3 o{0.f, 0.f, 0.f}, d{0.f, 0.f, 1.f}, inv{0.f, 0.f, 0.f};
+  f3 o{0.f, 0.f, 0.f}, d{0.f, 0.f, 1.f};
+  RaySlab rs{};
   float t_min = 0.f;
   HitRec best{0.f, 0.f, 0.f, -1};
   int32_t best_orig = 0x7fffffff;
@@ -195,15 +229,15 @@ __global__ void __launch_bounds__(kTraceThreads)
           o = mk(ro.x, ro.y, ro.z);
           d = mk(rd.x, rd.y, rd.z);
           t_min = rd.w;
-          inv = ray_inverse(d);
+          rs = ray_slab(o, d);
           best = HitRec{__int_as_float(0x7f800000), 0.f, 0.f, -1};
           best_orig = 0x7fffffff;
           sp = 0;
           if (COUNT) ++nn;
           float t_root;
-          node = slab(o, inv, sc.root_lo[0], sc.root_hi[0], sc.root_lo[1], sc.root_hi[1],
+          node = slab(rs, sc.root_lo[0], sc.root_hi[0], sc.root_lo[1], sc.root_hi[1],
                       sc.root_lo[2], sc.root_hi[2], t_min, best.t, t_root)
-                     ? sc.root_link
+                     ? sc.wroot_link
                      : LT_LINK_EXIT;
         }
       }
@@ -231,79 +265,31 @@ __global__ void __launch_bounds__(kTraceThreads)
         }
         return LT_LINK_EXIT;
       };
-      // ---- internal nodes (speculative while-while, Aila & Laine 2009):
-      // a lane that reaches a leaf parks it in `leaf` and keeps descending
-      // until every lane in the loop holds a leaf, so the node loop runs
-      // with more lanes busy; culling with the older best t is only
-      // conservative, never wrong.
-      int32_t leaf = 0;  // >= 0: none pending
+      auto push = [&](int32_t x, float tx) {
+        if (sp < kShortStack) {
+          s_node[sp * kTraceThreads + tid] = x;
+          s_t[sp * kTraceThreads + tid] = tx;
+        } else {
+          l_node[sp - kShortStack] = x;
+          l_t[sp - kShortStack] = tx;
+        }
+        ++sp;
+      };
+      // ---- wide nodes: descend nearest-first until a leaf or a dead end;
+      // the other hit children go on the stack farthest first
+      const float kInf = __int_as_float(0x7f800000);
       while (node >= 0) {
-        float4 a, b, c, e;
-        if (USE_SMEM && node < n_top) {
-          const float4 *np = s_mem + 4 * node;
-          a = np[0];
-          b = np[1];
-          c = np[2];
-          e = np[3];
-        } else {
-          const float4 *np = sc.nodes + 4 * (int64_t)node;
-          a = __ldg(np + 0);
-          b = __ldg(np + 1);
-          c = __ldg(np + 2);
-          e = __ldg(np + 3);
-        }
-        if (COUNT) nn += 2;
-        float tl, tr;
-        const bool hl = slab(o, inv, a.x, a.y, a.z, a.w, c.x, c.y, t_min, best.t, tl);
-        const bool hr = slab(o, inv, b.x, b.y, b.z, b.w, c.z, c.w, t_min, best.t, tr);
-        const int32_t lc = __float_as_int(e.x), rc = __float_as_int(e.y);
-        if (hl && hr) {
-          const bool left_near = tl <= tr;  // bvh.py:414
-          const int32_t far_node = left_near ? rc : lc;
-          const float far_t = left_near ? tr : tl;
-          if (sp < kShortStack) {
-            s_node[sp * kTraceThreads + tid] = far_node;
-            s_t[sp * kTraceThreads + tid] = far_t;
-          } else {
-            l_node[sp - kShortStack] = far_node;
-            l_t[sp - kShortStack] = far_t;
-          }
-          ++sp;
-          node = left_near ? lc : rc;
-        } else if (hl) {
-          node = lc;
-        } else if (hr) {
-          node = rc;
-        } else {
-          node = pop();
-        }
-        if (node < 0 && node != LT_LINK_EXIT && leaf >= 0) {
-          leaf = node;
-          node = pop();
-        }
-        if (!__any_sync(__activemask(), leaf >= 0)) break;
+        const Hits4 h = visit4(sc.wnodes + 8 * (int64_t)node, rs, t_min, best.t);
+        if (COUNT) nn += 4;
+        if (h.k3 < kInf) push(h.l3, h.k3);
+        if (h.k2 < kInf) push(h.l2, h.k2);
+        if (h.k1 < kInf) push(h.l1, h.k1);
+        node = h.k0 < kInf ? h.l0 : pop();
       }
-      if (leaf >= 0 && node < 0 && node != LT_LINK_EXIT) {
-        leaf = node;
+      // ---- leaf: its triangles, then the next stack entry
+      if (node != LT_LINK_EXIT) {
+        leaf_test<COUNT>(sc, ~(int64_t)node, o, d, t_min, best, best_orig, nt);
         node = pop();
-      }
-      // ---- pending leaves: their triangles (the last carries the end flag)
-      while (leaf < 0) {
-        int64_t k = ~leaf;
-        while (true) {
-          const float4 t0 = __ldg(&sc.tris[3 * k]);
-          const float4 t1 = __ldg(&sc.tris[3 * k + 1]);
-          const float4 t2 = __ldg(&sc.tris[3 * k + 2]);
-          if (COUNT) ++nt;
-          mt_test(o, d, t_min, t0, t1, t2, (int32_t)k, best, best_orig);
-          if (__float_as_int(t1.w) != 0) break;
-          ++k;
-        }
-        leaf = 0;
-        if (node < 0 && node != LT_LINK_EXIT) {
-          leaf = node;
-          node = pop();
-        }
       }
       if (node == LT_LINK_EXIT) {
         __stcs(&hits[q], make_float4(best.t, best.u, best.v, __int_as_float(best.k)));
@@ -335,8 +321,10 @@ __global__ void __launch_bounds__(kTraceThreads)
   const float4 ro = q_o[q];
   const float4 rd = q_d[q];
   int nn = 0, nt = 0;
-  const HitRec h = traverse<COUNT>(sc, mk(ro.x, ro.y, ro.z), mk(rd.x, rd.y, rd.z), rd.w, ro.w,
-                                   &nn, &nt);
+  // closest-hit queries walk the wide layout (as the render path); the
+  // counter query walks the reference's binary nodes (its counter semantics)
+  const HitRec h = traverse<!COUNT, COUNT>(sc, mk(ro.x, ro.y, ro.z), mk(rd.x, rd.y, rd.z), rd.w,
+                                           ro.w, &nn, &nt);
   hits[q] = make_float4(h.t, h.u, h.v, __int_as_float(h.k));
   if (COUNT) {
     nodes[q] = nn;
@@ -351,7 +339,7 @@ __global__ void __launch_bounds__(kTraceThreads)
 // frame, 3 draws, BSDF sample, throughput, Russian roulette (4th draw), and
 // the continuation ray is appended to the next queue (warp ballot +
 // one atomic per warp).
-__global__ void __launch_bounds__(kShadeThreads)
+__global__ void __launch_bounds__(kShadeThreads, LT_SHADE_MIN_BLOCKS)
     k_shade(SceneView sc, ShadeArgs sa, PathArrays pa, const float4 *__restrict__ q_o,
             const float4 *__restrict__ q_d, const float4 *__restrict__ hits,
             const int32_t *__restrict__ count_in, float4 *__restrict__ n_o,
@@ -558,6 +546,14 @@ void launch_flatten_nodes(const double *bmin, const double *bmax, const int32_t 
   if (n_internal <= 0) return;
   k_flatten_nodes<<<(unsigned)((n_internal + 255) / 256), 256, 0, st>>>(
       bmin, bmax, left, right, first, count, perm, new_index, n_internal, out);
+}
+
+void launch_flatten_wide(const double *bmin, const double *bmax, const int32_t *first,
+                         const int32_t *count, const int32_t *children, const int32_t *wide_of,
+                         int64_t n_wide, float4 *out, cudaStream_t st) {
+  if (n_wide <= 0) return;
+  k_flatten_wide<<<(unsigned)((n_wide + 255) / 256), 256, 0, st>>>(bmin, bmax, first, count,
+                                                                   children, wide_of, n_wide, out);
 }
 
 void launch_flatten_tris(const double *v0, const double *v1, const double *v2, const double *n0,

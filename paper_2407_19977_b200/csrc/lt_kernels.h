@@ -9,7 +9,17 @@ namespace lt {
 
 constexpr int kTraceThreads = 128;
 constexpr int kShadeThreads = 256;
-constexpr int kShortStack = 16;   // per-lane traversal stack entries in shared memory
+#ifndef LT_SHORT_STACK
+#define LT_SHORT_STACK 16
+#endif
+// resident CTAs per SM the register allocation must allow (occupancy)
+#ifndef LT_TRACE_MIN_BLOCKS
+#define LT_TRACE_MIN_BLOCKS 9
+#endif
+#ifndef LT_SHADE_MIN_BLOCKS
+#define LT_SHADE_MIN_BLOCKS 4
+#endif
+constexpr int kShortStack = LT_SHORT_STACK;  // per-lane traversal stack entries in shared memory
 
 struct PathArrays {
   float4 *T;           // throughput rgb
@@ -46,6 +56,9 @@ void launch_flatten_nodes(const double *bmin, const double *bmax, const int32_t 
                           const int32_t *right, const int32_t *first, const int32_t *count,
                           const int32_t *perm, const int32_t *new_index, int64_t n_internal,
                           float4 *out, cudaStream_t st);
+void launch_flatten_wide(const double *bmin, const double *bmax, const int32_t *first,
+                         const int32_t *count, const int32_t *children, const int32_t *wide_of,
+                         int64_t n_wide, float4 *out, cudaStream_t st);
 void launch_flatten_tris(const double *v0, const double *v1, const double *v2, const double *n0,
                          const double *n1, const double *n2, const int32_t *mat_index,
                          const int32_t *order, const uint8_t *leaf_end, int64_t n, float4 *tris,

@@ -1,5 +1,15 @@
 // lt_traverse.cuh -- closest-hit BVH traversal (bvh.py:359-425) in fp32.
 //
+// Two node layouts of the same host-built tree (lt_device.cuh):
+//   * BVH2 records (the reference's nodes, children boxes in the parent):
+//     used by the counter query so `traversal_counts_batch` keeps the
+//     reference's per-node semantics;
+//   * BVH4 records: the reference tree collapsed to 4-wide nodes (the same
+//     leaves and boxes; intermediate levels skipped), used by the render and
+//     closest-hit kernels.  The closest hit is a lexicographic minimum over
+//     (t, original triangle index), so the grouping changes work, not
+//     results.
+//
 // Semantics kept from the reference:
 //   * slab test (geometry.py:170-207): a zero direction component gives an
 //     "infinite" inverse (bvh.py:367-369).  The reference's compare/select
@@ -10,8 +20,7 @@
 //     identical except for origins within ~1e-20 of a plane;
 //   * Moller-Trumbore, double sided, |det| <= 1e-9 rejected, inclusive
 //     [t_min, best_t] (geometry.py:138-167), reference term order;
-//   * ties on t go to the lower ORIGINAL triangle index (bvh.py:399), so the
-//     result is independent of traversal order.
+//   * ties on t go to the lower ORIGINAL triangle index (bvh.py:399).
 // Robustness: child exit distances are widened by LT_SLAB_WIDEN (relative
 // 4e-7) so fp32 rounding cannot cull a box the float64 traversal enters.
 #pragma once
@@ -35,23 +44,53 @@ __device__ __forceinline__ float fmax3f(float a, float b, float c) {
   return r;
 }
 
-__device__ __forceinline__ f3 ray_inverse(f3 d) {
-  return f3{fminf(fmaxf(1.f / d.x, -LT_INV_CLAMP), LT_INV_CLAMP),
-            fminf(fmaxf(1.f / d.y, -LT_INV_CLAMP), LT_INV_CLAMP),
-            fminf(fmaxf(1.f / d.z, -LT_INV_CLAMP), LT_INV_CLAMP)};
+// Per-ray constants of the slab test.  `inv` is the clamped inverse
+// direction; with LT_SLAB_FMA the plane distances are one FMA each,
+// t = lo * inv + (-o * inv), whose rounding error is absolute
+// (<= |o * inv| 2^-24 per axis), so `slack` widens the exit distance by
+// that bound (axes with a clamped, "infinite" inverse excluded: their t is
+// exactly 0 or beyond any hit).
+struct RaySlab {
+  f3 o, inv, oinv;
+  float slack;
+};
+
+__device__ __forceinline__ RaySlab ray_slab(f3 o, f3 d) {
+  RaySlab r;
+  r.o = o;
+  r.inv = f3{fminf(fmaxf(1.f / d.x, -LT_INV_CLAMP), LT_INV_CLAMP),
+             fminf(fmaxf(1.f / d.y, -LT_INV_CLAMP), LT_INV_CLAMP),
+             fminf(fmaxf(1.f / d.z, -LT_INV_CLAMP), LT_INV_CLAMP)};
+  r.oinv = f3{-o.x * r.inv.x, -o.y * r.inv.y, -o.z * r.inv.z};
+  const float big = 1e18f;
+  const float ex = fabsf(r.inv.x) < big ? fabsf(r.oinv.x) : 0.f;
+  const float ey = fabsf(r.inv.y) < big ? fabsf(r.oinv.y) : 0.f;
+  const float ez = fabsf(r.inv.z) < big ? fabsf(r.oinv.z) : 0.f;
+  r.slack = fmax3f(ex, ey, ez) * 2.4e-7f;  // 2^-22
+  return r;
 }
 
 // _slab_intersect with a clipped interval [t_min, t_max]
-__device__ __forceinline__ bool slab(f3 o, f3 inv, float lox, float hix, float loy, float hiy,
+__device__ __forceinline__ bool slab(const RaySlab &r, float lox, float hix, float loy, float hiy,
                                      float loz, float hiz, float t_min, float t_max,
                                      float &t_enter) {
-  const float t0x = (lox - o.x) * inv.x, t1x = (hix - o.x) * inv.x;
-  const float t0y = (loy - o.y) * inv.y, t1y = (hiy - o.y) * inv.y;
-  const float t0z = (loz - o.z) * inv.z, t1z = (hiz - o.z) * inv.z;
+#ifdef LT_SLAB_FMA
+  const float t0x = fmaf(lox, r.inv.x, r.oinv.x), t1x = fmaf(hix, r.inv.x, r.oinv.x);
+  const float t0y = fmaf(loy, r.inv.y, r.oinv.y), t1y = fmaf(hiy, r.inv.y, r.oinv.y);
+  const float t0z = fmaf(loz, r.inv.z, r.oinv.z), t1z = fmaf(hiz, r.inv.z, r.oinv.z);
+#else
+  const float t0x = (lox - r.o.x) * r.inv.x, t1x = (hix - r.o.x) * r.inv.x;
+  const float t0y = (loy - r.o.y) * r.inv.y, t1y = (hiy - r.o.y) * r.inv.y;
+  const float t0z = (loz - r.o.z) * r.inv.z, t1z = (hiz - r.o.z) * r.inv.z;
+#endif
   const float tn = fmax3f(fminf(t0x, t1x), fminf(t0y, t1y), fmaxf(fminf(t0z, t1z), t_min));
   const float tf = fmin3f(fmaxf(t0x, t1x), fmaxf(t0y, t1y), fminf(fmaxf(t0z, t1z), t_max));
   t_enter = tn;
+#ifdef LT_SLAB_FMA
+  return tn <= fmaf(tf, LT_SLAB_WIDEN, r.slack);
+#else
   return tn <= tf * LT_SLAB_WIDEN;
+#endif
 }
 
 // _mt_intersect (geometry.py:138-167) against the leaf-ordered record
@@ -83,57 +122,120 @@ __device__ __forceinline__ void mt_test(f3 o, f3 d, float t_min, float4 t0, floa
   }
 }
 
-// Simple per-thread traversal with a local-memory stack: the query kernel
-// (intersect_scene_batch / traversal counts).  The render path uses the
-// persistent kernel in lt_kernels.cu.
+// All triangles of the leaf starting at leaf-order position `first` (the
+// last one carries the end-of-leaf flag).
 template <bool COUNT>
+__device__ __forceinline__ void leaf_test(const SceneView &sc, int64_t k, f3 o, f3 d, float t_min,
+                                          HitRec &best, int32_t &best_orig, int &tests) {
+  while (true) {
+    const float4 t0 = __ldg(&sc.tris[3 * k]);
+    const float4 t1 = __ldg(&sc.tris[3 * k + 1]);
+    const float4 t2 = __ldg(&sc.tris[3 * k + 2]);
+    if (COUNT) ++tests;
+    mt_test(o, d, t_min, t0, t1, t2, (int32_t)k, best, best_orig);
+    if (__float_as_int(t1.w) != 0) break;
+    ++k;
+  }
+}
+
+__device__ __forceinline__ void cswap(float &ka, int32_t &la, float &kb, int32_t &lb) {
+  const bool s = kb < ka;
+  const float tk = s ? kb : ka;
+  const int32_t tl = s ? lb : la;
+  kb = s ? ka : kb;
+  lb = s ? la : lb;
+  ka = tk;
+  la = tl;
+}
+
+// One BVH4 node visit: test the four child boxes against [t_min, best_t],
+// sort the hits by entry distance (5-comparator network) and return them
+// nearest first in (l0..l3) with +inf keys for misses / empty slots.
+struct Hits4 {
+  float k0, k1, k2, k3;
+  int32_t l0, l1, l2, l3;
+};
+
+__device__ __forceinline__ Hits4 visit4(const float4 *__restrict__ np, const RaySlab &rs, float t_min,
+                                        float t_max) {
+  const float kInf = __int_as_float(0x7f800000);
+  const float4 lx = __ldg(np + 0), hx = __ldg(np + 1), ly = __ldg(np + 2), hy = __ldg(np + 3);
+  const float4 lz = __ldg(np + 4), hz = __ldg(np + 5);
+  const int4 ln = __ldg(reinterpret_cast<const int4 *>(np + 6));
+  Hits4 h;
+  float t;
+  h.k0 = slab(rs,lx.x, hx.x, ly.x, hy.x, lz.x, hz.x, t_min, t_max, t) && ln.x != LT_LINK_EXIT
+             ? t : kInf;
+  h.k1 = slab(rs,lx.y, hx.y, ly.y, hy.y, lz.y, hz.y, t_min, t_max, t) && ln.y != LT_LINK_EXIT
+             ? t : kInf;
+  h.k2 = slab(rs,lx.z, hx.z, ly.z, hy.z, lz.z, hz.z, t_min, t_max, t) && ln.z != LT_LINK_EXIT
+             ? t : kInf;
+  h.k3 = slab(rs,lx.w, hx.w, ly.w, hy.w, lz.w, hz.w, t_min, t_max, t) && ln.w != LT_LINK_EXIT
+             ? t : kInf;
+  h.l0 = ln.x;
+  h.l1 = ln.y;
+  h.l2 = ln.z;
+  h.l3 = ln.w;
+  cswap(h.k0, h.l0, h.k1, h.l1);
+  cswap(h.k2, h.l2, h.k3, h.l3);
+  cswap(h.k0, h.l0, h.k2, h.l2);
+  cswap(h.k1, h.l1, h.k3, h.l3);
+  cswap(h.k1, h.l1, h.k2, h.l2);
+  return h;
+}
+
+// Per-thread traversal with a local-memory stack for the query kernels.
+// WIDE: the BVH4 layout (closest-hit queries); otherwise the BVH2 layout
+// with the reference's counters (traversal_counts_batch).
+template <bool WIDE, bool COUNT>
 __device__ __forceinline__ HitRec traverse(const SceneView &sc, f3 o, f3 d, float t_min,
                                            float t_max, int *n_nodes, int *n_tests) {
-  const f3 inv = ray_inverse(d);
+  const float kInf = __int_as_float(0x7f800000);
+  const RaySlab rs = ray_slab(o, d);
   HitRec best{t_max, 0.f, 0.f, -1};
   int32_t best_orig = 0x7fffffff;
   int nodes = 1, tests = 0;
   float t_root;
-  if (slab(o, inv, sc.root_lo[0], sc.root_hi[0], sc.root_lo[1], sc.root_hi[1], sc.root_lo[2],
+  if (slab(rs,sc.root_lo[0], sc.root_hi[0], sc.root_lo[1], sc.root_hi[1], sc.root_lo[2],
            sc.root_hi[2], t_min, t_max, t_root)) {
     int32_t stk_node[LT_STACK];
     float stk_t[LT_STACK];
     int sp = 0;
-    int32_t node = sc.root_link;
+    int32_t node = WIDE ? sc.wroot_link : sc.root_link;
     while (true) {
       while (node >= 0) {
-        const float4 *np = sc.nodes + 4 * (int64_t)node;
-        const float4 a = __ldg(np + 0), b = __ldg(np + 1), c = __ldg(np + 2), e = __ldg(np + 3);
-        if (COUNT) nodes += 2;
-        float tl, tr;
-        const bool hl = slab(o, inv, a.x, a.y, a.z, a.w, c.x, c.y, t_min, best.t, tl);
-        const bool hr = slab(o, inv, b.x, b.y, b.z, b.w, c.z, c.w, t_min, best.t, tr);
-        const int32_t lc = __float_as_int(e.x), rc = __float_as_int(e.y);
-        if (hl && hr) {
-          const bool left_near = tl <= tr;  // bvh.py:414
-          stk_node[sp] = left_near ? rc : lc;
-          stk_t[sp] = left_near ? tr : tl;
-          ++sp;
-          node = left_near ? lc : rc;
-        } else if (hl) {
-          node = lc;
-        } else if (hr) {
-          node = rc;
+        if (WIDE) {
+          const Hits4 h = visit4(sc.wnodes + 8 * (int64_t)node, rs, t_min, best.t);
+          if (COUNT) nodes += 4;
+          if (h.k3 < kInf) { stk_node[sp] = h.l3; stk_t[sp] = h.k3; ++sp; }
+          if (h.k2 < kInf) { stk_node[sp] = h.l2; stk_t[sp] = h.k2; ++sp; }
+          if (h.k1 < kInf) { stk_node[sp] = h.l1; stk_t[sp] = h.k1; ++sp; }
+          node = h.k0 < kInf ? h.l0 : LT_LINK_EXIT;
         } else {
-          node = LT_LINK_EXIT;
+          const float4 *np = sc.nodes + 4 * (int64_t)node;
+          const float4 a = __ldg(np + 0), b = __ldg(np + 1), c = __ldg(np + 2), e = __ldg(np + 3);
+          if (COUNT) nodes += 2;
+          float tl, tr;
+          const bool hl = slab(rs,a.x, a.y, a.z, a.w, c.x, c.y, t_min, best.t, tl);
+          const bool hr = slab(rs,b.x, b.y, b.z, b.w, c.z, c.w, t_min, best.t, tr);
+          const int32_t lc = __float_as_int(e.x), rc = __float_as_int(e.y);
+          if (hl && hr) {
+            const bool left_near = tl <= tr;  // bvh.py:414
+            stk_node[sp] = left_near ? rc : lc;
+            stk_t[sp] = left_near ? tr : tl;
+            ++sp;
+            node = left_near ? lc : rc;
+          } else if (hl) {
+            node = lc;
+          } else if (hr) {
+            node = rc;
+          } else {
+            node = LT_LINK_EXIT;
+          }
         }
       }
-      if (node != LT_LINK_EXIT) {
-        int64_t k = ~node;
-        while (true) {
-          const float4 t0 = __ldg(&sc.tris[3 * k]), t1 = __ldg(&sc.tris[3 * k + 1]),
-                       t2 = __ldg(&sc.tris[3 * k + 2]);
-          if (COUNT) ++tests;
-          mt_test(o, d, t_min, t0, t1, t2, (int32_t)k, best, best_orig);
-          if (__float_as_int(t1.w) != 0) break;
-          ++k;
-        }
-      }
+      if (node != LT_LINK_EXIT) leaf_test<COUNT>(sc, ~(int64_t)node, o, d, t_min, best,
+                                                 best_orig, tests);
       const float cull = best.t * LT_SLAB_WIDEN;
       node = LT_LINK_EXIT;
       while (sp > 0) {
