@@ -351,6 +351,9 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
 
     # roofline of the dominant kernel (closest-hit traversal), this rank
     peak, peak_src = measured_peak()
+    from paper_2407_19977_b200._lib import read_bandwidth
+    l2_gbs = read_bandwidth(local_rank, 32 << 20, 200)     # 32 MB: L2-resident
+    hbm_probe = read_bandwidth(local_rank, 4 << 30, 5)      # 4 GB: HBM
     trace_ms = st["trace_ms"]
     launches = max(1, st["trace_launches"])
     achieved = (st["rays"] * bytes_per_ray) / (trace_ms / 1e3) / 1e9 if trace_ms > 0 else None
@@ -365,6 +368,11 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         "tri_tests_per_ray": tri_per_ray, "trace_launches_per_step": launches,
         "trace_ms_per_step": trace_ms, "trace_share_of_step": trace_ms / (ms / args.steps),
         "peak_source": peak_src, "traffic_source": traffic_src,
+        "l2_read_gbs_measured": l2_gbs, "frac_of_l2": achieved / l2_gbs if achieved else None,
+        "hbm_read_gbs_probe": hbm_probe,
+        "note": "the traversal set (wide nodes + leaf triangles, ~70 MB at 1 M tris) is held "
+                "in L2 (persisting window), so algorithmic bytes per second can exceed the HBM "
+                "copy peak; frac_of_l2 is the fraction of the measured L2 streaming-read rate",
     }
 
     # end to end through the public API: scene upload (pinned host arrays),

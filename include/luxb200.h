@@ -171,6 +171,12 @@ int lt_trace_paths_host(lt_scene *scene, const double *origins, const double *di
  * (h*w*3) float32 device -> sRGB u8 (h*w*3) device ---- */
 int lt_tonemap_u8(const float *linear, int64_t n_pixels, uint8_t *out, void *stream);
 
+/* ---- measurement helper (not on the render path): streaming-read
+ * bandwidth of a `bytes` device buffer, `iters` passes, CUDA events.  A
+ * buffer smaller than L2 measures L2 bandwidth (the roofline denominator for
+ * the L2-resident traversal set), a large one HBM. ---- */
+int lt_read_bandwidth(int32_t device, int64_t bytes, int32_t iters, double *gbps);
+
 #ifdef __cplusplus
 }
 #endif

@@ -118,7 +118,15 @@ SIGNATURES = {
     "lt_trace_paths_host": (C.c_int, [C.c_void_p, _dp, _dp, _up, _up, C.c_int64, C.c_int32,
                                       C.c_int32, C.c_double, _dp, _up]),
     "lt_tonemap_u8": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
+    "lt_read_bandwidth": (C.c_int, [C.c_int32, C.c_int64, C.c_int32, C.POINTER(C.c_double)]),
 }
+
+
+def read_bandwidth(device: int, nbytes: int, iters: int = 20) -> float:
+    """GB/s of a streaming read over an `nbytes` device buffer."""
+    g = C.c_double()
+    check(lib().lt_read_bandwidth(int(device), int(nbytes), int(iters), C.byref(g)))
+    return float(g.value)
 
 _lib = None
 

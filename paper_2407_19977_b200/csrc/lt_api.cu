@@ -47,7 +47,12 @@ int lt_fail(int code, const char *fmt, ...) {
 
 namespace {
 
-constexpr int64_t kDefaultBatchPaths = int64_t(1) << 22;  // 4M paths (~512 MB of queues)
+// Paths per wavefront batch.  Large batches amortize the drain tail of every
+// persistent trace launch (the last, longest rays of a bounce run on a few
+// lanes while the rest of the GPU idles): 4M -> 64M paths took the C4 step
+// from 452 to 277 ms (profiles/r01_batch_sweep.jsonl).  128 B of queues and
+// path state per path: 64M paths = 8 GB, bounded by a quarter of free HBM.
+constexpr int64_t kMaxBatchPaths = int64_t(1) << 26;
 constexpr int32_t kMaxBfsNodes = 2048;                    // BFS-ordered top of the tree
 
 struct DevBuf {
@@ -140,6 +145,7 @@ struct lt_scene {
   int trace_grid[2] = {0, 0};  // [no smem, smem]
   int shade_grid = 0;
   int smem_nodes = 0;
+  int64_t default_batch = int64_t(1) << 22;
   // stats of the last pass
   lt_render_stats stats{};
   std::vector<cudaEvent_t> ev_pool;
@@ -330,6 +336,11 @@ static int configure_launches(lt_scene *s) {
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, trace_kernel_ptr(top, false),
                                                      kTraceThreads, smem));
     s->trace_grid[v] = std::max(1, blocks) * s->sm_count;
+  }
+  size_t free_b = 0, total_b = 0;
+  if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
+    const int64_t by_mem = (int64_t)(free_b / 4 / 128);
+    s->default_batch = std::max<int64_t>(int64_t(1) << 20, std::min(kMaxBatchPaths, by_mem));
   }
   int blocks = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, shade_kernel_ptr(), kShadeThreads, 0));
@@ -705,7 +716,8 @@ static int render_impl(lt_scene *s, const lt_render_params *p, float *accum, uin
   int64_t n_local = 0;
   RET(pixel_set(s, p, &pix_list, &n_local));
   if (n_local == 0 || p->sample_count == 0) return LT_OK;
-  const int64_t B = p->max_batch_paths > 0 ? p->max_batch_paths : kDefaultBatchPaths;
+  const int64_t B = std::min(p->max_batch_paths > 0 ? p->max_batch_paths : s->default_batch,
+                             kMaxBatchPaths);
   const int64_t pix_chunk = std::min(n_local, B);
   const int64_t spb = std::min<int64_t>(std::max<int64_t>(1, B / pix_chunk), p->sample_count);
   RET(ensure_workspace(s, pix_chunk * spb, p->max_depth));
@@ -943,6 +955,39 @@ extern "C" int lt_trace_paths_host(lt_scene *s, const double *origins, const dou
   CK(cudaMemcpyAsync(rgb, d_rgb, 24 * n, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(state_out, d_sout, 8 * n, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  return LT_OK;
+}
+
+extern "C" int lt_read_bandwidth(int32_t device, int64_t bytes, int32_t iters, double *gbps) {
+  if (!gbps || bytes < 1024 || iters < 1) return lt_fail(LT_ERR_INVALID, "invalid probe arguments");
+  DeviceGuard g(device);
+  int sms = 0;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  DevBuf buf, sink;
+  RET(buf.ensure((size_t)bytes));
+  RET(sink.ensure(4096));
+  CK(cudaMemset(buf.p, 0, (size_t)bytes));
+  cudaStream_t st;
+  CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int64_t n4 = bytes / 16;
+  const int grid = sms * 4;
+  for (int w = 0; w < 3; ++w) launch_read_probe(buf.as<float4>(), n4, sink.as<float>(), grid, st);
+  cudaEventRecord(e0, st);
+  for (int i = 0; i < iters; ++i) launch_read_probe(buf.as<float4>(), n4, sink.as<float>(), grid, st);
+  cudaEventRecord(e1, st);
+  cudaError_t e = cudaEventSynchronize(e1);
+  float ms = 0.f;
+  if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaStreamDestroy(st);
+  buf.release();
+  sink.release();
+  if (e != cudaSuccess) return lt_fail(LT_ERR_CUDA, "probe failed: %s", cudaGetErrorString(e));
+  *gbps = (double)bytes * iters / (ms * 1e-3) / 1e9;
   return LT_OK;
 }
 

@@ -531,6 +531,30 @@ __global__ void k_tonemap_u8(const float *__restrict__ lin, int64_t n_pixels,
   }
 }
 
+// ------------------------------------------------------------------ probe
+
+// Streaming read of `n4` float4 (grid-stride, 4 independent loads in flight
+// per thread); the bandwidth probe behind lt_read_bandwidth.
+__global__ void k_read_probe(const float4 *__restrict__ src, int64_t n4, float *__restrict__ sink) {
+  float acc = 0.f;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < n4; i += 4 * stride) {
+    const float4 a = __ldcg(src + i), b = __ldcg(src + i + stride);
+    const float4 c = __ldcg(src + i + 2 * stride), d = __ldcg(src + i + 3 * stride);
+    acc += a.x + a.w + b.y + b.z + c.x + c.w + d.y + d.z;
+  }
+  for (; i < n4; i += stride) {
+    const float4 a = __ldcg(src + i);
+    acc += a.x + a.w;
+  }
+  if (acc == 123.456f) sink[threadIdx.x] = acc;  // keeps the loads alive
+}
+
+void launch_read_probe(const float4 *src, int64_t n4, float *sink, int grid, cudaStream_t st) {
+  k_read_probe<<<grid, 512, 0, st>>>(src, n4, sink);
+}
+
 // ------------------------------------------------------------------ launchers
 
 const void *trace_kernel_ptr(bool smem, bool count) {

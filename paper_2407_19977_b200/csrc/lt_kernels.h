@@ -90,5 +90,6 @@ void launch_pack_rays_f64(const double *o, const double *d, int64_t n, float t_m
 void launch_unpack_hits(const SceneView &sc, const float4 *hits, int64_t n, int32_t *idx32,
                         float *t32, int64_t *idx64, double *t64, cudaStream_t st);
 void launch_tonemap_u8(const float *lin, int64_t n_pixels, uint8_t *out, cudaStream_t st);
+void launch_read_probe(const float4 *src, int64_t n4, float *sink, int grid, cudaStream_t st);
 
 }  // namespace lt
