@@ -79,6 +79,10 @@ typedef struct lt_scene_info {
   int64_t n_triangles, n_nodes, n_internal, n_smem_nodes;
   int64_t device_bytes;         /* resident scene bytes in HBM */
   int32_t sm_count;
+  int64_t n_wide;               /* 4-wide nodes of the render layout */
+  int64_t l2_persist_bytes;     /* persisting-L2 limit set for the scene (0: none) */
+  int64_t l2_window_bytes;      /* access-policy window of the trace launches */
+  int64_t default_batch_paths;  /* paths per wavefront batch when not overridden */
 } lt_scene_info;
 
 /* One render pass: `_render_pass(..., sample_start, sample_count, cam, width,

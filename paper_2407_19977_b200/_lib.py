@@ -69,6 +69,8 @@ class SceneInfo(C.Structure):
         ("n_triangles", C.c_int64), ("n_nodes", C.c_int64), ("n_internal", C.c_int64),
         ("n_smem_nodes", C.c_int64), ("device_bytes", C.c_int64),
         ("sm_count", C.c_int32),
+        ("n_wide", C.c_int64), ("l2_persist_bytes", C.c_int64), ("l2_window_bytes", C.c_int64),
+        ("default_batch_paths", C.c_int64),
     ]
 
 

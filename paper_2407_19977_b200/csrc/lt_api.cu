@@ -129,7 +129,8 @@ struct lt_scene {
   size_t nodes_bytes = 0, geo_bytes = 0;
   int64_t n_wide = 0;
   bool use_window = false;
-  cudaAccessPolicyWindow window{};
+  cudaAccessPolicyWindow window{}, shade_window{};
+  size_t persist_bytes = 0;
   // wavefront workspace
   int64_t cap = 0;
   int32_t depth_cap = 0;
@@ -352,17 +353,30 @@ static int configure_launches(lt_scene *s) {
   cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, s->device);
   s->use_window = !(pe && pe[0] == '0') && max_persist > 0 && max_window > 0;
   if (s->use_window) {
-    const size_t limit = std::min<size_t>((size_t)max_persist, s->geo_bytes);
+    // geo = [wide nodes | triangles | shading]; trace launches keep
+    // [nodes, triangles] persisting, shade launches [triangles, shading]
+    const size_t tri_bytes = 48 * (size_t)s->n_tris;
+    const size_t trace_bytes = s->nodes_bytes + tri_bytes;
+    const size_t shade_bytes = 2 * tri_bytes;
+    const size_t limit =
+        std::min<size_t>((size_t)max_persist, std::max(trace_bytes, shade_bytes));
     size_t cur = 0;
     cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
     if (cur < limit) CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, limit));
     cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
-    const size_t win = std::min<size_t>((size_t)max_window, s->geo_bytes);
-    s->window.base_ptr = s->geo.p;
-    s->window.num_bytes = win;
-    s->window.hitRatio = win > 0 ? (float)std::min(1.0, (double)cur / (double)win) : 0.f;
-    s->window.hitProp = cudaAccessPropertyPersisting;
-    s->window.missProp = cudaAccessPropertyStreaming;
+    s->persist_bytes = cur;
+    auto make = [&](void *base, size_t bytes) {
+      cudaAccessPolicyWindow w{};
+      const size_t win = std::min<size_t>((size_t)max_window, bytes);
+      w.base_ptr = base;
+      w.num_bytes = win;
+      w.hitRatio = win > 0 ? (float)std::min(1.0, (double)cur / (double)win) : 0.f;
+      w.hitProp = cudaAccessPropertyPersisting;
+      w.missProp = cudaAccessPropertyStreaming;
+      return w;
+    };
+    s->window = make(s->geo.p, trace_bytes);
+    s->shade_window = make(static_cast<char *>(s->geo.p) + s->nodes_bytes, shade_bytes);
   }
   return LT_OK;
 }
@@ -464,17 +478,17 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
     if ((rc = upload(t_order, d->triangle_order, n, st))) break;
     if ((rc = upload(t_end, leaf_end.data(), n, st))) break;
     s->nodes_bytes = (size_t)std::max<int64_t>(1, s->n_wide) * 128;
-    s->geo_bytes = s->nodes_bytes + 48 * (size_t)n;
+    s->geo_bytes = s->nodes_bytes + 96 * (size_t)n;
     if ((rc = s->geo.ensure(s->geo_bytes))) break;
-    if ((rc = s->shade.ensure(48 * n))) break;
     if ((rc = s->nodes2.ensure((size_t)std::max<int64_t>(1, s->n_internal) * 64))) break;
     float4 *g_wide = s->geo.as<float4>();
     float4 *g_tris = g_wide + s->nodes_bytes / 16;
+    float4 *g_shade = g_tris + 3 * n;
     float4 *g_nodes = s->nodes2.as<float4>();
     launch_flatten_tris(t_v[0].as<double>(), t_v[1].as<double>(), t_v[2].as<double>(),
                         t_v[3].as<double>(), t_v[4].as<double>(), t_v[5].as<double>(),
                         t_mat.as<int32_t>(), t_order.as<int32_t>(), t_end.as<uint8_t>(), n,
-                        g_tris, s->shade.as<float4>(), st);
+                        g_tris, g_shade, st);
     if (s->n_internal > 0) {
       if ((rc = upload(t_bmin, d->bounds_min, 3 * nn, st))) break;
       if ((rc = upload(t_bmax, d->bounds_max, 3 * nn, st))) break;
@@ -529,7 +543,7 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
   v.wroot_link = is_leaf(0) ? ~d->first_triangle[0] : 0;
   v.nodes = s->nodes2.as<float4>();
   v.tris = s->geo.as<float4>() + s->nodes_bytes / 16;
-  v.shade = s->shade.as<float4>();
+  v.shade = v.tris + 3 * n;
   v.mats = s->mats.as<GpuMaterial>();
   v.env_map = s->env.as<float4>();
   v.root_link = is_leaf(0) ? ~d->first_triangle[0] : 0;
@@ -590,6 +604,10 @@ extern "C" int lt_scene_info_get(const lt_scene *s, lt_scene_info *info) {
   info->n_smem_nodes = s->smem_nodes;
   info->device_bytes = s->device_bytes;
   info->sm_count = s->sm_count;
+  info->n_wide = s->n_wide;
+  info->l2_persist_bytes = s->use_window ? (int64_t)s->persist_bytes : 0;
+  info->l2_window_bytes = s->use_window ? (int64_t)s->window.num_bytes : 0;
+  info->default_batch_paths = s->default_batch;
   return LT_OK;
 }
 
@@ -649,9 +667,10 @@ static int run_bounces(lt_scene *s, int32_t max_depth, int32_t rr_start, float t
                     s->ray_ctr.as<unsigned long long>(), st));
     if (flags & LT_FLAG_PROFILE) RET(record_event(s, st));
     ShadeArgs sa{depth, max_depth, rr_start, t_min};
-    launch_shade(sc, sa, pa, s->shade_grid, s->q_o[cur].as<float4>(), s->q_d[cur].as<float4>(),
-                 s->hits.as<float4>(), ctr + depth, s->q_o[cur ^ 1].as<float4>(),
-                 s->q_d[cur ^ 1].as<float4>(), ctr + depth + 1, st);
+    CK(launch_shade(sc, sa, pa, s->shade_grid, s->use_window ? &s->shade_window : nullptr,
+                    s->q_o[cur].as<float4>(), s->q_d[cur].as<float4>(), s->hits.as<float4>(),
+                    ctr + depth, s->q_o[cur ^ 1].as<float4>(), s->q_d[cur ^ 1].as<float4>(),
+                    ctr + depth + 1, st));
     s->stats.kernel_launches += 2;
     s->stats.trace_launches += 1;
     cur ^= 1;
@@ -974,9 +993,13 @@ extern "C" int lt_read_bandwidth(int32_t device, int64_t bytes, int32_t iters, d
   cudaEventCreate(&e1);
   const int64_t n4 = bytes / 16;
   const int grid = sms * 4;
-  for (int w = 0; w < 3; ++w) launch_read_probe(buf.as<float4>(), n4, sink.as<float>(), grid, st);
+  // enough passes per launch that launch overhead is < 1% of the time
+  const int passes = (int)std::max<int64_t>(1, std::min<int64_t>(64, (int64_t(1) << 31) / bytes));
+  for (int w = 0; w < 2; ++w)
+    launch_read_probe(buf.as<float4>(), n4, passes, sink.as<float>(), grid, st);
   cudaEventRecord(e0, st);
-  for (int i = 0; i < iters; ++i) launch_read_probe(buf.as<float4>(), n4, sink.as<float>(), grid, st);
+  for (int i = 0; i < iters; ++i)
+    launch_read_probe(buf.as<float4>(), n4, passes, sink.as<float>(), grid, st);
   cudaEventRecord(e1, st);
   cudaError_t e = cudaEventSynchronize(e1);
   float ms = 0.f;
@@ -987,7 +1010,7 @@ extern "C" int lt_read_bandwidth(int32_t device, int64_t bytes, int32_t iters, d
   buf.release();
   sink.release();
   if (e != cudaSuccess) return lt_fail(LT_ERR_CUDA, "probe failed: %s", cudaGetErrorString(e));
-  *gbps = (double)bytes * iters / (ms * 1e-3) / 1e9;
+  *gbps = (double)bytes * passes * iters / (ms * 1e-3) / 1e9;
   return LT_OK;
 }
 

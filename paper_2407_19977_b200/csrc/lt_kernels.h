@@ -77,10 +77,10 @@ cudaError_t launch_trace(const SceneView &sc, bool smem, bool count_work, int gr
                          unsigned long long *ray_ctr, cudaStream_t st);
 void launch_trace_rays(const SceneView &sc, const float4 *q_o, const float4 *q_d, int64_t n,
                        float4 *hits, int32_t *nodes, int32_t *tests, cudaStream_t st);
-void launch_shade(const SceneView &sc, const ShadeArgs &sa, const PathArrays &pa, int grid,
-                  const float4 *q_o, const float4 *q_d, const float4 *hits,
-                  const int32_t *count_in, float4 *n_o, float4 *n_d, int32_t *count_out,
-                  cudaStream_t st);
+cudaError_t launch_shade(const SceneView &sc, const ShadeArgs &sa, const PathArrays &pa, int grid,
+                         const cudaAccessPolicyWindow *window, const float4 *q_o,
+                         const float4 *q_d, const float4 *hits, const int32_t *count_in,
+                         float4 *n_o, float4 *n_d, int32_t *count_out, cudaStream_t st);
 void launch_accumulate(const AccumArgs &aa, const float4 *L, float *accum, uint32_t *valid,
                        uint32_t *invalid, cudaStream_t st);
 void launch_pack_rays_f32(const float *o, const float *d, int64_t n, float t_min, float t_max,
@@ -90,6 +90,7 @@ void launch_pack_rays_f64(const double *o, const double *d, int64_t n, float t_m
 void launch_unpack_hits(const SceneView &sc, const float4 *hits, int64_t n, int32_t *idx32,
                         float *t32, int64_t *idx64, double *t64, cudaStream_t st);
 void launch_tonemap_u8(const float *lin, int64_t n_pixels, uint8_t *out, cudaStream_t st);
-void launch_read_probe(const float4 *src, int64_t n4, float *sink, int grid, cudaStream_t st);
+void launch_read_probe(const float4 *src, int64_t n4, int passes, float *sink, int grid,
+                       cudaStream_t st);
 
 }  // namespace lt
