@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -116,6 +117,40 @@ struct DeviceGuard {
 
 }  // namespace
 
+// The wavefront queues and path state (up to 8 GB at the default batch) are
+// cached per device and shared by every scene on it, so creating a scene per
+// render call (the reference's render_progressive does) never re-allocates
+// them.  Users serialize on `mu` while enqueueing and on the `last_use` event
+// on the device: a pass on another stream waits for the previous pass.
+struct Workspace {
+  std::mutex mu;
+  int64_t cap = 0;
+  int32_t depth_cap = 0;
+  DevBuf q_o[2], q_d[2], hits, T, L, rng, counters;
+  cudaEvent_t last_use = nullptr;
+};
+
+static Workspace *workspace_for(int device) {
+  static std::mutex g_mu;
+  static std::vector<Workspace *> g_ws;
+  std::lock_guard<std::mutex> lk(g_mu);
+  if ((int)g_ws.size() <= device) g_ws.resize(device + 1, nullptr);
+  if (!g_ws[device]) g_ws[device] = new Workspace();  // process lifetime
+  return g_ws[device];
+}
+
+// Enqueue-side exclusive use of a device workspace on stream `st`.
+struct WorkspaceLease {
+  Workspace *ws;
+  cudaStream_t st;
+  std::unique_lock<std::mutex> lk;
+  WorkspaceLease(Workspace *w, cudaStream_t s) : ws(w), st(s), lk(w->mu) {
+    if (!ws->last_use) cudaEventCreateWithFlags(&ws->last_use, cudaEventDisableTiming);
+    else cudaStreamWaitEvent(st, ws->last_use, 0);
+  }
+  ~WorkspaceLease() { cudaEventRecord(ws->last_use, st); }
+};
+
 struct lt_scene {
   int device = 0;
   int sm_count = 0;
@@ -130,11 +165,11 @@ struct lt_scene {
   int64_t n_wide = 0;
   bool use_window = false;
   cudaAccessPolicyWindow window{}, shade_window{};
+  bool use_shade_window = false;
   size_t persist_bytes = 0;
-  // wavefront workspace
-  int64_t cap = 0;
-  int32_t depth_cap = 0;
-  DevBuf q_o[2], q_d[2], hits, T, L, rng, counters, ray_ctr;
+  // wavefront workspace: shared per device (see Workspace)
+  struct Workspace *ws = nullptr;
+  DevBuf ray_ctr;
   // sharding pixel list cache
   DevBuf pix_list;
   int64_t pix_key[5] = {-1, -1, -1, -1, -1};
@@ -312,9 +347,7 @@ static void destroy_scene(lt_scene *s) {
   if (!s) return;
   DeviceGuard g(s->device);
   if (s->stream) cudaStreamSynchronize(s->stream);
-  for (DevBuf *b : {&s->geo, &s->nodes2, &s->shade, &s->mats, &s->env, &s->q_o[0], &s->q_o[1],
-                    &s->q_d[0], &s->q_d[1], &s->hits, &s->T, &s->L, &s->rng, &s->counters,
-                    &s->ray_ctr, &s->pix_list, &s->s_a, &s->s_b, &s->s_c, &s->s_d, &s->s_e,
+  for (DevBuf *b : {&s->geo, &s->nodes2, &s->shade, &s->mats, &s->env, &s->ray_ctr, &s->pix_list, &s->s_a, &s->s_b, &s->s_c, &s->s_d, &s->s_e,
                     &s->s_f})
     b->release();
   s->h_stage.release();
@@ -358,8 +391,10 @@ static int configure_launches(lt_scene *s) {
     const size_t tri_bytes = 48 * (size_t)s->n_tris;
     const size_t trace_bytes = s->nodes_bytes + tri_bytes;
     const size_t shade_bytes = 2 * tri_bytes;
-    const size_t limit =
-        std::min<size_t>((size_t)max_persist, std::max(trace_bytes, shade_bytes));
+    const char *se = std::getenv("LT_L2_SHADE");
+    s->use_shade_window = se && se[0] == '1';
+    const size_t limit = std::min<size_t>(
+        (size_t)max_persist, s->use_shade_window ? std::max(trace_bytes, shade_bytes) : trace_bytes);
     size_t cur = 0;
     cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
     if (cur < limit) CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, limit));
@@ -386,6 +421,7 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
   CK(cudaSetDevice(device));
   CK(cudaDeviceGetAttribute(&s->sm_count, cudaDevAttrMultiProcessorCount, device));
   CK(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+  s->ws = workspace_for(device);
   cudaStream_t st = s->stream;
   const int64_t n = d->n_triangles, nn = d->n_nodes;
   s->n_tris = n;
@@ -614,27 +650,27 @@ extern "C" int lt_scene_info_get(const lt_scene *s, lt_scene_info *info) {
 // ------------------------------------------------------------------ workspace
 
 static int ensure_workspace(lt_scene *s, int64_t cap, int32_t max_depth) {
-  if (cap > s->cap) {
+  if (cap > s->ws->cap) {
     for (int k = 0; k < 2; ++k) {
-      RET(s->q_o[k].ensure(16 * cap));
-      RET(s->q_d[k].ensure(16 * cap));
+      RET(s->ws->q_o[k].ensure(16 * cap));
+      RET(s->ws->q_d[k].ensure(16 * cap));
     }
-    RET(s->hits.ensure(16 * cap));
-    RET(s->T.ensure(16 * cap));
-    RET(s->L.ensure(16 * cap));
-    RET(s->rng.ensure(16 * cap));
-    s->cap = cap;
+    RET(s->ws->hits.ensure(16 * cap));
+    RET(s->ws->T.ensure(16 * cap));
+    RET(s->ws->L.ensure(16 * cap));
+    RET(s->ws->rng.ensure(16 * cap));
+    s->ws->cap = cap;
   }
-  if (max_depth > s->depth_cap) {
-    RET(s->counters.ensure(sizeof(int32_t) * (2 * (size_t)max_depth + 2)));
-    s->depth_cap = max_depth;
+  if (max_depth > s->ws->depth_cap) {
+    RET(s->ws->counters.ensure(sizeof(int32_t) * (2 * (size_t)max_depth + 2)));
+    s->ws->depth_cap = max_depth;
   }
   RET(s->ray_ctr.ensure(3 * sizeof(unsigned long long)));
   return LT_OK;
 }
 
 static PathArrays path_arrays(lt_scene *s) {
-  return PathArrays{s->T.as<float4>(), s->L.as<float4>(), s->rng.as<ulonglong2>()};
+  return PathArrays{s->ws->T.as<float4>(), s->ws->L.as<float4>(), s->ws->rng.as<ulonglong2>()};
 }
 
 static int record_event(lt_scene *s, cudaStream_t st) {
@@ -655,21 +691,22 @@ static int run_bounces(lt_scene *s, int32_t max_depth, int32_t rr_start, float t
   const bool smem = !(flags & LT_FLAG_NO_SMEM_TOP) && s->smem_nodes > 0;
   SceneView sc = s->view;
   sc.n_top = smem ? s->smem_nodes : 0;
-  int32_t *ctr = s->counters.as<int32_t>();
+  int32_t *ctr = s->ws->counters.as<int32_t>();
   int32_t *fetch = ctr + max_depth + 1;
   const PathArrays pa = path_arrays(s);
   int cur = 0;
   for (int32_t depth = 0; depth < max_depth; ++depth) {
     if (flags & LT_FLAG_PROFILE) RET(record_event(s, st));
     CK(launch_trace(sc, smem, (flags & LT_FLAG_COUNT) != 0, s->trace_grid[smem ? 1 : 0],
-                    s->use_window ? &s->window : nullptr, s->q_o[cur].as<float4>(),
-                    s->q_d[cur].as<float4>(), ctr + depth, fetch + depth, s->hits.as<float4>(),
+                    s->use_window ? &s->window : nullptr, s->ws->q_o[cur].as<float4>(),
+                    s->ws->q_d[cur].as<float4>(), ctr + depth, fetch + depth, s->ws->hits.as<float4>(),
                     s->ray_ctr.as<unsigned long long>(), st));
     if (flags & LT_FLAG_PROFILE) RET(record_event(s, st));
     ShadeArgs sa{depth, max_depth, rr_start, t_min};
-    CK(launch_shade(sc, sa, pa, s->shade_grid, s->use_window ? &s->shade_window : nullptr,
-                    s->q_o[cur].as<float4>(), s->q_d[cur].as<float4>(), s->hits.as<float4>(),
-                    ctr + depth, s->q_o[cur ^ 1].as<float4>(), s->q_d[cur ^ 1].as<float4>(),
+    CK(launch_shade(sc, sa, pa, s->shade_grid,
+                    s->use_window && s->use_shade_window ? &s->shade_window : nullptr,
+                    s->ws->q_o[cur].as<float4>(), s->ws->q_d[cur].as<float4>(), s->ws->hits.as<float4>(),
+                    ctr + depth, s->ws->q_o[cur ^ 1].as<float4>(), s->ws->q_d[cur ^ 1].as<float4>(),
                     ctr + depth + 1, st));
     s->stats.kernel_launches += 2;
     s->stats.trace_launches += 1;
@@ -739,11 +776,12 @@ static int render_impl(lt_scene *s, const lt_render_params *p, float *accum, uin
                              kMaxBatchPaths);
   const int64_t pix_chunk = std::min(n_local, B);
   const int64_t spb = std::min<int64_t>(std::max<int64_t>(1, B / pix_chunk), p->sample_count);
+  WorkspaceLease lease(s->ws, st);
   RET(ensure_workspace(s, pix_chunk * spb, p->max_depth));
   CK(cudaMemsetAsync(s->ray_ctr.p, 0, 3 * sizeof(unsigned long long), st));
   const float t_min = (float)p->t_min;
   const PathArrays pa = path_arrays(s);
-  int32_t *ctr = s->counters.as<int32_t>();
+  int32_t *ctr = s->ws->counters.as<int32_t>();
   for (int64_t s0 = 0; s0 < p->sample_count; s0 += spb) {
     const int64_t ns = std::min(spb, p->sample_count - s0);
     for (int64_t pc0 = 0; pc0 < n_local; pc0 += pix_chunk) {
@@ -760,10 +798,10 @@ static int render_impl(lt_scene *s, const lt_render_params *p, float *accum, uin
       ra.pix_list = pix_list;
       ra.n_paths = np * ns;
       ra.t_min = t_min;
-      launch_raygen(ra, pa, s->q_o[0].as<float4>(), s->q_d[0].as<float4>(), ctr, st);
+      launch_raygen(ra, pa, s->ws->q_o[0].as<float4>(), s->ws->q_d[0].as<float4>(), ctr, st);
       RET(run_bounces(s, p->max_depth, p->rr_start, t_min, p->flags, st));
       AccumArgs aa{np, pc0, ns, pix_list};
-      launch_accumulate(aa, s->L.as<float4>(), accum, valid, invalid, st);
+      launch_accumulate(aa, s->ws->L.as<float4>(), accum, valid, invalid, st);
       s->stats.kernel_launches += 2;
       s->stats.batches += 1;
       s->stats.paths += np * ns;
@@ -950,6 +988,7 @@ extern "C" int lt_trace_paths_host(lt_scene *s, const double *origins, const dou
   cudaStream_t st = s->stream;
   s->stats = lt_render_stats{};
   s->ev_used = 0;
+  WorkspaceLease lease(s->ws, st);
   RET(ensure_workspace(s, n, max_depth));
   RET(s->s_a.ensure(64 * n));
   double *d_o = s->s_a.as<double>();
@@ -960,11 +999,11 @@ extern "C" int lt_trace_paths_host(lt_scene *s, const double *origins, const dou
   CK(cudaMemcpyAsync(d_d, dirs, 24 * n, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(d_state, state, 8 * n, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(d_inc, inc, 8 * n, cudaMemcpyHostToDevice, st));
-  CK(cudaMemsetAsync(s->counters.p, 0, sizeof(int32_t) * (2 * (size_t)max_depth + 2), st));
+  CK(cudaMemsetAsync(s->ws->counters.p, 0, sizeof(int32_t) * (2 * (size_t)max_depth + 2), st));
   CK(cudaMemsetAsync(s->ray_ctr.p, 0, 3 * sizeof(unsigned long long), st));
   const PathArrays pa = path_arrays(s);
-  launch_raygen_explicit(d_o, d_d, d_state, d_inc, n, (float)t_min, pa, s->q_o[0].as<float4>(),
-                         s->q_d[0].as<float4>(), s->counters.as<int32_t>(), st);
+  launch_raygen_explicit(d_o, d_d, d_state, d_inc, n, (float)t_min, pa, s->ws->q_o[0].as<float4>(),
+                         s->ws->q_d[0].as<float4>(), s->ws->counters.as<int32_t>(), st);
   RET(run_bounces(s, max_depth, rr_start, (float)t_min, 0u, st));
   RET(s->s_b.ensure(32 * n));
   double *d_rgb = s->s_b.as<double>();
