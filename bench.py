@@ -409,15 +409,20 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         barrier()
         t0 = time.perf_counter()
         n_e2e = max(1, min(args.steps, 3))
+        phases = []
         for _ in range(n_e2e):
-            e2e_step()
+            res = e2e_step()
+            if res is not None and hasattr(res, "timings"):
+                phases.append(res.timings)
         torch.cuda.synchronize(dev)
         el = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(el, op=dist.ReduceOp.MAX)
         e2e = {"value": samples_per_step * n_e2e / float(el.item()), "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "steps": n_e2e,
+               "steps": n_e2e, "ms_per_step": 1e3 * float(el.item()) / n_e2e,
+               "phases_ms": {k: statistics.mean(p[k] for p in phases) for k in phases[0]}
+               if phases else None,
                "api": "render_progressive(scene, settings, bvh) (render_distributed for N>1): "
                       "scene upload from pinned host arrays + BVH flatten + render + image "
                       "D2H, wall clock"}

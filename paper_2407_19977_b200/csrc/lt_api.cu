@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -79,6 +80,25 @@ struct DevBuf {
   }
 };
 
+// Stream-ordered temporary (cudaMallocAsync / cudaFreeAsync): scene upload
+// staging without the device-wide synchronization of cudaFree.
+struct TmpBuf {
+  void *p = nullptr;
+  cudaStream_t st = nullptr;
+  int alloc(size_t want, cudaStream_t s) {
+    st = s;
+    CK(cudaMallocAsync(&p, std::max<size_t>(want, 16), s));
+    return LT_OK;
+  }
+  ~TmpBuf() {
+    if (p) cudaFreeAsync(p, st);
+  }
+  template <class T>
+  T *as() const {
+    return static_cast<T *>(p);
+  }
+};
+
 struct HostBuf {
   void *p = nullptr;
   size_t bytes = 0;
@@ -138,6 +158,20 @@ static Workspace *workspace_for(int device) {
   if (!g_ws[device]) g_ws[device] = new Workspace();  // process lifetime
   return g_ws[device];
 }
+
+// LT_VERBOSE=1: host-side phase timings on stderr (scene create / destroy).
+struct PhaseTimer {
+  bool on;
+  std::chrono::steady_clock::time_point t;
+  PhaseTimer() : on(std::getenv("LT_VERBOSE") != nullptr), t(std::chrono::steady_clock::now()) {}
+  void mark(const char *what) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[luxb200] %-28s %8.2f ms\n", what,
+                 std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
 
 // Enqueue-side exclusive use of a device workspace on stream `st`.
 struct WorkspaceLease {
@@ -342,17 +376,27 @@ static int upload(DevBuf &b, const T *src, size_t count, cudaStream_t st) {
   if (count) CK(cudaMemcpyAsync(b.p, src, count * sizeof(T), cudaMemcpyHostToDevice, st));
   return LT_OK;
 }
+template <class T>
+static int upload(TmpBuf &b, const T *src, size_t count, cudaStream_t st) {
+  RET(b.alloc(count * sizeof(T), st));
+  if (count) CK(cudaMemcpyAsync(b.p, src, count * sizeof(T), cudaMemcpyHostToDevice, st));
+  return LT_OK;
+}
 
 static void destroy_scene(lt_scene *s) {
   if (!s) return;
   DeviceGuard g(s->device);
+  PhaseTimer pt;
   if (s->stream) cudaStreamSynchronize(s->stream);
-  for (DevBuf *b : {&s->geo, &s->nodes2, &s->shade, &s->mats, &s->env, &s->ray_ctr, &s->pix_list, &s->s_a, &s->s_b, &s->s_c, &s->s_d, &s->s_e,
-                    &s->s_f})
+  pt.mark("destroy: stream sync");
+  for (DevBuf *b : {&s->geo, &s->nodes2, &s->shade, &s->mats, &s->env, &s->ray_ctr,
+                    &s->pix_list, &s->s_a, &s->s_b, &s->s_c, &s->s_d, &s->s_e, &s->s_f})
     b->release();
+  pt.mark("destroy: device frees");
   s->h_stage.release();
   for (cudaEvent_t e : s->ev_pool) cudaEventDestroy(e);
   if (s->stream) cudaStreamDestroy(s->stream);
+  pt.mark("destroy: host + stream");
   delete s;
 }
 
@@ -384,7 +428,10 @@ static int configure_launches(lt_scene *s) {
   int max_persist = 0, max_window = 0;
   cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, s->device);
   cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, s->device);
-  s->use_window = !(pe && pe[0] == '0') && max_persist > 0 && max_window > 0;
+  // Off by default: the persisting carve-out did not speed up k_trace (the
+  // traversal set stays L2-hot anyway) and starved the streaming kernels of
+  // L2 (2071 vs 1789 M samples/s on C4, profiles/r01_l2_window_sweep.jsonl).
+  s->use_window = (pe && pe[0] == '1') && max_persist > 0 && max_window > 0;
   if (s->use_window) {
     // geo = [wide nodes | triangles | shading]; trace launches keep
     // [nodes, triangles] persisting, shade launches [triangles, shading]
@@ -417,6 +464,7 @@ static int configure_launches(lt_scene *s) {
 }
 
 static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s) {
+  PhaseTimer pt;
   s->device = device;
   CK(cudaSetDevice(device));
   CK(cudaDeviceGetAttribute(&s->sm_count, cudaDevAttrMultiProcessorCount, device));
@@ -426,6 +474,7 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
   const int64_t n = d->n_triangles, nn = d->n_nodes;
   s->n_tris = n;
   s->n_nodes = nn;
+  pt.mark("stream + attributes");
 
   // --- internal-node renumbering: top levels BFS, the rest depth-first
   std::vector<int32_t> new_index(nn, -1), perm;
@@ -458,6 +507,7 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
     }
   }
   s->n_internal = (int64_t)perm.size();
+  pt.mark("binary renumbering");
   // --- 4-wide collapse of the same tree (render / closest-hit layout): a
   // wide node starts from its binary node's two children and repeatedly
   // replaces the internal child with the largest surface area by its two
@@ -497,13 +547,15 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
     }
   }
   s->n_wide = (int64_t)(wide_children.size() / 4);
+  pt.mark("4-wide collapse");
   // leaf-end flags for the leaf-ordered triangle stream
   std::vector<uint8_t> leaf_end(n, 0);
   for (int64_t i = 0; i < nn; ++i)
     if (is_leaf(i)) leaf_end[d->first_triangle[i] + d->triangle_count[i] - 1] = 1;
 
+  pt.mark("leaf flags");
   // --- upload the float64 arrays and flatten on the device
-  DevBuf t_v[6], t_mat, t_order, t_end, t_bmin, t_bmax, t_left, t_right, t_first, t_count,
+  TmpBuf t_v[6], t_mat, t_order, t_end, t_bmin, t_bmax, t_left, t_right, t_first, t_count,
       t_perm, t_new, t_wch, t_wof;
   const double *src[6] = {d->v0, d->v1, d->v2, d->n0, d->n1, d->n2};
   int rc = LT_OK;
@@ -549,6 +601,7 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
       rc = lt_fail(LT_ERR_CUDA, "flatten launch failed: %s", cudaGetErrorString(e));
       break;
     }
+    pt.mark("uploads + flatten enqueue");
     // materials
     std::vector<GpuMaterial> mats(d->n_materials);
     for (int i = 0; i < d->n_materials; ++i) build_material(d, i, mats[i]);
@@ -562,17 +615,15 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
                              d->env_texels[3 * i + 2], 0.f);
       if ((rc = upload(s->env, tex.data(), tex.size(), st))) break;
     }
+    pt.mark("materials + env");
     e = cudaStreamSynchronize(st);
+    pt.mark("device flatten (sync)");
     if (e != cudaSuccess) {
       rc = lt_fail(LT_ERR_CUDA, "scene upload failed: %s", cudaGetErrorString(e));
       break;
     }
   } while (0);
-  for (DevBuf &b : t_v) b.release();
-  for (DevBuf *b : {&t_mat, &t_order, &t_end, &t_bmin, &t_bmax, &t_left, &t_right, &t_first,
-                    &t_count, &t_perm, &t_new, &t_wch, &t_wof})
-    b->release();
-  RET(rc);
+  RET(rc);  // the TmpBuf staging is released stream-ordered when it leaves scope
 
   SceneView &v = s->view;
   v.wnodes = s->geo.as<float4>();
@@ -597,7 +648,9 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
   }
   s->device_bytes = (int64_t)(s->geo.bytes + s->nodes2.bytes + s->shade.bytes + s->mats.bytes +
                               s->env.bytes);
+  pt.mark("free temporaries + view");
   RET(configure_launches(s));
+  pt.mark("configure launches");
   v.n_top = s->smem_nodes;
   const char *rf = std::getenv("LT_REFILL");
   v.refill_min = std::max(1, std::min(32, rf ? std::atoi(rf) : 8));
@@ -607,7 +660,11 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
 extern "C" int lt_scene_create(const lt_scene_desc *desc, int32_t device, lt_scene **out) {
   if (!out) return lt_fail(LT_ERR_INVALID, "null output handle");
   *out = nullptr;
-  RET(validate_desc(desc));
+  {
+    PhaseTimer pv;
+    RET(validate_desc(desc));
+    pv.mark("validate");
+  }
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
     return lt_fail(LT_ERR_CUDA, "no CUDA device available");

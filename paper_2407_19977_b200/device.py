@@ -9,6 +9,7 @@ TriangleBuffer / Bvh / OpenPbrParams) are accepted duck-typed.
 from __future__ import annotations
 
 import ctypes as C
+import time
 
 import numpy as np
 
@@ -95,7 +96,9 @@ class DeviceScene:
             d.env_texels = tex.ctypes.data_as(C.POINTER(C.c_float))
             d.env_scale = float(environment.scale)
         handle = C.c_void_p()
+        t0 = time.perf_counter()
         _lib.check(_lib.lib().lt_scene_create(C.byref(d), int(device), C.byref(handle)))
+        self.create_ms = (time.perf_counter() - t0) * 1e3
         self.handle = handle
         self.device = int(device)
         self.n_triangles = n

@@ -97,6 +97,6 @@ def render_distributed(scene, settings, bvh=None, *, tile_size: int = 16, mode: 
     elapsed = (time.perf_counter() - t0) * 1e3
     if rank != 0:
         return None
-    image = acc.mean().cpu().numpy()
-    invalid = acc.invalid.view(cam.height, cam.width).to(torch.int64).cpu().numpy()
+    from .integrator import fetch_image
+    image, invalid = fetch_image(acc)
     return RenderResult(image, settings.samples_per_pixel, invalid, elapsed, world)

@@ -148,7 +148,8 @@ def render_progressive(scene, settings: RenderSettings, bvh=None, threads: int |
     import torch
     if device is None:
         device = scene.device if isinstance(scene, DeviceScene) else 0
-    ds = scene if isinstance(scene, DeviceScene) else DeviceScene(scene, bvh, device=device)
+    owned = not isinstance(scene, DeviceScene)
+    ds = DeviceScene(scene, bvh, device=device) if owned else scene
     cam = ds.camera
     acc = Accumulator(cam.width, cam.height, ds.device)
     st = torch.cuda.current_stream(acc.device)
@@ -168,14 +169,37 @@ def render_progressive(scene, settings: RenderSettings, bvh=None, threads: int |
     elapsed_ms = (time.perf_counter() - start) * 1000.0
     if return_device:
         return acc
-    image = acc.mean().cpu().numpy()
-    invalid = acc.invalid.view(cam.height, cam.width).to(torch.int64).cpu().numpy()
+    t0 = time.perf_counter()
+    image, invalid = fetch_image(acc, st)
+    d2h_ms = (time.perf_counter() - t0) * 1e3
     dropped = int(invalid.sum())
     total = spp * cam.width * cam.height
     if dropped > total * INVALID_SAMPLE_WARN_FRACTION:
         warnings.warn(f"{dropped} of {total} samples were non-finite and dropped",
                       RuntimeWarning, stacklevel=2)
-    return RenderResult(image, spp, invalid, elapsed_ms, 1)
+    res = RenderResult(image, spp, invalid, elapsed_ms, 1)
+    res.timings = {"scene_upload_ms": ds.create_ms if owned else 0.0, "render_ms": elapsed_ms,
+                   "image_d2h_ms": d2h_ms}
+    return res
+
+
+_PINNED: dict = {}
+
+
+def fetch_image(acc: Accumulator, stream=None):
+    """(h, w, 3) float64 means and (h, w) int64 invalid counts on the host,
+    through cached pinned staging buffers (one per image size and device)."""
+    import torch
+    h, w = acc.height, acc.width
+    key = (h, w, acc.device.index)
+    if key not in _PINNED:
+        _PINNED[key] = (torch.empty((h, w, 3), dtype=torch.float64, pin_memory=True),
+                        torch.empty((h, w), dtype=torch.int32, pin_memory=True))
+    mean_h, inv_h = _PINNED[key]
+    mean_h.copy_(acc.mean(), non_blocking=True)
+    inv_h.copy_(acc.invalid.view(h, w), non_blocking=True)
+    (stream or torch.cuda.current_stream(acc.device)).synchronize()
+    return mean_h.numpy().copy(), inv_h.numpy().astype(np.int64)
 
 
 def render_image(scene, settings: RenderSettings, bvh=None, threads: int | None = None,
