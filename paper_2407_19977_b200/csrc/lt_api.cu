@@ -57,20 +57,33 @@ namespace {
 constexpr int64_t kMaxBatchPaths = int64_t(1) << 26;
 constexpr int32_t kMaxBfsNodes = 2048;                    // BFS-ordered top of the tree
 
+// Device buffer.  With `ast` set the memory comes stream-ordered from the
+// device's default mempool (cudaMallocAsync / cudaFreeAsync on `ast`), so a
+// scene's lifetime never costs a device-wide cudaFree synchronization (which
+// measured up to 1.5 s per scene destroy on the B200 box).
 struct DevBuf {
   void *p = nullptr;
   size_t bytes = 0;
+  cudaStream_t ast = nullptr;
+  bool stream_ordered = false;
   int ensure(size_t want) {
     if (want <= bytes) return LT_OK;
-    if (p) cudaFree(p);
-    p = nullptr;
-    bytes = 0;
-    CK(cudaMalloc(&p, want));
+    release();
+    if (stream_ordered) {
+      CK(cudaMallocAsync(&p, want, ast));
+      // usable from any stream once the allocation has executed (growth is rare)
+      CK(cudaStreamSynchronize(ast));
+    } else {
+      CK(cudaMalloc(&p, want));
+    }
     bytes = want;
     return LT_OK;
   }
   void release() {
-    if (p) cudaFree(p);
+    if (p) {
+      if (stream_ordered) cudaFreeAsync(p, ast);
+      else cudaFree(p);
+    }
     p = nullptr;
     bytes = 0;
   }
@@ -387,8 +400,14 @@ static void destroy_scene(lt_scene *s) {
   if (!s) return;
   DeviceGuard g(s->device);
   PhaseTimer pt;
-  if (s->stream) cudaStreamSynchronize(s->stream);
-  pt.mark("destroy: stream sync");
+  // every render pass records the workspace event on its stream when it
+  // ends: frees on the scene stream wait for it (no use-after-free when the
+  // caller destroys a scene while its last pass is still in flight)
+  if (s->stream && s->ws) {
+    std::lock_guard<std::mutex> lk(s->ws->mu);
+    if (s->ws->last_use) cudaStreamWaitEvent(s->stream, s->ws->last_use, 0);
+  }
+  pt.mark("destroy: order after last pass");
   for (DevBuf *b : {&s->geo, &s->nodes2, &s->shade, &s->mats, &s->env, &s->ray_ctr,
                     &s->pix_list, &s->s_a, &s->s_b, &s->s_c, &s->s_d, &s->s_e, &s->s_f})
     b->release();
@@ -470,6 +489,19 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
   CK(cudaDeviceGetAttribute(&s->sm_count, cudaDevAttrMultiProcessorCount, device));
   CK(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
   s->ws = workspace_for(device);
+  {
+    // keep stream-ordered scene / staging memory mapped between scenes
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t keep = 4ull << 30;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  }
+  for (DevBuf *b : {&s->geo, &s->nodes2, &s->shade, &s->mats, &s->env, &s->ray_ctr,
+                    &s->pix_list, &s->s_a, &s->s_b, &s->s_c, &s->s_d, &s->s_e, &s->s_f}) {
+    b->stream_ordered = true;
+    b->ast = s->stream;
+  }
   cudaStream_t st = s->stream;
   const int64_t n = d->n_triangles, nn = d->n_nodes;
   s->n_tris = n;

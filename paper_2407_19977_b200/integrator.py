@@ -149,7 +149,9 @@ def render_progressive(scene, settings: RenderSettings, bvh=None, threads: int |
     if device is None:
         device = scene.device if isinstance(scene, DeviceScene) else 0
     owned = not isinstance(scene, DeviceScene)
+    t_scene = time.perf_counter()
     ds = DeviceScene(scene, bvh, device=device) if owned else scene
+    scene_wall_ms = (time.perf_counter() - t_scene) * 1e3
     cam = ds.camera
     acc = Accumulator(cam.width, cam.height, ds.device)
     st = torch.cuda.current_stream(acc.device)
@@ -178,8 +180,13 @@ def render_progressive(scene, settings: RenderSettings, bvh=None, threads: int |
         warnings.warn(f"{dropped} of {total} samples were non-finite and dropped",
                       RuntimeWarning, stacklevel=2)
     res = RenderResult(image, spp, invalid, elapsed_ms, 1)
-    res.timings = {"scene_upload_ms": ds.create_ms if owned else 0.0, "render_ms": elapsed_ms,
+    res.timings = {"scene_create_ms": ds.create_ms if owned else 0.0,
+                   "scene_wall_ms": scene_wall_ms if owned else 0.0, "render_ms": elapsed_ms,
                    "image_d2h_ms": d2h_ms}
+    if owned:
+        t0 = time.perf_counter()
+        ds.close()
+        res.timings["scene_release_ms"] = (time.perf_counter() - t0) * 1e3
     return res
 
 
