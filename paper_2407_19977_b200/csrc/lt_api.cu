@@ -208,7 +208,7 @@ struct lt_scene {
   // nodes and leaf-ordered triangles share one allocation so a single L2
   // access-policy window keeps the whole traversal set persisting
   DevBuf geo, shade, mats, env, nodes2;
-  size_t nodes_bytes = 0, geo_bytes = 0;
+  size_t nodes_bytes = 0, geo_bytes = 0, shade_off = 0;
   int64_t n_wide = 0;
   bool use_window = false;
   cudaAccessPolicyWindow window{}, shade_window{};
@@ -456,7 +456,7 @@ static int configure_launches(lt_scene *s) {
     // [nodes, triangles] persisting, shade launches [triangles, shading]
     const size_t tri_bytes = 48 * (size_t)s->n_tris;
     const size_t trace_bytes = s->nodes_bytes + tri_bytes;
-    const size_t shade_bytes = 2 * tri_bytes;
+    const size_t shade_bytes = s->geo_bytes - s->nodes_bytes;
     const char *se = std::getenv("LT_L2_SHADE");
     s->use_shade_window = se && se[0] == '1';
     const size_t limit = std::min<size_t>(
@@ -598,12 +598,15 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
     if ((rc = upload(t_order, d->triangle_order, n, st))) break;
     if ((rc = upload(t_end, leaf_end.data(), n, st))) break;
     s->nodes_bytes = (size_t)std::max<int64_t>(1, s->n_wide) * 128;
-    s->geo_bytes = s->nodes_bytes + 96 * (size_t)n;
+    // shading records start on a 128 B boundary so each 64 B record is
+    // half of one cache line
+    s->shade_off = (s->nodes_bytes + 48 * (size_t)n + 127) / 128 * 128;
+    s->geo_bytes = s->shade_off + 64 * (size_t)n;
     if ((rc = s->geo.ensure(s->geo_bytes))) break;
     if ((rc = s->nodes2.ensure((size_t)std::max<int64_t>(1, s->n_internal) * 64))) break;
     float4 *g_wide = s->geo.as<float4>();
     float4 *g_tris = g_wide + s->nodes_bytes / 16;
-    float4 *g_shade = g_tris + 3 * n;
+    float4 *g_shade = g_wide + s->shade_off / 16;
     float4 *g_nodes = s->nodes2.as<float4>();
     launch_flatten_tris(t_v[0].as<double>(), t_v[1].as<double>(), t_v[2].as<double>(),
                         t_v[3].as<double>(), t_v[4].as<double>(), t_v[5].as<double>(),
@@ -662,7 +665,7 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
   v.wroot_link = is_leaf(0) ? ~d->first_triangle[0] : 0;
   v.nodes = s->nodes2.as<float4>();
   v.tris = s->geo.as<float4>() + s->nodes_bytes / 16;
-  v.shade = v.tris + 3 * n;
+  v.shade = s->geo.as<float4>() + s->shade_off / 16;
   v.mats = s->mats.as<GpuMaterial>();
   v.env_map = s->env.as<float4>();
   v.root_link = is_leaf(0) ? ~d->first_triangle[0] : 0;
@@ -773,30 +776,33 @@ static int record_event(lt_scene *s, cudaStream_t st) {
 }
 
 // The bounce loop of _trace (integrator.py:160-226) over the whole queue:
-// trace -> shade per segment; queue 0 must already hold the primary rays and
-// counters[0] their number.
+// trace -> shade per segment.  With `primary` the depth-0 launches generate
+// the camera rays themselves (render batches); otherwise queue 0 must hold
+// the primary rays and counters[0] their number (explicit rays).
 static int run_bounces(lt_scene *s, int32_t max_depth, int32_t rr_start, float t_min,
-                       uint32_t flags, cudaStream_t st) {
+                       uint32_t flags, cudaStream_t st, const RaygenArgs *primary = nullptr) {
   const bool smem = !(flags & LT_FLAG_NO_SMEM_TOP) && s->smem_nodes > 0;
   SceneView sc = s->view;
   sc.n_top = smem ? s->smem_nodes : 0;
-  int32_t *ctr = s->ws->counters.as<int32_t>();
+  Workspace *ws = s->ws;
+  int32_t *ctr = ws->counters.as<int32_t>();
   int32_t *fetch = ctr + max_depth + 1;
   const PathArrays pa = path_arrays(s);
   int cur = 0;
   for (int32_t depth = 0; depth < max_depth; ++depth) {
+    const RaygenArgs *prim = depth == 0 ? primary : nullptr;
     if (flags & LT_FLAG_PROFILE) RET(record_event(s, st));
     CK(launch_trace(sc, smem, (flags & LT_FLAG_COUNT) != 0, s->trace_grid[smem ? 1 : 0],
-                    s->use_window ? &s->window : nullptr, s->ws->q_o[cur].as<float4>(),
-                    s->ws->q_d[cur].as<float4>(), ctr + depth, fetch + depth, s->ws->hits.as<float4>(),
-                    s->ray_ctr.as<unsigned long long>(), st));
+                    s->use_window ? &s->window : nullptr, prim, ws->q_o[cur].as<float4>(),
+                    ws->q_d[cur].as<float4>(), ctr + depth, fetch + depth,
+                    ws->hits.as<float4>(), s->ray_ctr.as<unsigned long long>(), st));
     if (flags & LT_FLAG_PROFILE) RET(record_event(s, st));
-    ShadeArgs sa{depth, max_depth, rr_start, t_min};
+    ShadeArgs sa{depth, max_depth, rr_start, t_min, 0};
     CK(launch_shade(sc, sa, pa, s->shade_grid,
-                    s->use_window && s->use_shade_window ? &s->shade_window : nullptr,
-                    s->ws->q_o[cur].as<float4>(), s->ws->q_d[cur].as<float4>(), s->ws->hits.as<float4>(),
-                    ctr + depth, s->ws->q_o[cur ^ 1].as<float4>(), s->ws->q_d[cur ^ 1].as<float4>(),
-                    ctr + depth + 1, st));
+                    s->use_window && s->use_shade_window ? &s->shade_window : nullptr, prim,
+                    ws->q_o[cur].as<float4>(), ws->q_d[cur].as<float4>(),
+                    ws->hits.as<float4>(), ctr + depth, ws->q_o[cur ^ 1].as<float4>(),
+                    ws->q_d[cur ^ 1].as<float4>(), ctr + depth + 1, st));
     s->stats.kernel_launches += 2;
     s->stats.trace_launches += 1;
     cur ^= 1;
@@ -887,11 +893,11 @@ static int render_impl(lt_scene *s, const lt_render_params *p, float *accum, uin
       ra.pix_list = pix_list;
       ra.n_paths = np * ns;
       ra.t_min = t_min;
-      launch_raygen(ra, pa, s->ws->q_o[0].as<float4>(), s->ws->q_d[0].as<float4>(), ctr, st);
-      RET(run_bounces(s, p->max_depth, p->rr_start, t_min, p->flags, st));
+      // camera rays are generated inside the depth-0 trace / shade launches
+      RET(run_bounces(s, p->max_depth, p->rr_start, t_min, p->flags, st, &ra));
       AccumArgs aa{np, pc0, ns, pix_list};
       launch_accumulate(aa, s->ws->L.as<float4>(), accum, valid, invalid, st);
-      s->stats.kernel_launches += 2;
+      s->stats.kernel_launches += 1;
       s->stats.batches += 1;
       s->stats.paths += np * ns;
     }

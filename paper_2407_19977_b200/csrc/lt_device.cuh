@@ -20,8 +20,9 @@
 //   tris   : 3 x float4 per triangle in LEAF order (reference triangle_order)
 //              (v0.xyz, original index), (e1.xyz, last-in-leaf flag),
 //              (e2.xyz, 0); e1/e2 are rounded from the float64 differences.
-//   shade  : 3 x float4 per triangle in leaf order
-//              (n0.xyz, material index), (n1.xyz, 0), (n2.xyz, 0)
+//   shade  : 4 x float4 (64 B, one aligned half line) per triangle in leaf
+//            order: (g.xyz = float64 normalize(e1 x e2), material index),
+//            (n0.xyz, 0), (n1.xyz, 0), (n2.xyz, 0)
 //   mats   : 128-byte GpuMaterial records, derived constants precomputed in
 //            float64 on the host and rounded once.
 #pragma once
@@ -177,18 +178,13 @@ __device__ __forceinline__ f3 env_radiance(const SceneView &sc, f3 d) {
 }
 
 // --------------------------------------------------------------- hit frame
-// _hit_frame (geometry.py:210-241) from the stored e1/e2 and vertex normals
-__device__ __forceinline__ void hit_frame(f3 d, f3 e1, f3 e2, f3 n0, f3 n1, f3 n2, float u,
-                                          float v, f3 &g, f3 &s, bool &front) {
-  float gx = e1.y * e2.z - e1.z * e2.y;
-  float gy = e1.z * e2.x - e1.x * e2.z;
-  float gz = e1.x * e2.y - e1.y * e2.x;
-  float glen = sqrtf(gx * gx + gy * gy + gz * gz);
-  if (glen > 0.f) {
-    gx /= glen;
-    gy /= glen;
-    gz /= glen;
-  }
+// _hit_frame (geometry.py:210-241).  The unit geometric normal g0 =
+// normalize(e1 x e2) is precomputed per triangle in float64 at upload (the
+// reference's float64 value, rounded once); orientation, interpolation of
+// the vertex normals and the hemisphere flip happen here per hit.
+__device__ __forceinline__ void hit_frame(f3 d, f3 g0, f3 n0, f3 n1, f3 n2, float u, float v,
+                                          f3 &g, f3 &s, bool &front) {
+  float gx = g0.x, gy = g0.y, gz = g0.z;
   front = (gx * d.x + gy * d.y + gz * d.z) < 0.f;
   if (!front) {
     gx = -gx;

@@ -100,35 +100,59 @@ __global__ void k_flatten_tris(const double *__restrict__ v0, const double *__re
                                 __int_as_float(leaf_end[k] ? 1 : 0));
   tris[3 * k + 2] =
       make_float4((float)(c[0] - a[0]), (float)(c[1] - a[1]), (float)(c[2] - a[2]), 0.f);
+  // geometric normal as _hit_frame computes it (geometry.py:217-224), float64
+  const double e1x = b[0] - a[0], e1y = b[1] - a[1], e1z = b[2] - a[2];
+  const double e2x = c[0] - a[0], e2y = c[1] - a[1], e2z = c[2] - a[2];
+  double gx = e1y * e2z - e1z * e2y;
+  double gy = e1z * e2x - e1x * e2z;
+  double gz = e1x * e2y - e1y * e2x;
+  const double glen = sqrt(gx * gx + gy * gy + gz * gz);
+  if (glen > 0.0) {
+    gx /= glen;
+    gy /= glen;
+    gz /= glen;
+  }
   const double *p0 = n0 + 3 * ti, *p1 = n1 + 3 * ti, *p2 = n2 + 3 * ti;
-  shade[3 * k + 0] =
-      make_float4((float)p0[0], (float)p0[1], (float)p0[2], __int_as_float(mat_index[ti]));
-  shade[3 * k + 1] = make_float4((float)p1[0], (float)p1[1], (float)p1[2], 0.f);
-  shade[3 * k + 2] = make_float4((float)p2[0], (float)p2[1], (float)p2[2], 0.f);
+  shade[4 * k + 0] =
+      make_float4((float)gx, (float)gy, (float)gz, __int_as_float(mat_index[ti]));
+  shade[4 * k + 1] = make_float4((float)p0[0], (float)p0[1], (float)p0[2], 0.f);
+  shade[4 * k + 2] = make_float4((float)p1[0], (float)p1[1], (float)p1[2], 0.f);
+  shade[4 * k + 3] = make_float4((float)p2[0], (float)p2[1], (float)p2[2], 0.f);
 }
 
 // ------------------------------------------------------------------ raygen
 
-// Primary rays for paths p = s_local * n_pix + i (sample-major), keyed by the
-// GLOBAL pixel index and sample index (integrator.py:253-258).
-__global__ void k_raygen(RaygenArgs ra, PathArrays pa, float4 *__restrict__ q_o,
-                         float4 *__restrict__ q_d, int32_t *__restrict__ count0) {
-  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (p == 0) *count0 = (int32_t)ra.n_paths;
-  if (p >= ra.n_paths) return;
+// Primary ray of path p = s_local * n_pix + i (sample-major), keyed by the
+// GLOBAL pixel index and sample index (integrator.py:253-258): stream seed,
+// two jitter draws, float64 pinhole direction.  Evaluated where it is
+// consumed (the depth-0 trace and shade launches), so primary rays never
+// round-trip through HBM; returns the PCG state after the two draws.
+__device__ __forceinline__ void primary_ray(const RaygenArgs &ra, int64_t p, f3 &o, f3 &d,
+                                            uint64_t &state, uint64_t &inc) {
   const int64_t s_local = p / ra.n_pix;
   const int64_t i = p - s_local * ra.n_pix;
   const int64_t pix = ra.pix_list ? (int64_t)ra.pix_list[ra.pix_offset + i] : ra.pix_offset + i;
   const int64_t sample = ra.sample_base + s_local;
   const int64_t py = pix / ra.width;
   const int64_t px = pix - py * ra.width;
-  uint64_t state, inc;
   seed_stream((uint64_t)pix, (uint64_t)sample, ra.seed, state, inc);
   const double jx = unit_f64(state, inc);
   const double jy = unit_f64(state, inc);
-  const f3 d = camera_dir(ra.cam, (double)px, (double)py, jx, jy, ra.width, ra.height);
-  q_o[p] = make_float4((float)ra.cam[0], (float)ra.cam[1], (float)ra.cam[2],
-                       __int_as_float((int32_t)p));
+  d = camera_dir(ra.cam, (double)px, (double)py, jx, jy, ra.width, ra.height);
+  o = f3{(float)ra.cam[0], (float)ra.cam[1], (float)ra.cam[2]};
+}
+
+// Materialized primary rays (kept for the ray-dump debug path; the render
+// loop generates them in place).
+__global__ void k_raygen(RaygenArgs ra, PathArrays pa, float4 *__restrict__ q_o,
+                         float4 *__restrict__ q_d, int32_t *__restrict__ count0) {
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p == 0) *count0 = (int32_t)ra.n_paths;
+  if (p >= ra.n_paths) return;
+  f3 o, d;
+  uint64_t state, inc;
+  primary_ray(ra, p, o, d, state, inc);
+  q_o[p] = make_float4(o.x, o.y, o.z, __int_as_float((int32_t)p));
   q_d[p] = make_float4(d.x, d.y, d.z, ra.t_min);
   pa.T[p] = make_float4(1.f, 1.f, 1.f, 0.f);
   pa.L[p] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -182,9 +206,10 @@ __global__ void k_gather_explicit(PathArrays pa, int64_t n, double *__restrict__
 // ray_ctr[2] += triangle tests.
 template <bool USE_SMEM, bool COUNT>
 __global__ void __launch_bounds__(kTraceThreads, LT_TRACE_MIN_BLOCKS)
-    k_trace(SceneView sc, const float4 *__restrict__ q_o, const float4 *__restrict__ q_d,
-            const int32_t *__restrict__ count, int32_t *__restrict__ fetch,
-            float4 *__restrict__ hits, unsigned long long *__restrict__ ray_ctr) {
+    k_trace(SceneView sc, RaygenArgs ra, int primary, const float4 *__restrict__ q_o,
+            const float4 *__restrict__ q_d, const int32_t *__restrict__ count,
+            int32_t *__restrict__ fetch, float4 *__restrict__ hits,
+            unsigned long long *__restrict__ ray_ctr) {
   // (USE_SMEM: the top-level staging variant measured slower than L1
   // caching -- profiles/r01_sweep -- and is kept only as a launch option.)
   extern __shared__ float4 s_mem[];
@@ -196,7 +221,8 @@ __global__ void __launch_bounds__(kTraceThreads, LT_TRACE_MIN_BLOCKS)
   int32_t l_node[LT_STACK - kShortStack];
   float l_t[LT_STACK - kShortStack];
 
-  const int n = *count;
+  // primary launch (depth 0 of a render batch): rays generated in place
+  const int n = primary ? (int)ra.n_paths : *count;
   if (blockIdx.x == 0 && tid == 0) atomicAdd(ray_ctr, (unsigned long long)n);
 
   int q = -1;
@@ -224,11 +250,17 @@ __global__ void __launch_bounds__(kTraceThreads, LT_TRACE_MIN_BLOCKS)
         const int r = base + __popc(idle & lanes_below);
         if (r < n) {
           q = r;
-          const float4 ro = __ldcs(&q_o[r]);
-          const float4 rd = __ldcs(&q_d[r]);
-          o = mk(ro.x, ro.y, ro.z);
-          d = mk(rd.x, rd.y, rd.z);
-          t_min = rd.w;
+          if (primary) {
+            uint64_t st_, inc_;
+            primary_ray(ra, r, o, d, st_, inc_);
+            t_min = ra.t_min;
+          } else {
+            const float4 ro = __ldcs(&q_o[r]);
+            const float4 rd = __ldcs(&q_d[r]);
+            o = mk(ro.x, ro.y, ro.z);
+            d = mk(rd.x, rd.y, rd.z);
+            t_min = rd.w;
+          }
           rs = ray_slab(o, d);
           best = HitRec{__int_as_float(0x7f800000), 0.f, 0.f, -1};
           best_orig = 0x7fffffff;
@@ -340,11 +372,14 @@ __global__ void __launch_bounds__(kTraceThreads)
 // the continuation ray is appended to the next queue (warp ballot +
 // one atomic per warp).
 __global__ void __launch_bounds__(kShadeThreads, LT_SHADE_MIN_BLOCKS)
-    k_shade(SceneView sc, ShadeArgs sa, PathArrays pa, const float4 *__restrict__ q_o,
-            const float4 *__restrict__ q_d, const float4 *__restrict__ hits,
-            const int32_t *__restrict__ count_in, float4 *__restrict__ n_o,
-            float4 *__restrict__ n_d, int32_t *__restrict__ count_out) {
-  const int n = *count_in;
+    k_shade(SceneView sc, ShadeArgs sa, RaygenArgs ra, PathArrays pa,
+            const float4 *__restrict__ q_o, const float4 *__restrict__ q_d,
+            const float4 *__restrict__ hits, const int32_t *__restrict__ count_in,
+            float4 *__restrict__ n_o, float4 *__restrict__ n_d, int32_t *__restrict__ count_out) {
+  // primary launch (depth 0 of a render batch): queue slot == path id, the
+  // ray and its PCG state are regenerated here instead of read back
+  const bool primary = sa.primary != 0;
+  const int n = primary ? (int)ra.n_paths : *count_in;
   const int lane = threadIdx.x & 31;
   for (int base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
     const int q = base + threadIdx.x;
@@ -352,34 +387,49 @@ __global__ void __launch_bounds__(kShadeThreads, LT_SHADE_MIN_BLOCKS)
     float4 out_o, out_d;
     if (q < n) {
       // queue entries and path state stream through (evict-first) so the
-      // L2 keeps the triangle / shading records (persisting window)
-      const float4 ro = __ldcs(&q_o[q]);
-      const float4 rd = __ldcs(&q_d[q]);
+      // L2 keeps the triangle / shading records
       const float4 h = __ldcs(&hits[q]);
-      const int32_t p = __float_as_int(ro.w);
       const int32_t k = __float_as_int(h.w);
-      const f3 d = mk(rd.x, rd.y, rd.z);
-      const float4 T = __ldcs(&pa.T[p]);
-      float4 L = __ldcs(&pa.L[p]);
+      int32_t p;
+      f3 o, d;
+      float4 T, L;
+      ulonglong2 rs{};
+      if (primary) {
+        p = q;
+        uint64_t st0, inc0;
+        primary_ray(ra, q, o, d, st0, inc0);
+        rs = make_ulonglong2(st0, inc0);
+        T = make_float4(1.f, 1.f, 1.f, 0.f);
+        L = make_float4(0.f, 0.f, 0.f, 0.f);
+      } else {
+        const float4 ro = __ldcs(&q_o[q]);
+        const float4 rd = __ldcs(&q_d[q]);
+        p = __float_as_int(ro.w);
+        o = mk(ro.x, ro.y, ro.z);
+        d = mk(rd.x, rd.y, rd.z);
+        T = __ldcs(&pa.T[p]);
+        L = __ldcs(&pa.L[p]);
+      }
+      bool wrote_l = false;
       if (k < 0) {
         const f3 e = env_radiance(sc, d);
         L.x += T.x * e.x;
         L.y += T.y * e.y;
         L.z += T.z * e.z;
         __stcs(&pa.L[p], L);
+        wrote_l = true;
       } else {
-        // issue every random load of this hit before using any of them
-        const int64_t k3 = 3 * (int64_t)k;
+        // issue every random load of this hit before using any of them: one
+        // 64 B shading record (geometric normal + material, vertex normals)
+        const int64_t k4 = 4 * (int64_t)k;
         const bool scatter = sa.depth != sa.max_depth - 1;
-        const float4 s0 = __ldg(&sc.shade[k3]);
-        float4 e1{}, e2{}, s1{}, s2{};
-        ulonglong2 rs{};
+        const float4 s0 = __ldg(&sc.shade[k4]);
+        float4 s1{}, s2{}, s3{};
         if (scatter) {
-          e1 = __ldg(&sc.tris[k3 + 1]);
-          e2 = __ldg(&sc.tris[k3 + 2]);
-          s1 = __ldg(&sc.shade[k3 + 1]);
-          s2 = __ldg(&sc.shade[k3 + 2]);
-          rs = __ldcs(&pa.rng[p]);
+          s1 = __ldg(&sc.shade[k4 + 1]);
+          s2 = __ldg(&sc.shade[k4 + 2]);
+          s3 = __ldg(&sc.shade[k4 + 3]);
+          if (!primary) rs = __ldcs(&pa.rng[p]);
         }
         const int32_t mi = __float_as_int(s0.w);
         const GpuMaterial &mt = sc.mats[mi];
@@ -388,12 +438,13 @@ __global__ void __launch_bounds__(kShadeThreads, LT_SHADE_MIN_BLOCKS)
           L.y += T.y * mt.el * mt.ec[1];
           L.z += T.z * mt.el * mt.ec[2];
           __stcs(&pa.L[p], L);
+          wrote_l = true;
         }
         if (scatter) {
           f3 g, sn;
           bool front;
-          hit_frame(d, mk(e1.x, e1.y, e1.z), mk(e2.x, e2.y, e2.z), mk(s0.x, s0.y, s0.z),
-                    mk(s1.x, s1.y, s1.z), mk(s2.x, s2.y, s2.z), h.y, h.z, g, sn, front);
+          hit_frame(d, mk(s0.x, s0.y, s0.z), mk(s1.x, s1.y, s1.z), mk(s2.x, s2.y, s2.z),
+                    mk(s3.x, s3.y, s3.z), h.y, h.z, g, sn, front);
           uint64_t state = rs.x;
           const uint64_t inc = rs.y;
           const float u_lobe = unit_f32(state, inc);
@@ -424,12 +475,15 @@ __global__ void __launch_bounds__(kShadeThreads, LT_SHADE_MIN_BLOCKS)
           if (alive) {
             __stcs(&pa.T[p], Tn);
             const float t = h.x;
-            out_o = make_float4(ro.x + t * d.x, ro.y + t * d.y, ro.z + t * d.z, ro.w);
+            out_o = make_float4(o.x + t * d.x, o.y + t * d.y, o.z + t * d.z, __int_as_float(p));
             out_d = make_float4(wi.x, wi.y, wi.z, sa.t_min);
             emit = true;
           }
         }
       }
+      // the radiance slot of every path is written by its primary launch
+      // (raygen no longer clears it)
+      if (primary && !wrote_l) __stcs(&pa.L[p], L);
     }
     // warp-aggregated append to the next queue
     const unsigned mask = __ballot_sync(kFull, emit);
@@ -627,9 +681,12 @@ size_t trace_smem_bytes(int n_top) {
 }
 
 cudaError_t launch_trace(const SceneView &sc, bool smem, bool count_work, int grid,
-                         const cudaAccessPolicyWindow *window, const float4 *q_o,
-                         const float4 *q_d, const int32_t *count, int32_t *fetch, float4 *hits,
-                         unsigned long long *ray_ctr, cudaStream_t st) {
+                         const cudaAccessPolicyWindow *window, const RaygenArgs *primary,
+                         const float4 *q_o, const float4 *q_d, const int32_t *count,
+                         int32_t *fetch, float4 *hits, unsigned long long *ray_ctr,
+                         cudaStream_t st) {
+  const RaygenArgs ra = primary ? *primary : RaygenArgs{};
+  const int prim = primary ? 1 : 0;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kTraceThreads);
@@ -643,16 +700,16 @@ cudaError_t launch_trace(const SceneView &sc, bool smem, bool count_work, int gr
     cfg.numAttrs = 1;
   }
   if (smem && count_work)
-    return cudaLaunchKernelEx(&cfg, k_trace<true, true>, sc, q_o, q_d, count, fetch, hits,
-                              ray_ctr);
+    return cudaLaunchKernelEx(&cfg, k_trace<true, true>, sc, ra, prim, q_o, q_d, count, fetch,
+                              hits, ray_ctr);
   if (smem)
-    return cudaLaunchKernelEx(&cfg, k_trace<true, false>, sc, q_o, q_d, count, fetch, hits,
-                              ray_ctr);
+    return cudaLaunchKernelEx(&cfg, k_trace<true, false>, sc, ra, prim, q_o, q_d, count, fetch,
+                              hits, ray_ctr);
   if (count_work)
-    return cudaLaunchKernelEx(&cfg, k_trace<false, true>, sc, q_o, q_d, count, fetch, hits,
-                              ray_ctr);
-  return cudaLaunchKernelEx(&cfg, k_trace<false, false>, sc, q_o, q_d, count, fetch, hits,
-                            ray_ctr);
+    return cudaLaunchKernelEx(&cfg, k_trace<false, true>, sc, ra, prim, q_o, q_d, count, fetch,
+                              hits, ray_ctr);
+  return cudaLaunchKernelEx(&cfg, k_trace<false, false>, sc, ra, prim, q_o, q_d, count, fetch,
+                            hits, ray_ctr);
 }
 
 void launch_trace_rays(const SceneView &sc, const float4 *q_o, const float4 *q_d, int64_t n,
@@ -666,9 +723,13 @@ void launch_trace_rays(const SceneView &sc, const float4 *q_o, const float4 *q_d
 }
 
 cudaError_t launch_shade(const SceneView &sc, const ShadeArgs &sa, const PathArrays &pa, int grid,
-                         const cudaAccessPolicyWindow *window, const float4 *q_o,
-                         const float4 *q_d, const float4 *hits, const int32_t *count_in,
-                         float4 *n_o, float4 *n_d, int32_t *count_out, cudaStream_t st) {
+                         const cudaAccessPolicyWindow *window, const RaygenArgs *primary,
+                         const float4 *q_o, const float4 *q_d, const float4 *hits,
+                         const int32_t *count_in, float4 *n_o, float4 *n_d, int32_t *count_out,
+                         cudaStream_t st) {
+  const RaygenArgs ra = primary ? *primary : RaygenArgs{};
+  ShadeArgs s2 = sa;
+  s2.primary = primary ? 1 : 0;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kShadeThreads);
@@ -680,7 +741,7 @@ cudaError_t launch_shade(const SceneView &sc, const ShadeArgs &sa, const PathArr
     cfg.attrs = attr;
     cfg.numAttrs = 1;
   }
-  return cudaLaunchKernelEx(&cfg, k_shade, sc, sa, pa, q_o, q_d, hits, count_in, n_o, n_d,
+  return cudaLaunchKernelEx(&cfg, k_shade, sc, s2, ra, pa, q_o, q_d, hits, count_in, n_o, n_d,
                             count_out);
 }
 
