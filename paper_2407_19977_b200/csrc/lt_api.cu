@@ -792,8 +792,10 @@ static int run_bounces(lt_scene *s, int32_t max_depth, int32_t rr_start, float t
   for (int32_t depth = 0; depth < max_depth; ++depth) {
     const RaygenArgs *prim = depth == 0 ? primary : nullptr;
     if (flags & LT_FLAG_PROFILE) RET(record_event(s, st));
+    // (in-kernel ray generation for trace measured slower than reading the
+    // 32 B ray record: the float64 camera math serializes the refill path)
     CK(launch_trace(sc, smem, (flags & LT_FLAG_COUNT) != 0, s->trace_grid[smem ? 1 : 0],
-                    s->use_window ? &s->window : nullptr, prim, ws->q_o[cur].as<float4>(),
+                    s->use_window ? &s->window : nullptr, nullptr, ws->q_o[cur].as<float4>(),
                     ws->q_d[cur].as<float4>(), ctr + depth, fetch + depth,
                     ws->hits.as<float4>(), s->ray_ctr.as<unsigned long long>(), st));
     if (flags & LT_FLAG_PROFILE) RET(record_event(s, st));
@@ -893,11 +895,13 @@ static int render_impl(lt_scene *s, const lt_render_params *p, float *accum, uin
       ra.pix_list = pix_list;
       ra.n_paths = np * ns;
       ra.t_min = t_min;
-      // camera rays are generated inside the depth-0 trace / shade launches
+      // raygen writes only the ray records; the depth-0 shade regenerates
+      // throughput / radiance / PCG state
+      launch_raygen(ra, pa, s->ws->q_o[0].as<float4>(), s->ws->q_d[0].as<float4>(), ctr, st);
       RET(run_bounces(s, p->max_depth, p->rr_start, t_min, p->flags, st, &ra));
       AccumArgs aa{np, pc0, ns, pix_list};
       launch_accumulate(aa, s->ws->L.as<float4>(), accum, valid, invalid, st);
-      s->stats.kernel_launches += 1;
+      s->stats.kernel_launches += 2;
       s->stats.batches += 1;
       s->stats.paths += np * ns;
     }

@@ -142,8 +142,21 @@ __device__ __forceinline__ void primary_ray(const RaygenArgs &ra, int64_t p, f3 
   o = f3{(float)ra.cam[0], (float)ra.cam[1], (float)ra.cam[2]};
 }
 
-// Materialized primary rays (kept for the ray-dump debug path; the render
-// loop generates them in place).
+// The PCG state of path p after its two jitter draws (integer only): the
+// depth-0 shade launch regenerates it instead of reading it back.
+__device__ __forceinline__ void primary_rng(const RaygenArgs &ra, int64_t p, uint64_t &state,
+                                            uint64_t &inc) {
+  const int64_t s_local = p / ra.n_pix;
+  const int64_t i = p - s_local * ra.n_pix;
+  const int64_t pix = ra.pix_list ? (int64_t)ra.pix_list[ra.pix_offset + i] : ra.pix_offset + i;
+  seed_stream((uint64_t)pix, (uint64_t)(ra.sample_base + s_local), ra.seed, state, inc);
+  (void)pcg_next(state, inc);
+  (void)pcg_next(state, inc);
+}
+
+// Primary rays of a render batch: only the 32 B ray record is written; the
+// throughput (1), radiance (0) and PCG state are implied / regenerated by
+// the depth-0 shade launch.
 __global__ void k_raygen(RaygenArgs ra, PathArrays pa, float4 *__restrict__ q_o,
                          float4 *__restrict__ q_d, int32_t *__restrict__ count0) {
   const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -152,11 +165,8 @@ __global__ void k_raygen(RaygenArgs ra, PathArrays pa, float4 *__restrict__ q_o,
   f3 o, d;
   uint64_t state, inc;
   primary_ray(ra, p, o, d, state, inc);
-  q_o[p] = make_float4(o.x, o.y, o.z, __int_as_float((int32_t)p));
-  q_d[p] = make_float4(d.x, d.y, d.z, ra.t_min);
-  pa.T[p] = make_float4(1.f, 1.f, 1.f, 0.f);
-  pa.L[p] = make_float4(0.f, 0.f, 0.f, 0.f);
-  pa.rng[p] = make_ulonglong2(state, inc);
+  __stcs(&q_o[p], make_float4(o.x, o.y, o.z, __int_as_float((int32_t)p)));
+  __stcs(&q_d[p], make_float4(d.x, d.y, d.z, ra.t_min));
 }
 
 // Explicit rays with caller-supplied PCG state (trace_radiance,
@@ -376,10 +386,10 @@ __global__ void __launch_bounds__(kShadeThreads, LT_SHADE_MIN_BLOCKS)
             const float4 *__restrict__ q_o, const float4 *__restrict__ q_d,
             const float4 *__restrict__ hits, const int32_t *__restrict__ count_in,
             float4 *__restrict__ n_o, float4 *__restrict__ n_d, int32_t *__restrict__ count_out) {
-  // primary launch (depth 0 of a render batch): queue slot == path id, the
-  // ray and its PCG state are regenerated here instead of read back
+  // primary launch (depth 0 of a render batch): throughput 1, radiance 0 and
+  // the PCG state are regenerated here instead of read back
   const bool primary = sa.primary != 0;
-  const int n = primary ? (int)ra.n_paths : *count_in;
+  const int n = *count_in;
   const int lane = threadIdx.x & 31;
   for (int base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
     const int q = base + threadIdx.x;
@@ -394,19 +404,20 @@ __global__ void __launch_bounds__(kShadeThreads, LT_SHADE_MIN_BLOCKS)
       f3 o, d;
       float4 T, L;
       ulonglong2 rs{};
-      if (primary) {
-        p = q;
-        uint64_t st0, inc0;
-        primary_ray(ra, q, o, d, st0, inc0);
-        rs = make_ulonglong2(st0, inc0);
-        T = make_float4(1.f, 1.f, 1.f, 0.f);
-        L = make_float4(0.f, 0.f, 0.f, 0.f);
-      } else {
+      {
         const float4 ro = __ldcs(&q_o[q]);
         const float4 rd = __ldcs(&q_d[q]);
         p = __float_as_int(ro.w);
         o = mk(ro.x, ro.y, ro.z);
         d = mk(rd.x, rd.y, rd.z);
+      }
+      if (primary) {
+        uint64_t st0, inc0;
+        primary_rng(ra, p, st0, inc0);
+        rs = make_ulonglong2(st0, inc0);
+        T = make_float4(1.f, 1.f, 1.f, 0.f);
+        L = make_float4(0.f, 0.f, 0.f, 0.f);
+      } else {
         T = __ldcs(&pa.T[p]);
         L = __ldcs(&pa.L[p]);
       }
