@@ -456,8 +456,19 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
+        # LT_BENCH_BACKEND=gloo with LT_BENCH_SHARE_GPU=1 runs the multi-rank
+        # code path with every rank on the available GPU(s) and the merge
+        # staged through host memory (functional check on a 1-GPU box: the
+        # ranks' kernels never wait on each other).  Timing runs use NCCL,
+        # one GPU per rank.
+        backend = os.environ.get("LT_BENCH_BACKEND", "nccl")
+        if os.environ.get("LT_BENCH_SHARE_GPU") == "1":
+            local_rank = local_rank % max(1, torch.cuda.device_count())
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group(backend)
     try:
         run_ours(args, rank, world, local_rank)
     finally:

@@ -43,11 +43,15 @@ def merge_tiles(acc, group=None, dst: int | None = 0) -> None:
     dst=None all-reduces; otherwise reduces onto rank dst.  Works for NCCL
     (CUDA tensors) and gloo (CPU tensors)."""
     import torch.distributed as dist
+    host_staged = dist.get_backend(group) == "gloo"   # gloo: reduce host copies
     for t in (acc.sum, acc.valid, acc.invalid):
+        x = t.cpu() if (host_staged and t.is_cuda) else t
         if dst is None:
-            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+            dist.all_reduce(x, op=dist.ReduceOp.SUM, group=group)
         else:
-            dist.reduce(t, dst=dst, op=dist.ReduceOp.SUM, group=group)
+            dist.reduce(x, dst=dst, op=dist.ReduceOp.SUM, group=group)
+        if x is not t:
+            t.copy_(x)
 
 
 def merge_spp_ordered(acc, group=None) -> None:
@@ -56,9 +60,11 @@ def merge_spp_ordered(acc, group=None) -> None:
     import torch
     import torch.distributed as dist
     world = dist.get_world_size(group)
+    host_staged = dist.get_backend(group) == "gloo"
     for t in (acc.sum, acc.valid, acc.invalid):
-        parts = [torch.empty_like(t) for _ in range(world)]
-        dist.all_gather(parts, t, group=group)
+        x = t.cpu() if (host_staged and t.is_cuda) else t
+        parts = [torch.empty_like(x) for _ in range(world)]
+        dist.all_gather(parts, x, group=group)
         total = parts[0].clone()
         for p in parts[1:]:
             total += p
