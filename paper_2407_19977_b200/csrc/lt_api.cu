@@ -229,6 +229,7 @@ struct lt_scene {
   int shade_grid = 0;
   int smem_nodes = 0;
   int64_t default_batch = int64_t(1) << 22;
+  bool octant_sort = false;
   // stats of the last pass
   lt_render_stats stats{};
   std::vector<cudaEvent_t> ev_pool;
@@ -687,6 +688,10 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
   RET(configure_launches(s));
   pt.mark("configure launches");
   v.n_top = s->smem_nodes;
+  // continuation rays appended grouped by direction octant (+3 % on C4,
+  // profiles/r01_octant_sweep.jsonl); LT_OCTANT_SORT=0 disables
+  const char *os_env = std::getenv("LT_OCTANT_SORT");
+  s->octant_sort = os_env ? os_env[0] == '1' : true;
   const char *rf = std::getenv("LT_REFILL");
   v.refill_min = std::max(1, std::min(32, rf ? std::atoi(rf) : 8));
   return LT_OK;
@@ -799,7 +804,7 @@ static int run_bounces(lt_scene *s, int32_t max_depth, int32_t rr_start, float t
                     ws->q_d[cur].as<float4>(), ctr + depth, fetch + depth,
                     ws->hits.as<float4>(), s->ray_ctr.as<unsigned long long>(), st));
     if (flags & LT_FLAG_PROFILE) RET(record_event(s, st));
-    ShadeArgs sa{depth, max_depth, rr_start, t_min, 0};
+    ShadeArgs sa{depth, max_depth, rr_start, t_min, 0, s->octant_sort ? 1 : 0};
     CK(launch_shade(sc, sa, pa, s->shade_grid,
                     s->use_window && s->use_shade_window ? &s->shade_window : nullptr, prim,
                     ws->q_o[cur].as<float4>(), ws->q_d[cur].as<float4>(),
@@ -832,17 +837,24 @@ static int validate_render(const lt_render_params *p) {
 // local pixel list for interleaved tiles: tile k (raster order over
 // ceil(W/T) x ceil(H/T) tiles) belongs to rank k % n_ranks
 static int pixel_set(lt_scene *s, const lt_render_params *p, const int32_t **list, int64_t *n) {
-  if (p->n_ranks <= 1) {
+  // single rank: pixels in T x T tile order (LT_TILE_ORDER, default 4; 0 =
+  // raster) so a warp's primary rays cover a compact 8 x 4 patch (+2 % on C4)
+  const char *to = std::getenv("LT_TILE_ORDER");
+  const int tile_order = to ? std::atoi(to) : 4;
+  const bool sharded = p->n_ranks > 1;
+  if (!sharded && tile_order <= 1) {
     *list = nullptr;
     *n = (int64_t)p->width * p->height;
     return LT_OK;
   }
-  const int64_t key[5] = {p->width, p->height, p->tile_size, p->rank, p->n_ranks};
+  const int64_t rank = sharded ? p->rank : 0, n_ranks = sharded ? p->n_ranks : 1;
+  const int64_t tile_sz = sharded ? p->tile_size : tile_order;
+  const int64_t key[5] = {p->width, p->height, tile_sz, rank, n_ranks};
   if (!std::equal(key, key + 5, s->pix_key)) {
-    const int64_t W = p->width, H = p->height, T = p->tile_size;
+    const int64_t W = p->width, H = p->height, T = tile_sz;
     const int64_t ntx = (W + T - 1) / T, nty = (H + T - 1) / T;
     std::vector<int32_t> pix;
-    for (int64_t tile = p->rank; tile < ntx * nty; tile += p->n_ranks) {
+    for (int64_t tile = rank; tile < ntx * nty; tile += n_ranks) {
       const int64_t ty = tile / ntx, tx = tile - ty * ntx;
       for (int64_t y = ty * T; y < std::min(H, (ty + 1) * T); ++y)
         for (int64_t x = tx * T; x < std::min(W, (tx + 1) * T); ++x)

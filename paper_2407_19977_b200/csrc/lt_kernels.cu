@@ -496,17 +496,43 @@ __global__ void __launch_bounds__(kShadeThreads, LT_SHADE_MIN_BLOCKS)
       // (raygen no longer clears it)
       if (primary && !wrote_l) __stcs(&pa.L[p], L);
     }
-    // warp-aggregated append to the next queue
-    const unsigned mask = __ballot_sync(kFull, emit);
-    if (mask) {
-      const int leader = __ffs(mask) - 1;
-      int slot0 = 0;
-      if (lane == leader) slot0 = atomicAdd(count_out, __popc(mask));
-      slot0 = __shfl_sync(kFull, slot0, leader);
+    if (sa.octant_sort) {
+      // block-aggregated append grouped by direction octant: the block's
+      // continuation rays (nearby origins) land in the next queue as runs of
+      // equal octant, so a trace warp fetches rays that descend the tree
+      // alike (higher SIMT efficiency for incoherent bounces)
+      __shared__ int s_cnt[8], s_base[8];
+      if (threadIdx.x < 8) s_cnt[threadIdx.x] = 0;
+      __syncthreads();
+      int oct = 0, rank = 0;
       if (emit) {
-        const int slot = slot0 + __popc(mask & ((1u << lane) - 1u));
+        oct = (out_d.x < 0.f ? 1 : 0) | (out_d.y < 0.f ? 2 : 0) | (out_d.z < 0.f ? 4 : 0);
+        rank = atomicAdd(&s_cnt[oct], 1);
+      }
+      __syncthreads();
+      if (threadIdx.x < 8) {
+        const int c = s_cnt[threadIdx.x];
+        s_base[threadIdx.x] = c ? atomicAdd(count_out, c) : 0;
+      }
+      __syncthreads();
+      if (emit) {
+        const int slot = s_base[oct] + rank;
         __stcs(&n_o[slot], out_o);
         __stcs(&n_d[slot], out_d);
+      }
+    } else {
+      // warp-aggregated append to the next queue
+      const unsigned mask = __ballot_sync(kFull, emit);
+      if (mask) {
+        const int leader = __ffs(mask) - 1;
+        int slot0 = 0;
+        if (lane == leader) slot0 = atomicAdd(count_out, __popc(mask));
+        slot0 = __shfl_sync(kFull, slot0, leader);
+        if (emit) {
+          const int slot = slot0 + __popc(mask & ((1u << lane) - 1u));
+          __stcs(&n_o[slot], out_o);
+          __stcs(&n_d[slot], out_d);
+        }
       }
     }
   }

@@ -8,7 +8,10 @@
 namespace lt {
 
 constexpr int kTraceThreads = 128;
-constexpr int kShadeThreads = 256;
+#ifndef LT_SHADE_THREADS
+#define LT_SHADE_THREADS 256
+#endif
+constexpr int kShadeThreads = LT_SHADE_THREADS;
 #ifndef LT_SHORT_STACK
 #define LT_SHORT_STACK 16
 #endif
@@ -43,6 +46,7 @@ struct ShadeArgs {
   int32_t depth, max_depth, rr_start;
   float t_min;
   int32_t primary;  // depth-0 launch of a render batch: rays from RaygenArgs
+  int32_t octant_sort;  // append continuation rays grouped by direction octant
 };
 
 struct AccumArgs {
