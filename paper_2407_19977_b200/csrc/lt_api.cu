@@ -155,11 +155,20 @@ struct DeviceGuard {
 // render call (the reference's render_progressive does) never re-allocates
 // them.  Users serialize on `mu` while enqueueing and on the `last_use` event
 // on the device: a pass on another stream waits for the previous pass.
-struct Workspace {
-  std::mutex mu;
+// A render pass runs kLanes independent batch streams ("lanes") over
+// disjoint pixel ranges, so the drain tail of one lane's bounce launches
+// overlaps the other lane's work; each lane owns its queues.
+constexpr int kLanes = 2;
+
+struct Lane {
   int64_t cap = 0;
   int32_t depth_cap = 0;
   DevBuf q_o[2], q_d[2], hits, T, L, rng, counters;
+};
+
+struct Workspace {
+  std::mutex mu;
+  Lane lane[kLanes];
   cudaEvent_t last_use = nullptr;
 };
 
@@ -229,6 +238,9 @@ struct lt_scene {
   int shade_grid = 0;
   int smem_nodes = 0;
   int64_t default_batch = int64_t(1) << 22;
+  int n_lanes = kLanes;
+  cudaStream_t lane_st[kLanes] = {nullptr, nullptr};
+  cudaEvent_t fork_ev = nullptr, join_ev[kLanes] = {nullptr, nullptr};
   bool octant_sort = false;
   // stats of the last pass
   lt_render_stats stats{};
@@ -415,6 +427,11 @@ static void destroy_scene(lt_scene *s) {
   pt.mark("destroy: device frees");
   s->h_stage.release();
   for (cudaEvent_t e : s->ev_pool) cudaEventDestroy(e);
+  for (int k = 0; k < kLanes; ++k) {
+    if (s->lane_st[k]) cudaStreamDestroy(s->lane_st[k]);
+    if (s->join_ev[k]) cudaEventDestroy(s->join_ev[k]);
+  }
+  if (s->fork_ev) cudaEventDestroy(s->fork_ev);
   if (s->stream) cudaStreamDestroy(s->stream);
   pt.mark("destroy: host + stream");
   delete s;
@@ -490,6 +507,15 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
   CK(cudaDeviceGetAttribute(&s->sm_count, cudaDevAttrMultiProcessorCount, device));
   CK(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
   s->ws = workspace_for(device);
+  for (int k = 0; k < kLanes; ++k) {
+    CK(cudaStreamCreateWithFlags(&s->lane_st[k], cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&s->join_ev[k], cudaEventDisableTiming));
+  }
+  CK(cudaEventCreateWithFlags(&s->fork_ev, cudaEventDisableTiming));
+  {
+    const char *ls = std::getenv("LT_LANES");
+    s->n_lanes = std::max(1, std::min(kLanes, ls ? std::atoi(ls) : kLanes));
+  }
   {
     // keep stream-ordered scene / staging memory mapped between scenes
     cudaMemPool_t pool;
@@ -746,28 +772,28 @@ extern "C" int lt_scene_info_get(const lt_scene *s, lt_scene_info *info) {
 
 // ------------------------------------------------------------------ workspace
 
-static int ensure_workspace(lt_scene *s, int64_t cap, int32_t max_depth) {
-  if (cap > s->ws->cap) {
+static int ensure_lane(lt_scene *s, Lane &ln, int64_t cap, int32_t max_depth) {
+  if (cap > ln.cap) {
     for (int k = 0; k < 2; ++k) {
-      RET(s->ws->q_o[k].ensure(16 * cap));
-      RET(s->ws->q_d[k].ensure(16 * cap));
+      RET(ln.q_o[k].ensure(16 * cap));
+      RET(ln.q_d[k].ensure(16 * cap));
     }
-    RET(s->ws->hits.ensure(16 * cap));
-    RET(s->ws->T.ensure(16 * cap));
-    RET(s->ws->L.ensure(16 * cap));
-    RET(s->ws->rng.ensure(16 * cap));
-    s->ws->cap = cap;
+    RET(ln.hits.ensure(16 * cap));
+    RET(ln.T.ensure(16 * cap));
+    RET(ln.L.ensure(16 * cap));
+    RET(ln.rng.ensure(16 * cap));
+    ln.cap = cap;
   }
-  if (max_depth > s->ws->depth_cap) {
-    RET(s->ws->counters.ensure(sizeof(int32_t) * (2 * (size_t)max_depth + 2)));
-    s->ws->depth_cap = max_depth;
+  if (max_depth > ln.depth_cap) {
+    RET(ln.counters.ensure(sizeof(int32_t) * (2 * (size_t)max_depth + 2)));
+    ln.depth_cap = max_depth;
   }
   RET(s->ray_ctr.ensure(3 * sizeof(unsigned long long)));
   return LT_OK;
 }
 
-static PathArrays path_arrays(lt_scene *s) {
-  return PathArrays{s->ws->T.as<float4>(), s->ws->L.as<float4>(), s->ws->rng.as<ulonglong2>()};
+static PathArrays path_arrays(Lane &ln) {
+  return PathArrays{ln.T.as<float4>(), ln.L.as<float4>(), ln.rng.as<ulonglong2>()};
 }
 
 static int record_event(lt_scene *s, cudaStream_t st) {
@@ -784,15 +810,15 @@ static int record_event(lt_scene *s, cudaStream_t st) {
 // trace -> shade per segment.  With `primary` the depth-0 launches generate
 // the camera rays themselves (render batches); otherwise queue 0 must hold
 // the primary rays and counters[0] their number (explicit rays).
-static int run_bounces(lt_scene *s, int32_t max_depth, int32_t rr_start, float t_min,
+static int run_bounces(lt_scene *s, Lane &lane, int32_t max_depth, int32_t rr_start, float t_min,
                        uint32_t flags, cudaStream_t st, const RaygenArgs *primary = nullptr) {
   const bool smem = !(flags & LT_FLAG_NO_SMEM_TOP) && s->smem_nodes > 0;
   SceneView sc = s->view;
   sc.n_top = smem ? s->smem_nodes : 0;
-  Workspace *ws = s->ws;
+  Lane *ws = &lane;
   int32_t *ctr = ws->counters.as<int32_t>();
   int32_t *fetch = ctr + max_depth + 1;
-  const PathArrays pa = path_arrays(s);
+  const PathArrays pa = path_arrays(lane);
   int cur = 0;
   for (int32_t depth = 0; depth < max_depth; ++depth) {
     const RaygenArgs *prim = depth == 0 ? primary : nullptr;
@@ -800,7 +826,7 @@ static int run_bounces(lt_scene *s, int32_t max_depth, int32_t rr_start, float t
     // (in-kernel ray generation for trace measured slower than reading the
     // 32 B ray record: the float64 camera math serializes the refill path)
     CK(launch_trace(sc, smem, (flags & LT_FLAG_COUNT) != 0, s->trace_grid[smem ? 1 : 0],
-                    s->use_window ? &s->window : nullptr, nullptr, ws->q_o[cur].as<float4>(),
+                    s->use_window ? &s->window : nullptr, ws->q_o[cur].as<float4>(),
                     ws->q_d[cur].as<float4>(), ctr + depth, fetch + depth,
                     ws->hits.as<float4>(), s->ray_ctr.as<unsigned long long>(), st));
     if (flags & LT_FLAG_PROFILE) RET(record_event(s, st));
@@ -883,40 +909,77 @@ static int render_impl(lt_scene *s, const lt_render_params *p, float *accum, uin
   if (n_local == 0 || p->sample_count == 0) return LT_OK;
   const int64_t B = std::min(p->max_batch_paths > 0 ? p->max_batch_paths : s->default_batch,
                              kMaxBatchPaths);
-  const int64_t pix_chunk = std::min(n_local, B);
-  const int64_t spb = std::min<int64_t>(std::max<int64_t>(1, B / pix_chunk), p->sample_count);
-  WorkspaceLease lease(s->ws, st);
-  RET(ensure_workspace(s, pix_chunk * spb, p->max_depth));
-  CK(cudaMemsetAsync(s->ray_ctr.p, 0, 3 * sizeof(unsigned long long), st));
-  const float t_min = (float)p->t_min;
-  const PathArrays pa = path_arrays(s);
-  int32_t *ctr = s->ws->counters.as<int32_t>();
-  for (int64_t s0 = 0; s0 < p->sample_count; s0 += spb) {
-    const int64_t ns = std::min(spb, p->sample_count - s0);
-    for (int64_t pc0 = 0; pc0 < n_local; pc0 += pix_chunk) {
-      const int64_t np = std::min(pix_chunk, n_local - pc0);
-      CK(cudaMemsetAsync(ctr, 0, sizeof(int32_t) * (2 * (size_t)p->max_depth + 2), st));
-      RaygenArgs ra{};
-      std::memcpy(ra.cam, p->camera, sizeof(ra.cam));
-      ra.width = p->width;
-      ra.height = p->height;
-      ra.seed = p->seed;
-      ra.sample_base = p->sample_start + s0;
-      ra.n_pix = np;
-      ra.pix_offset = pc0;
-      ra.pix_list = pix_list;
-      ra.n_paths = np * ns;
-      ra.t_min = t_min;
-      // raygen writes only the ray records; the depth-0 shade regenerates
-      // throughput / radiance / PCG state
-      launch_raygen(ra, pa, s->ws->q_o[0].as<float4>(), s->ws->q_d[0].as<float4>(), ctr, st);
-      RET(run_bounces(s, p->max_depth, p->rr_start, t_min, p->flags, st, &ra));
-      AccumArgs aa{np, pc0, ns, pix_list};
-      launch_accumulate(aa, s->ws->L.as<float4>(), accum, valid, invalid, st);
-      s->stats.kernel_launches += 2;
-      s->stats.batches += 1;
-      s->stats.paths += np * ns;
+  // lanes: disjoint contiguous ranges of the (tile-ordered) local pixels,
+  // each with its own batches on its own stream; per pixel, samples still
+  // accumulate in index order, so results do not depend on the lane count
+  const int n_lanes = (int)std::max<int64_t>(1, std::min<int64_t>(s->n_lanes, n_local));
+  struct Batch {
+    int lane;
+    int64_t s0, ns, pc0, np;
+  };
+  std::vector<Batch> order;
+  int64_t lane_cap[kLanes] = {0, 0};
+  {
+    std::vector<std::vector<Batch>> per(n_lanes);
+    for (int k = 0; k < n_lanes; ++k) {
+      const int64_t lo = n_local * k / n_lanes, hi = n_local * (k + 1) / n_lanes;
+      const int64_t n_k = hi - lo, B_k = std::max<int64_t>(1, B / n_lanes);
+      const int64_t chunk = std::min(n_k, B_k);
+      const int64_t spb = std::min<int64_t>(std::max<int64_t>(1, B_k / chunk), p->sample_count);
+      lane_cap[k] = chunk * spb;
+      for (int64_t s0 = 0; s0 < p->sample_count; s0 += spb)
+        for (int64_t pc = lo; pc < hi; pc += chunk)
+          per[k].push_back(Batch{k, s0, std::min(spb, p->sample_count - s0), pc,
+                                 std::min(chunk, hi - pc)});
     }
+    // enqueue round-robin so every lane stream always has work queued
+    for (size_t i = 0;; ++i) {
+      bool any = false;
+      for (int k = 0; k < n_lanes; ++k)
+        if (i < per[k].size()) {
+          order.push_back(per[k][i]);
+          any = true;
+        }
+      if (!any) break;
+    }
+  }
+  WorkspaceLease lease(s->ws, st);
+  for (int k = 0; k < n_lanes; ++k) RET(ensure_lane(s, s->ws->lane[k], lane_cap[k], p->max_depth));
+  CK(cudaMemsetAsync(s->ray_ctr.p, 0, 3 * sizeof(unsigned long long), st));
+  // fork the lane streams off the caller's stream
+  CK(cudaEventRecord(s->fork_ev, st));
+  for (int k = 0; k < n_lanes; ++k) CK(cudaStreamWaitEvent(s->lane_st[k], s->fork_ev, 0));
+  const float t_min = (float)p->t_min;
+  for (const Batch &b : order) {
+    Lane &ln = s->ws->lane[b.lane];
+    cudaStream_t ls = s->lane_st[b.lane];
+    int32_t *ctr = ln.counters.as<int32_t>();
+    CK(cudaMemsetAsync(ctr, 0, sizeof(int32_t) * (2 * (size_t)p->max_depth + 2), ls));
+    RaygenArgs ra{};
+    std::memcpy(ra.cam, p->camera, sizeof(ra.cam));
+    ra.width = p->width;
+    ra.height = p->height;
+    ra.seed = p->seed;
+    ra.sample_base = p->sample_start + b.s0;
+    ra.n_pix = b.np;
+    ra.pix_offset = b.pc0;
+    ra.pix_list = pix_list;
+    ra.n_paths = b.np * b.ns;
+    ra.t_min = t_min;
+    // raygen writes only the ray records; the depth-0 shade regenerates
+    // throughput / radiance / PCG state
+    launch_raygen(ra, path_arrays(ln), ln.q_o[0].as<float4>(), ln.q_d[0].as<float4>(), ctr, ls);
+    RET(run_bounces(s, ln, p->max_depth, p->rr_start, t_min, p->flags, ls, &ra));
+    AccumArgs aa{b.np, b.pc0, b.ns, pix_list};
+    launch_accumulate(aa, ln.L.as<float4>(), accum, valid, invalid, ls);
+    s->stats.kernel_launches += 2;
+    s->stats.batches += 1;
+    s->stats.paths += b.np * b.ns;
+  }
+  // join back into the caller's stream
+  for (int k = 0; k < n_lanes; ++k) {
+    CK(cudaEventRecord(s->join_ev[k], s->lane_st[k]));
+    CK(cudaStreamWaitEvent(st, s->join_ev[k], 0));
   }
   CK(cudaGetLastError());
   return LT_OK;
@@ -940,13 +1003,28 @@ extern "C" int lt_render_stats_get(const lt_scene *cs, lt_render_stats *out) {
     s->stats.slab_tests = (int64_t)c[1];
     s->stats.tri_tests = (int64_t)c[2];
   }
-  double ms = 0.0;
+  // trace launches of concurrent lanes overlap: report the union of their
+  // [start, end] intervals (time during which any trace kernel ran)
+  std::vector<std::pair<double, double>> iv;
   for (int i = 0; i + 1 < s->ev_used; i += 2) {
     CK(cudaEventSynchronize(s->ev_pool[i + 1]));
-    float e = 0.f;
-    CK(cudaEventElapsedTime(&e, s->ev_pool[i], s->ev_pool[i + 1]));
-    ms += e;
+    float a = 0.f, b = 0.f;
+    CK(cudaEventElapsedTime(&a, s->ev_pool[0], s->ev_pool[i]));
+    CK(cudaEventElapsedTime(&b, s->ev_pool[0], s->ev_pool[i + 1]));
+    iv.emplace_back(a, b);
   }
+  std::sort(iv.begin(), iv.end());
+  double ms = 0.0, cur_a = 0.0, cur_b = -1.0;
+  for (const auto &x : iv) {
+    if (x.first > cur_b) {
+      if (cur_b > cur_a) ms += cur_b - cur_a;
+      cur_a = x.first;
+      cur_b = x.second;
+    } else if (x.second > cur_b) {
+      cur_b = x.second;
+    }
+  }
+  if (cur_b > cur_a) ms += cur_b - cur_a;
   s->stats.trace_ms = ms;
   *out = s->stats;
   return LT_OK;
@@ -1100,7 +1178,8 @@ extern "C" int lt_trace_paths_host(lt_scene *s, const double *origins, const dou
   s->stats = lt_render_stats{};
   s->ev_used = 0;
   WorkspaceLease lease(s->ws, st);
-  RET(ensure_workspace(s, n, max_depth));
+  Lane &ln = s->ws->lane[0];
+  RET(ensure_lane(s, ln, n, max_depth));
   RET(s->s_a.ensure(64 * n));
   double *d_o = s->s_a.as<double>();
   double *d_d = d_o + 3 * n;
@@ -1110,12 +1189,12 @@ extern "C" int lt_trace_paths_host(lt_scene *s, const double *origins, const dou
   CK(cudaMemcpyAsync(d_d, dirs, 24 * n, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(d_state, state, 8 * n, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(d_inc, inc, 8 * n, cudaMemcpyHostToDevice, st));
-  CK(cudaMemsetAsync(s->ws->counters.p, 0, sizeof(int32_t) * (2 * (size_t)max_depth + 2), st));
+  CK(cudaMemsetAsync(ln.counters.p, 0, sizeof(int32_t) * (2 * (size_t)max_depth + 2), st));
   CK(cudaMemsetAsync(s->ray_ctr.p, 0, 3 * sizeof(unsigned long long), st));
-  const PathArrays pa = path_arrays(s);
-  launch_raygen_explicit(d_o, d_d, d_state, d_inc, n, (float)t_min, pa, s->ws->q_o[0].as<float4>(),
-                         s->ws->q_d[0].as<float4>(), s->ws->counters.as<int32_t>(), st);
-  RET(run_bounces(s, max_depth, rr_start, (float)t_min, 0u, st));
+  const PathArrays pa = path_arrays(ln);
+  launch_raygen_explicit(d_o, d_d, d_state, d_inc, n, (float)t_min, pa, ln.q_o[0].as<float4>(),
+                         ln.q_d[0].as<float4>(), ln.counters.as<int32_t>(), st);
+  RET(run_bounces(s, ln, max_depth, rr_start, (float)t_min, 0u, st));
   RET(s->s_b.ensure(32 * n));
   double *d_rgb = s->s_b.as<double>();
   uint64_t *d_sout = reinterpret_cast<uint64_t *>(d_rgb + 3 * n);

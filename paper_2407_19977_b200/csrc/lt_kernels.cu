@@ -216,10 +216,9 @@ __global__ void k_gather_explicit(PathArrays pa, int64_t n, double *__restrict__
 // ray_ctr[2] += triangle tests.
 template <bool USE_SMEM, bool COUNT>
 __global__ void __launch_bounds__(kTraceThreads, LT_TRACE_MIN_BLOCKS)
-    k_trace(SceneView sc, RaygenArgs ra, int primary, const float4 *__restrict__ q_o,
-            const float4 *__restrict__ q_d, const int32_t *__restrict__ count,
-            int32_t *__restrict__ fetch, float4 *__restrict__ hits,
-            unsigned long long *__restrict__ ray_ctr) {
+    k_trace(SceneView sc, const float4 *__restrict__ q_o, const float4 *__restrict__ q_d,
+            const int32_t *__restrict__ count, int32_t *__restrict__ fetch,
+            float4 *__restrict__ hits, unsigned long long *__restrict__ ray_ctr) {
   // (USE_SMEM: the top-level staging variant measured slower than L1
   // caching -- profiles/r01_sweep -- and is kept only as a launch option.)
   extern __shared__ float4 s_mem[];
@@ -231,8 +230,7 @@ __global__ void __launch_bounds__(kTraceThreads, LT_TRACE_MIN_BLOCKS)
   int32_t l_node[LT_STACK - kShortStack];
   float l_t[LT_STACK - kShortStack];
 
-  // primary launch (depth 0 of a render batch): rays generated in place
-  const int n = primary ? (int)ra.n_paths : *count;
+  const int n = *count;
   if (blockIdx.x == 0 && tid == 0) atomicAdd(ray_ctr, (unsigned long long)n);
 
   int q = -1;
@@ -260,17 +258,11 @@ __global__ void __launch_bounds__(kTraceThreads, LT_TRACE_MIN_BLOCKS)
         const int r = base + __popc(idle & lanes_below);
         if (r < n) {
           q = r;
-          if (primary) {
-            uint64_t st_, inc_;
-            primary_ray(ra, r, o, d, st_, inc_);
-            t_min = ra.t_min;
-          } else {
-            const float4 ro = __ldcs(&q_o[r]);
-            const float4 rd = __ldcs(&q_d[r]);
-            o = mk(ro.x, ro.y, ro.z);
-            d = mk(rd.x, rd.y, rd.z);
-            t_min = rd.w;
-          }
+          const float4 ro = __ldcs(&q_o[r]);
+          const float4 rd = __ldcs(&q_d[r]);
+          o = mk(ro.x, ro.y, ro.z);
+          d = mk(rd.x, rd.y, rd.z);
+          t_min = rd.w;
           rs = ray_slab(o, d);
           best = HitRec{__int_as_float(0x7f800000), 0.f, 0.f, -1};
           best_orig = 0x7fffffff;
@@ -718,12 +710,9 @@ size_t trace_smem_bytes(int n_top) {
 }
 
 cudaError_t launch_trace(const SceneView &sc, bool smem, bool count_work, int grid,
-                         const cudaAccessPolicyWindow *window, const RaygenArgs *primary,
-                         const float4 *q_o, const float4 *q_d, const int32_t *count,
-                         int32_t *fetch, float4 *hits, unsigned long long *ray_ctr,
-                         cudaStream_t st) {
-  const RaygenArgs ra = primary ? *primary : RaygenArgs{};
-  const int prim = primary ? 1 : 0;
+                         const cudaAccessPolicyWindow *window, const float4 *q_o,
+                         const float4 *q_d, const int32_t *count, int32_t *fetch, float4 *hits,
+                         unsigned long long *ray_ctr, cudaStream_t st) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kTraceThreads);
@@ -737,16 +726,16 @@ cudaError_t launch_trace(const SceneView &sc, bool smem, bool count_work, int gr
     cfg.numAttrs = 1;
   }
   if (smem && count_work)
-    return cudaLaunchKernelEx(&cfg, k_trace<true, true>, sc, ra, prim, q_o, q_d, count, fetch,
-                              hits, ray_ctr);
+    return cudaLaunchKernelEx(&cfg, k_trace<true, true>, sc, q_o, q_d, count, fetch, hits,
+                              ray_ctr);
   if (smem)
-    return cudaLaunchKernelEx(&cfg, k_trace<true, false>, sc, ra, prim, q_o, q_d, count, fetch,
-                              hits, ray_ctr);
+    return cudaLaunchKernelEx(&cfg, k_trace<true, false>, sc, q_o, q_d, count, fetch, hits,
+                              ray_ctr);
   if (count_work)
-    return cudaLaunchKernelEx(&cfg, k_trace<false, true>, sc, ra, prim, q_o, q_d, count, fetch,
-                              hits, ray_ctr);
-  return cudaLaunchKernelEx(&cfg, k_trace<false, false>, sc, ra, prim, q_o, q_d, count, fetch,
-                            hits, ray_ctr);
+    return cudaLaunchKernelEx(&cfg, k_trace<false, true>, sc, q_o, q_d, count, fetch, hits,
+                              ray_ctr);
+  return cudaLaunchKernelEx(&cfg, k_trace<false, false>, sc, q_o, q_d, count, fetch, hits,
+                            ray_ctr);
 }
 
 void launch_trace_rays(const SceneView &sc, const float4 *q_o, const float4 *q_d, int64_t n,

@@ -76,13 +76,10 @@ void launch_raygen_explicit(const double *o, const double *d, const uint64_t *st
 void launch_gather_explicit(const PathArrays &pa, int64_t n, double *rgb, uint64_t *state_out,
                             cudaStream_t st);
 size_t trace_smem_bytes(int n_top);
-// `primary`: depth-0 launch of a render batch, rays generated from these
-// args (NULL: rays read from the queue)
 cudaError_t launch_trace(const SceneView &sc, bool smem, bool count_work, int grid,
-                         const cudaAccessPolicyWindow *window, const RaygenArgs *primary,
-                         const float4 *q_o, const float4 *q_d, const int32_t *count,
-                         int32_t *fetch, float4 *hits, unsigned long long *ray_ctr,
-                         cudaStream_t st);
+                         const cudaAccessPolicyWindow *window, const float4 *q_o,
+                         const float4 *q_d, const int32_t *count, int32_t *fetch, float4 *hits,
+                         unsigned long long *ray_ctr, cudaStream_t st);
 void launch_trace_rays(const SceneView &sc, const float4 *q_o, const float4 *q_d, int64_t n,
                        float4 *hits, int32_t *nodes, int32_t *tests, cudaStream_t st);
 cudaError_t launch_shade(const SceneView &sc, const ShadeArgs &sa, const PathArrays &pa, int grid,
