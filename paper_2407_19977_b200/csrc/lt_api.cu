@@ -158,7 +158,8 @@ struct DeviceGuard {
 // A render pass runs kLanes independent batch streams ("lanes") over
 // disjoint pixel ranges, so the drain tail of one lane's bounce launches
 // overlaps the other lane's work; each lane owns its queues.
-constexpr int kLanes = 2;
+constexpr int kLanes = 4;          // upper bound; LT_LANES picks 1..kLanes (default 2)
+constexpr int kDefaultLanes = 2;
 
 struct Lane {
   int64_t cap = 0;
@@ -239,8 +240,8 @@ struct lt_scene {
   int smem_nodes = 0;
   int64_t default_batch = int64_t(1) << 22;
   int n_lanes = kLanes;
-  cudaStream_t lane_st[kLanes] = {nullptr, nullptr};
-  cudaEvent_t fork_ev = nullptr, join_ev[kLanes] = {nullptr, nullptr};
+  cudaStream_t lane_st[kLanes] = {};
+  cudaEvent_t fork_ev = nullptr, join_ev[kLanes] = {};
   bool octant_sort = false;
   // stats of the last pass
   lt_render_stats stats{};
@@ -514,7 +515,7 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
   CK(cudaEventCreateWithFlags(&s->fork_ev, cudaEventDisableTiming));
   {
     const char *ls = std::getenv("LT_LANES");
-    s->n_lanes = std::max(1, std::min(kLanes, ls ? std::atoi(ls) : kLanes));
+    s->n_lanes = std::max(1, std::min(kLanes, ls ? std::atoi(ls) : kDefaultLanes));
   }
   {
     // keep stream-ordered scene / staging memory mapped between scenes
@@ -918,7 +919,7 @@ static int render_impl(lt_scene *s, const lt_render_params *p, float *accum, uin
     int64_t s0, ns, pc0, np;
   };
   std::vector<Batch> order;
-  int64_t lane_cap[kLanes] = {0, 0};
+  int64_t lane_cap[kLanes] = {};
   {
     std::vector<std::vector<Batch>> per(n_lanes);
     for (int k = 0; k < n_lanes; ++k) {
