@@ -175,6 +175,25 @@ int lt_trace_paths_host(lt_scene *scene, const double *origins, const double *di
  * (h*w*3) float32 device -> sRGB u8 (h*w*3) device ---- */
 int lt_tonemap_u8(const float *linear, int64_t n_pixels, uint8_t *out, void *stream);
 
+/* ---- BSDF kernels on caller inputs (material.py:389-426: eval_bsdf,
+ * pdf_bsdf, sample_bsdf), the device code the shade kernel runs, in fp32.
+ * Host buffers; params (n,21) float64 per case:
+ *   [bw, bc.rgb, metalness, sw, sc.rgb, roughness, ior,
+ *    coat_w, coat_rough, coat_ior, coat_color.rgb, transmission_w, transmission_color.rgb]
+ * wo, wi, normal (n,3) unit float64; u (n,3) the three lobe / direction
+ * draws; front (n,) geometric-side flag (transmission only). ---- */
+int lt_bsdf_eval_batch(const double *params, const double *wo, const double *wi,
+                       const double *normal, int64_t n, double *f, double *pdf);
+int lt_bsdf_sample_batch(const double *params, const double *wo, const double *normal,
+                         const double *u, const int32_t *front, int64_t n, int32_t *ok,
+                         double *wi, double *weight);
+
+/* ---- any-hit occlusion: intersect_any (bvh.py:658-664) / _traverse_any
+ * (bvh.py:511-551), host buffers; occluded (n,) 1 if any triangle is hit
+ * within [t_min, t_max]. ---- */
+int lt_occluded_batch_host(lt_scene *scene, const double *origins, const double *dirs,
+                           int64_t n, double t_min, double t_max, int32_t *occluded);
+
 /* ---- measurement helper (not on the render path): streaming-read
  * bandwidth of a `bytes` device buffer, `iters` passes, CUDA events.  A
  * buffer smaller than L2 measures L2 bandwidth (the roofline denominator for

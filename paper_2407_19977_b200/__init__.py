@@ -10,8 +10,9 @@ from .geometry import (DEFAULT_T_MIN, Ray, Triangle, TriangleBuffer, normalize, 
 from .material import (OpenPbrParams, emitted_radiance, pack_material_table, pack_materials)
 from .scene import (CameraConfig, EnvironmentConfig, SceneDescription, SceneError, camera_pack)
 from .rng import PcgState, next_unit_real, pcg_next_u32, pcg_seed, seed_stream
-from .bvh import (STACK_SIZE, BuildStats, Bvh, build_bvh, intersect_scene,
-                  intersect_scene_batch, traversal_counts_batch)
+from .bvh import (STACK_SIZE, BuildStats, Bvh, build_bvh, intersect_any, intersect_any_batch,
+                  intersect_scene, intersect_scene_batch, traversal_counts_batch)
+from .bsdf import BsdfSample, eval_bsdf, pdf_bsdf, sample_bsdf
 from .device import DeviceScene
 from .integrator import (RenderResult, RenderSettings, environment_radiance,
                          generate_camera_ray, render_image, render_pass, render_progressive,
@@ -25,8 +26,9 @@ __all__ = [
     "OpenPbrParams", "emitted_radiance", "pack_material_table", "pack_materials",
     "CameraConfig", "EnvironmentConfig", "SceneDescription", "SceneError", "camera_pack",
     "PcgState", "next_unit_real", "pcg_next_u32", "pcg_seed", "seed_stream",
-    "STACK_SIZE", "BuildStats", "Bvh", "build_bvh", "intersect_scene", "intersect_scene_batch",
-    "traversal_counts_batch", "DeviceScene",
+    "STACK_SIZE", "BuildStats", "Bvh", "build_bvh", "intersect_any", "intersect_any_batch",
+    "intersect_scene", "intersect_scene_batch", "traversal_counts_batch", "DeviceScene",
+    "BsdfSample", "eval_bsdf", "pdf_bsdf", "sample_bsdf",
     "RenderResult", "RenderSettings", "environment_radiance", "generate_camera_ray",
     "render_image", "render_pass", "render_progressive", "trace_radiance",
     "trace_radiance_batch",

@@ -120,6 +120,28 @@ def traversal_counts_batch(triangles, bvh, origins, directions, t_min: float = 1
     return nodes, tests
 
 
+def intersect_any_batch(triangles, bvh, origins, directions, t_min: float = 1e-4,
+                        t_max: float = np.inf, *, device: int = 0, scene=None) -> np.ndarray:
+    """(n,) bool: any hit within [t_min, t_max] (the any-hit query of
+    _traverse_any, bvh.py:511-551), on the GPU."""
+    from .device import DeviceScene
+    o, d = _rays(origins, directions)
+    ds = scene if scene is not None else DeviceScene.from_geometry(triangles, bvh, device=device)
+    out = np.zeros(o.shape[0], np.int32)
+    if o.shape[0]:
+        P = _lib.ptr
+        _lib.check(_lib.lib().lt_occluded_batch_host(
+            ds.handle, P(o, C.c_double), P(d, C.c_double), o.shape[0], float(t_min),
+            float(t_max), P(out, C.c_int32)))
+    return out.astype(bool)
+
+
+def intersect_any(triangles, bvh, ray: Ray, *, device: int = 0, scene=None) -> bool:
+    """intersect_any (bvh.py:658-664)."""
+    return bool(intersect_any_batch(triangles, bvh, ray.origin[None], ray.direction[None],
+                                    ray.t_min, ray.t_max, device=device, scene=scene)[0])
+
+
 def intersect_scene(triangles, bvh, ray: Ray, *, device: int = 0, scene=None):
     """Nearest hit for one ray as (triangle_index, t) or None.  (The reference
     returns a Hit with normals; the hit frame is computed on the device inside

@@ -1207,6 +1207,118 @@ extern "C" int lt_trace_paths_host(lt_scene *s, const double *origins, const dou
   return LT_OK;
 }
 
+// ------------------------------------------------------------------ BSDF queries
+
+// GpuMaterial records from (n,21) parameter rows (layout in luxb200.h)
+static void materials_from_params(const double *p, int64_t n, std::vector<GpuMaterial> &out) {
+  std::vector<double> bw(n), bc(3 * n), m(n), sw(n), sc(3 * n), r(n), ior(n), zero(3 * n, 0.0);
+  std::vector<double> cw(n), cr(n), ci(n), cc(3 * n), tw(n), tc(3 * n);
+  for (int64_t i = 0; i < n; ++i) {
+    const double *q = p + 21 * i;
+    bw[i] = q[0];
+    for (int k = 0; k < 3; ++k) {
+      bc[3 * i + k] = q[1 + k];
+      sc[3 * i + k] = q[6 + k];
+      cc[3 * i + k] = q[14 + k];
+      tc[3 * i + k] = q[18 + k];
+    }
+    m[i] = q[4];
+    sw[i] = q[5];
+    r[i] = q[9];
+    ior[i] = q[10];
+    cw[i] = q[11];
+    cr[i] = q[12];
+    ci[i] = q[13];
+    tw[i] = q[17];
+  }
+  lt_scene_desc d{};
+  d.n_materials = (int32_t)n;
+  d.base_weight = bw.data();
+  d.base_color = bc.data();
+  d.base_metalness = m.data();
+  d.specular_weight = sw.data();
+  d.specular_color = sc.data();
+  d.specular_roughness = r.data();
+  d.specular_ior = ior.data();
+  d.emission_luminance = zero.data();
+  d.emission_color = zero.data();
+  d.coat_weight = cw.data();
+  d.coat_roughness = cr.data();
+  d.coat_ior = ci.data();
+  d.coat_color = cc.data();
+  d.transmission_weight = tw.data();
+  d.transmission_color = tc.data();
+  out.resize(n);
+  for (int64_t i = 0; i < n; ++i) build_material(&d, (int)i, out[i]);
+}
+
+extern "C" int lt_bsdf_eval_batch(const double *params, const double *wo, const double *wi,
+                                  const double *normal, int64_t n, double *f, double *pdf) {
+  if (n < 0 || (n > 0 && (!params || !wo || !wi || !normal || !f || !pdf)))
+    return lt_fail(LT_ERR_INVALID, "invalid bsdf arguments");
+  if (n == 0) return LT_OK;
+  std::vector<GpuMaterial> mats;
+  materials_from_params(params, n, mats);
+  DevBuf dm, da;
+  RET(dm.ensure(sizeof(GpuMaterial) * n));
+  RET(da.ensure(sizeof(double) * 13 * n));
+  double *dwo = da.as<double>(), *dwi = dwo + 3 * n, *dn = dwi + 3 * n, *df = dn + 3 * n,
+         *dp = df + 3 * n;
+  CK(cudaMemcpy(dm.p, mats.data(), sizeof(GpuMaterial) * n, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dwo, wo, 24 * n, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dwi, wi, 24 * n, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dn, normal, 24 * n, cudaMemcpyHostToDevice));
+  launch_bsdf_eval(dm.as<GpuMaterial>(), dwo, dwi, dn, n, df, dp, 0);
+  CK(cudaGetLastError());
+  CK(cudaMemcpy(f, df, 24 * n, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(pdf, dp, 8 * n, cudaMemcpyDeviceToHost));
+  return LT_OK;
+}
+
+extern "C" int lt_bsdf_sample_batch(const double *params, const double *wo, const double *normal,
+                                    const double *u, const int32_t *front, int64_t n, int32_t *ok,
+                                    double *wi, double *weight) {
+  if (n < 0 || (n > 0 && (!params || !wo || !normal || !u || !ok || !wi || !weight)))
+    return lt_fail(LT_ERR_INVALID, "invalid bsdf arguments");
+  if (n == 0) return LT_OK;
+  std::vector<GpuMaterial> mats;
+  materials_from_params(params, n, mats);
+  DevBuf dm, da, di;
+  RET(dm.ensure(sizeof(GpuMaterial) * n));
+  RET(da.ensure(sizeof(double) * 15 * n));
+  RET(di.ensure(sizeof(int32_t) * 2 * n));
+  double *dwo = da.as<double>(), *dn = dwo + 3 * n, *du = dn + 3 * n, *dwi = du + 3 * n,
+         *dw = dwi + 3 * n;
+  int32_t *dok = di.as<int32_t>(), *dfr = dok + n;
+  CK(cudaMemcpy(dm.p, mats.data(), sizeof(GpuMaterial) * n, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dwo, wo, 24 * n, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dn, normal, 24 * n, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(du, u, 24 * n, cudaMemcpyHostToDevice));
+  if (front) CK(cudaMemcpy(dfr, front, 4 * n, cudaMemcpyHostToDevice));
+  launch_bsdf_sample(dm.as<GpuMaterial>(), dwo, dn, du, front ? dfr : nullptr, n, dok, dwi, dw, 0);
+  CK(cudaGetLastError());
+  CK(cudaMemcpy(ok, dok, 4 * n, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(wi, dwi, 24 * n, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(weight, dw, 24 * n, cudaMemcpyDeviceToHost));
+  return LT_OK;
+}
+
+extern "C" int lt_occluded_batch_host(lt_scene *s, const double *origins, const double *dirs,
+                                      int64_t n, double t_min, double t_max, int32_t *occluded) {
+  if (!s || n < 0) return lt_fail(LT_ERR_INVALID, "invalid arguments");
+  if (n == 0) return LT_OK;
+  if (!origins || !dirs || !occluded) return lt_fail(LT_ERR_INVALID, "null buffer");
+  DeviceGuard g(s->device);
+  cudaStream_t st = s->stream;
+  RET(upload_rays_f64(s, origins, dirs, n, t_min, t_max, st));
+  RET(s->s_b.ensure(std::max<int64_t>(16, 4 * n)));
+  launch_occluded(s->view, s->s_d.as<float4>(), s->s_e.as<float4>(), n, s->s_b.as<int32_t>(), st);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(occluded, s->s_b.p, 4 * n, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return LT_OK;
+}
+
 extern "C" int lt_read_bandwidth(int32_t device, int64_t bytes, int32_t iters, double *gbps) {
   if (!gbps || bytes < 1024 || iters < 1) return lt_fail(LT_ERR_INVALID, "invalid probe arguments");
   DeviceGuard g(device);

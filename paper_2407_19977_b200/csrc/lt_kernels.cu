@@ -623,6 +623,78 @@ __global__ void k_tonemap_u8(const float *__restrict__ lin, int64_t n_pixels,
   }
 }
 
+// ------------------------------------------------------------------ BSDF / any-hit queries
+
+__device__ __forceinline__ f3 load3(const double *a, int64_t i) {
+  return f3{(float)a[3 * i], (float)a[3 * i + 1], (float)a[3 * i + 2]};
+}
+
+// eval_bsdf / pdf_bsdf (material.py:389-407) with the shade kernel's code
+__global__ void k_bsdf_eval(const GpuMaterial *__restrict__ mats, const double *__restrict__ wo,
+                            const double *__restrict__ wi, const double *__restrict__ nrm,
+                            int64_t n, double *__restrict__ f, double *__restrict__ pdf) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const GpuMaterial mt = mats[i];
+  const float opaque = (mt.flags & MAT_GLASS) ? 1.f - mt.tw : 1.f;
+  const f3 a = load3(wo, i), b = load3(wi, i), c = load3(nrm, i);
+  const f3 v = eval_core(a, b, c, mt, opaque);
+  f[3 * i] = v.x;
+  f[3 * i + 1] = v.y;
+  f[3 * i + 2] = v.z;
+  pdf[i] = pdf_core(a, b, c, mt, opaque);
+}
+
+// sample_bsdf (material.py:410-426): the draws are rounded toward zero to
+// fp32 as the shade kernel's unit_f32 does
+__global__ void k_bsdf_sample(const GpuMaterial *__restrict__ mats, const double *__restrict__ wo,
+                              const double *__restrict__ nrm, const double *__restrict__ u,
+                              const int32_t *__restrict__ front, int64_t n,
+                              int32_t *__restrict__ ok, double *__restrict__ wi,
+                              double *__restrict__ wgt) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const GpuMaterial mt = mats[i];
+  f3 w{0.f, 0.f, 0.f}, g{0.f, 0.f, 0.f};
+  const bool r = sample_material(load3(wo, i), load3(nrm, i), mt, front ? front[i] != 0 : true,
+                                 __double2float_rz(u[3 * i]), __double2float_rz(u[3 * i + 1]),
+                                 __double2float_rz(u[3 * i + 2]), w, g);
+  ok[i] = r ? 1 : 0;
+  wi[3 * i] = r ? w.x : 0.0;
+  wi[3 * i + 1] = r ? w.y : 0.0;
+  wi[3 * i + 2] = r ? w.z : 0.0;
+  wgt[3 * i] = r ? g.x : 0.0;
+  wgt[3 * i + 1] = r ? g.y : 0.0;
+  wgt[3 * i + 2] = r ? g.z : 0.0;
+}
+
+__global__ void k_occluded(SceneView sc, const float4 *__restrict__ q_o,
+                           const float4 *__restrict__ q_d, int64_t n,
+                           int32_t *__restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float4 ro = q_o[i], rd = q_d[i];
+  out[i] = occluded(sc, mk(ro.x, ro.y, ro.z), mk(rd.x, rd.y, rd.z), rd.w, ro.w) ? 1 : 0;
+}
+
+void launch_bsdf_eval(const GpuMaterial *mats, const double *wo, const double *wi,
+                      const double *nrm, int64_t n, double *f, double *pdf, cudaStream_t st) {
+  if (n > 0) k_bsdf_eval<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(mats, wo, wi, nrm, n, f, pdf);
+}
+
+void launch_bsdf_sample(const GpuMaterial *mats, const double *wo, const double *nrm,
+                        const double *u, const int32_t *front, int64_t n, int32_t *ok, double *wi,
+                        double *wgt, cudaStream_t st) {
+  if (n > 0)
+    k_bsdf_sample<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(mats, wo, nrm, u, front, n, ok, wi,
+                                                               wgt);
+}
+
+void launch_occluded(const SceneView &sc, const float4 *q_o, const float4 *q_d, int64_t n,
+                     int32_t *out, cudaStream_t st) {
+  if (n > 0) k_occluded<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(sc, q_o, q_d, n, out);
+}
+
 // ------------------------------------------------------------------ probe
 
 // Streaming read of `n4` float4 (grid-stride, 4 independent loads in flight

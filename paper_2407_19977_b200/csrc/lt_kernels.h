@@ -96,6 +96,13 @@ void launch_pack_rays_f64(const double *o, const double *d, int64_t n, float t_m
 void launch_unpack_hits(const SceneView &sc, const float4 *hits, int64_t n, int32_t *idx32,
                         float *t32, int64_t *idx64, double *t64, cudaStream_t st);
 void launch_tonemap_u8(const float *lin, int64_t n_pixels, uint8_t *out, cudaStream_t st);
+void launch_bsdf_eval(const GpuMaterial *mats, const double *wo, const double *wi,
+                      const double *nrm, int64_t n, double *f, double *pdf, cudaStream_t st);
+void launch_bsdf_sample(const GpuMaterial *mats, const double *wo, const double *nrm,
+                        const double *u, const int32_t *front, int64_t n, int32_t *ok, double *wi,
+                        double *wgt, cudaStream_t st);
+void launch_occluded(const SceneView &sc, const float4 *q_o, const float4 *q_d, int64_t n,
+                     int32_t *out, cudaStream_t st);
 void launch_read_probe(const float4 *src, int64_t n4, int passes, float *sink, int grid,
                        cudaStream_t st);
 

@@ -184,6 +184,39 @@ __device__ __forceinline__ Hits4 visit4(const float4 *__restrict__ np, const Ray
   return h;
 }
 
+// Any-hit occlusion (_traverse_any, bvh.py:511-551): true as soon as any
+// triangle is hit within [t_min, t_max]; wide layout, no ordering needed.
+__device__ __forceinline__ bool occluded(const SceneView &sc, f3 o, f3 d, float t_min,
+                                         float t_max) {
+  const float kInf = __int_as_float(0x7f800000);
+  const RaySlab rs = ray_slab(o, d);
+  float t_root;
+  if (!slab(rs, sc.root_lo[0], sc.root_hi[0], sc.root_lo[1], sc.root_hi[1], sc.root_lo[2],
+            sc.root_hi[2], t_min, t_max, t_root))
+    return false;
+  int32_t stk[LT_STACK];
+  int sp = 0;
+  int32_t node = sc.wroot_link;
+  HitRec best{t_max, 0.f, 0.f, -1};
+  int32_t best_orig = 0x7fffffff;
+  while (true) {
+    while (node >= 0) {
+      const Hits4 h = visit4(sc.wnodes + 8 * (int64_t)node, rs, t_min, t_max);
+      if (h.k3 < kInf) stk[sp++] = h.l3;
+      if (h.k2 < kInf) stk[sp++] = h.l2;
+      if (h.k1 < kInf) stk[sp++] = h.l1;
+      node = h.k0 < kInf ? h.l0 : LT_LINK_EXIT;
+      if (node == LT_LINK_EXIT && sp > 0) node = stk[--sp];
+    }
+    if (node == LT_LINK_EXIT) return false;
+    int tests = 0;
+    leaf_test<false>(sc, ~(int64_t)node, o, d, t_min, best, best_orig, tests);
+    if (best.k >= 0) return true;
+    if (sp == 0) return false;
+    node = stk[--sp];
+  }
+}
+
 // Per-thread traversal with a local-memory stack for the query kernels.
 // WIDE: the BVH4 layout (closest-hit queries); otherwise the BVH2 layout
 // with the reference's counters (traversal_counts_batch).
