@@ -64,12 +64,17 @@ __device__ __forceinline__ f3 cosine_sample(f3 n, float u1, float u2) {
             x * t.z + y * b.z + z * n.z};
 }
 
-// _ggx_sample_half (material.py:277-290)
+// _ggx_sample_half (material.py:277-290).  The reference's
+// ct = sqrt((1-u1)/(1+(a2-1)u1)) is exact in float64 but cancels in fp32
+// (a2-1 rounds to -1 for a2 < 2^-25, and 1-ct^2 loses the tangent near the
+// mirror direction); the same angle through tan^2 = a2 u1/(1-u1) has no
+// cancellation (1-u1 is exact for u1 >= 0.5 by Sterbenz).
 __device__ __forceinline__ f3 ggx_sample_half(f3 n, float a2, float u1, float u2) {
   f3 t, b;
   onb(n, t, b);
-  float ct = sqrtf((1.f - u1) / (1.f + (a2 - 1.f) * u1));
-  float st = sqrtf(fmaxf(0.f, 1.f - ct * ct));
+  float t2 = a2 * u1 / (1.f - u1);
+  float ct = 1.f / sqrtf(1.f + t2);
+  float st = sqrtf(t2) * ct;
   float sphi, cphi;
   sincospif(2.f * u2, &sphi, &cphi);
   float x = st * cphi, y = st * sphi;
