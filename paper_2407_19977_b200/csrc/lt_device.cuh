@@ -197,9 +197,13 @@ __device__ __forceinline__ void hit_frame(f3 d, f3 g0, f3 n0, f3 n1, f3 n2, floa
   float sz = w * n0.z + u * n1.z + v * n2.z;
   float slen = sqrtf(sx * sx + sy * sy + sz * sz);
   if (slen > 0.f) {
-    sx /= slen;
-    sy /= slen;
-    sz /= slen;
+    // one reciprocal, three products (<= 1 ulp from the quotients): an IEEE
+    // quotient with an exactly-zero numerator (axis-aligned normals) takes
+    // the division slow path
+    const float r = 1.f / slen;
+    sx *= r;
+    sy *= r;
+    sz *= r;
   } else {
     sx = gx;
     sy = gy;

@@ -43,10 +43,12 @@ __device__ __forceinline__ void onb(f3 n, f3 &t, f3 &b) {
   float tx = ay * n.z - az * n.y;
   float ty = az * n.x - ax * n.z;
   float tz = ax * n.y - ay * n.x;
-  float tl = sqrtf(tx * tx + ty * ty + tz * tz);
-  tx /= tl;
-  ty /= tl;
-  tz /= tl;
+  // reciprocal once (tl >= 0.43): the tangent always has an exactly-zero
+  // component, whose IEEE quotient would take the division slow path
+  const float rl = 1.f / sqrtf(tx * tx + ty * ty + tz * tz);
+  tx *= rl;
+  ty *= rl;
+  tz *= rl;
   t = f3{tx, ty, tz};
   b = f3{n.y * tz - n.z * ty, n.z * tx - n.x * tz, n.x * ty - n.y * tx};
 }
@@ -104,9 +106,10 @@ __device__ __forceinline__ f3 eval_core(f3 wo, f3 wi, f3 n, const GpuMaterial &m
   float hx = wo.x + wi.x, hy = wo.y + wi.y, hz = wo.z + wi.z;
   float hl = sqrtf(hx * hx + hy * hy + hz * hz);
   if (hl <= 0.f) return f;
-  hx /= hl;
-  hy /= hl;
-  hz /= hl;
+  const float rh = 1.f / hl;
+  hx *= rh;
+  hy *= rh;
+  hz *= rh;
   float nh = n.x * hx + n.y * hy + n.z * hz;
   float oh = wo.x * hx + wo.y * hy + wo.z * hz;
   if (oh <= 0.f) return f;
@@ -137,9 +140,10 @@ __device__ __forceinline__ float pdf_core(f3 wo, f3 wi, f3 n, const GpuMaterial 
   float hx = wo.x + wi.x, hy = wo.y + wi.y, hz = wo.z + wi.z;
   float hl = sqrtf(hx * hx + hy * hy + hz * hz);
   if (hl <= 0.f) return 0.f;
-  hx /= hl;
-  hy /= hl;
-  hz /= hl;
+  const float rh = 1.f / hl;
+  hx *= rh;
+  hy *= rh;
+  hz *= rh;
   float nh = n.x * hx + n.y * hy + n.z * hz;
   float oh = wo.x * hx + wo.y * hy + wo.z * hz;
   float pdf_ggx = 0.f;
