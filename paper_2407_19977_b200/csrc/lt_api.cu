@@ -536,6 +536,27 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
   s->n_nodes = nn;
   pt.mark("stream + attributes");
 
+  // --- start every upload that depends only on the description now, so the
+  // copies (pinned sources: asynchronous DMA) overlap the host-side
+  // renumbering and collapse below
+  TmpBuf t_v[6], t_mat, t_order, t_end, t_bmin, t_bmax, t_left, t_right, t_first, t_count,
+      t_perm, t_new, t_wch, t_wof;
+  const double *src[6] = {d->v0, d->v1, d->v2, d->n0, d->n1, d->n2};
+  for (int k = 0; k < 6; ++k) RET(upload(t_v[k], src[k], 3 * n, st));
+  RET(upload(t_mat, d->material_index, n, st));
+  RET(upload(t_order, d->triangle_order, n, st));
+  RET(upload(t_bmin, d->bounds_min, 3 * nn, st));
+  RET(upload(t_bmax, d->bounds_max, 3 * nn, st));
+  RET(upload(t_left, d->left_child, nn, st));
+  RET(upload(t_right, d->right_child, nn, st));
+  RET(upload(t_first, d->first_triangle, nn, st));
+  RET(upload(t_count, d->triangle_count, nn, st));
+  // leaf-end flags of the leaf-ordered triangle stream, on the device
+  RET(t_end.alloc(std::max<int64_t>(n, 16), st));
+  CK(cudaMemsetAsync(t_end.p, 0, (size_t)n, st));
+  launch_leaf_end(t_first.as<int32_t>(), t_count.as<int32_t>(), nn, t_end.as<uint8_t>(), st);
+  pt.mark("uploads enqueue");
+
   // --- internal-node renumbering: top levels BFS, the rest depth-first
   std::vector<int32_t> new_index(nn, -1), perm;
   perm.reserve(nn);
@@ -608,23 +629,9 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
   }
   s->n_wide = (int64_t)(wide_children.size() / 4);
   pt.mark("4-wide collapse");
-  // leaf-end flags for the leaf-ordered triangle stream
-  std::vector<uint8_t> leaf_end(n, 0);
-  for (int64_t i = 0; i < nn; ++i)
-    if (is_leaf(i)) leaf_end[d->first_triangle[i] + d->triangle_count[i] - 1] = 1;
-
-  pt.mark("leaf flags");
-  // --- upload the float64 arrays and flatten on the device
-  TmpBuf t_v[6], t_mat, t_order, t_end, t_bmin, t_bmax, t_left, t_right, t_first, t_count,
-      t_perm, t_new, t_wch, t_wof;
-  const double *src[6] = {d->v0, d->v1, d->v2, d->n0, d->n1, d->n2};
+  // --- flatten on the device
   int rc = LT_OK;
   do {
-    for (int k = 0; k < 6 && rc == LT_OK; ++k) rc = upload(t_v[k], src[k], 3 * n, st);
-    if (rc) break;
-    if ((rc = upload(t_mat, d->material_index, n, st))) break;
-    if ((rc = upload(t_order, d->triangle_order, n, st))) break;
-    if ((rc = upload(t_end, leaf_end.data(), n, st))) break;
     s->nodes_bytes = (size_t)std::max<int64_t>(1, s->n_wide) * 128;
     // shading records start on a 128 B boundary so each 64 B record is
     // half of one cache line
@@ -641,12 +648,6 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
                         t_mat.as<int32_t>(), t_order.as<int32_t>(), t_end.as<uint8_t>(), n,
                         g_tris, g_shade, st);
     if (s->n_internal > 0) {
-      if ((rc = upload(t_bmin, d->bounds_min, 3 * nn, st))) break;
-      if ((rc = upload(t_bmax, d->bounds_max, 3 * nn, st))) break;
-      if ((rc = upload(t_left, d->left_child, nn, st))) break;
-      if ((rc = upload(t_right, d->right_child, nn, st))) break;
-      if ((rc = upload(t_first, d->first_triangle, nn, st))) break;
-      if ((rc = upload(t_count, d->triangle_count, nn, st))) break;
       if ((rc = upload(t_perm, perm.data(), perm.size(), st))) break;
       if ((rc = upload(t_new, new_index.data(), nn, st))) break;
       launch_flatten_nodes(t_bmin.as<double>(), t_bmax.as<double>(), t_left.as<int32_t>(),
@@ -720,7 +721,7 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
   const char *os_env = std::getenv("LT_OCTANT_SORT");
   s->octant_sort = os_env ? os_env[0] == '1' : true;
   const char *rf = std::getenv("LT_REFILL");
-  v.refill_min = std::max(1, std::min(32, rf ? std::atoi(rf) : 8));
+  v.refill_min = std::max(1, std::min(32, rf ? std::atoi(rf) : 16));
   return LT_OK;
 }
 

@@ -87,6 +87,15 @@ __global__ void k_flatten_wide(const double *__restrict__ bmin, const double *__
   o[7] = make_float4(0.f, 0.f, 0.f, 0.f);
 }
 
+// End-of-leaf flags of the leaf-ordered triangle stream.
+__global__ void k_leaf_end(const int32_t *__restrict__ first, const int32_t *__restrict__ count,
+                           int64_t n_nodes, uint8_t *__restrict__ leaf_end) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n_nodes) return;
+  const int32_t c = count[i];
+  if (c > 0) leaf_end[(int64_t)first[i] + c - 1] = 1;
+}
+
 // Triangles in leaf order k (triangle_order[k]); e1/e2 from float64
 // differences rounded once; shading normals + material index alongside.
 __global__ void k_flatten_tris(const double *__restrict__ v0, const double *__restrict__ v1,
@@ -134,7 +143,9 @@ __global__ void k_flatten_tris(const double *__restrict__ v0, const double *__re
 // round-trip through HBM; returns the PCG state after the two draws.
 __device__ __forceinline__ void primary_ray(const RaygenArgs &ra, int64_t p, f3 &o, f3 &d,
                                             uint64_t &state, uint64_t &inc) {
-  const int64_t s_local = p / ra.n_pix;
+  // batch-local path index and pixel count are < 2^31 (int32 queues): a
+  // 32-bit division instead of the 64-bit software routine
+  const int64_t s_local = (int64_t)((uint32_t)p / (uint32_t)ra.n_pix);
   const int64_t i = p - s_local * ra.n_pix;
   const int64_t pix = ra.pix_list ? (int64_t)ra.pix_list[ra.pix_offset + i] : ra.pix_offset + i;
   const int64_t sample = ra.sample_base + s_local;
@@ -151,7 +162,9 @@ __device__ __forceinline__ void primary_ray(const RaygenArgs &ra, int64_t p, f3 
 // depth-0 shade launch regenerates it instead of reading it back.
 __device__ __forceinline__ void primary_rng(const RaygenArgs &ra, int64_t p, uint64_t &state,
                                             uint64_t &inc) {
-  const int64_t s_local = p / ra.n_pix;
+  // batch-local path index and pixel count are < 2^31 (int32 queues): a
+  // 32-bit division instead of the 64-bit software routine
+  const int64_t s_local = (int64_t)((uint32_t)p / (uint32_t)ra.n_pix);
   const int64_t i = p - s_local * ra.n_pix;
   const int64_t pix = ra.pix_list ? (int64_t)ra.pix_list[ra.pix_offset + i] : ra.pix_offset + i;
   seed_stream((uint64_t)pix, (uint64_t)(ra.sample_base + s_local), ra.seed, state, inc);
@@ -815,6 +828,12 @@ void launch_flatten_wide(const double *bmin, const double *bmax, const int32_t *
   if (n_wide <= 0) return;
   k_flatten_wide<<<(unsigned)((n_wide + 255) / 256), 256, 0, st>>>(bmin, bmax, first, count,
                                                                    children, wide_of, n_wide, out);
+}
+
+void launch_leaf_end(const int32_t *first, const int32_t *count, int64_t n_nodes,
+                     uint8_t *leaf_end, cudaStream_t st) {
+  if (n_nodes <= 0) return;
+  k_leaf_end<<<(unsigned)((n_nodes + 255) / 256), 256, 0, st>>>(first, count, n_nodes, leaf_end);
 }
 
 void launch_flatten_tris(const double *v0, const double *v1, const double *v2, const double *n0,

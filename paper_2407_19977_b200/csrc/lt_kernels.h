@@ -67,6 +67,9 @@ void launch_flatten_nodes(const double *bmin, const double *bmax, const int32_t 
                           const int32_t *right, const int32_t *first, const int32_t *count,
                           const int32_t *perm, const int32_t *new_index, int64_t n_internal,
                           float4 *out, cudaStream_t st);
+// leaf_end[first + count - 1] = 1 for every leaf node (flags pre-zeroed)
+void launch_leaf_end(const int32_t *first, const int32_t *count, int64_t n_nodes,
+                     uint8_t *leaf_end, cudaStream_t st);
 void launch_flatten_wide(const double *bmin, const double *bmax, const int32_t *first,
                          const int32_t *count, const int32_t *children, const int32_t *wide_of,
                          int64_t n_wide, float4 *out, cudaStream_t st);

@@ -190,23 +190,32 @@ def render_progressive(scene, settings: RenderSettings, bvh=None, threads: int |
     return res
 
 
-_PINNED: dict = {}
+_PINNED_PRIMED: set = set()
 
 
 def fetch_image(acc: Accumulator, stream=None):
-    """(h, w, 3) float64 means and (h, w) int64 invalid counts on the host,
-    through cached pinned staging buffers (one per image size and device)."""
+    """(h, w, 3) float64 means and (h, w) int64 invalid counts on the host.
+    Both are produced in their final dtype on the device and copied once into
+    page-locked buffers from torch's caching host allocator; the returned
+    arrays own those buffers (no host-side copy), which return to the cache
+    when the caller drops them."""
     import torch
     h, w = acc.height, acc.width
-    key = (h, w, acc.device.index)
-    if key not in _PINNED:
-        _PINNED[key] = (torch.empty((h, w, 3), dtype=torch.float64, pin_memory=True),
-                        torch.empty((h, w), dtype=torch.int32, pin_memory=True))
-    mean_h, inv_h = _PINNED[key]
+    key = (h, w)
+    if key not in _PINNED_PRIMED:
+        # page-locking is slow (tens of ms for a 1080p result); two spare
+        # pairs stay in the allocator's cache so a caller that still holds the
+        # previous image (res = render(...) in a loop) never pins anew
+        spare = [(torch.empty((h, w, 3), dtype=torch.float64, pin_memory=True),
+                  torch.empty((h, w), dtype=torch.int64, pin_memory=True)) for _ in range(2)]
+        del spare
+        _PINNED_PRIMED.add(key)
+    mean_h = torch.empty((h, w, 3), dtype=torch.float64, pin_memory=True)
+    inv_h = torch.empty((h, w), dtype=torch.int64, pin_memory=True)
     mean_h.copy_(acc.mean(), non_blocking=True)
-    inv_h.copy_(acc.invalid.view(h, w), non_blocking=True)
+    inv_h.copy_(acc.invalid.view(h, w).to(torch.int64), non_blocking=True)
     (stream or torch.cuda.current_stream(acc.device)).synchronize()
-    return mean_h.numpy().copy(), inv_h.numpy().astype(np.int64)
+    return mean_h.numpy(), inv_h.numpy()
 
 
 def render_image(scene, settings: RenderSettings, bvh=None, threads: int | None = None,
