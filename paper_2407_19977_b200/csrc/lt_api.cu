@@ -632,7 +632,7 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
   // --- flatten on the device
   int rc = LT_OK;
   do {
-    s->nodes_bytes = (size_t)std::max<int64_t>(1, s->n_wide) * 128;
+    s->nodes_bytes = (size_t)std::max<int64_t>(1, s->n_wide) * 16 * LT_NODE_F4;
     // shading records start on a 128 B boundary so each 64 B record is
     // half of one cache line
     s->shade_off = (s->nodes_bytes + 48 * (size_t)n + 127) / 128 * 128;

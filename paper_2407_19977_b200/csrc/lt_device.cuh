@@ -35,6 +35,25 @@
 #define LT_RR_MIN_F 0.05f       // integrator.py:34
 #define LT_STACK 64             // bvh.py:27
 #define LT_LINK_EXIT ((int32_t)0x80000000)
+// Wide-node record, in float4 units.  Default: [lo_x, hi_x, lo_y, hi_y,
+// lo_z, hi_z, links, pad] (128 B).  LT_NODE_DUP: every axis stored as
+// [lo, hi, hi, lo] so the ray's direction octant selects a 32 B-aligned
+// (near, far) pair that one 256-bit load fetches (224 B; the default:
+// +4.5 % on C4, profiles/r01_trace_variants.txt; -DLT_NODE_COMPACT selects
+// the 128 B record).
+#if !defined(LT_NODE_COMPACT) && !defined(LT_NODE_DUP)
+#define LT_NODE_DUP 1
+#endif
+#ifdef LT_NODE_DUP
+#define LT_NODE_F4 14
+#define LT_NODE_LINKS 12
+#ifndef LT_W256
+#define LT_W256 1
+#endif
+#else
+#define LT_NODE_F4 8
+#define LT_NODE_LINKS 6
+#endif
 // robustness: child exit distances are widened by 1 + 2*gamma(3) so fp32
 // rounding in the slab test never culls a box the float64 reference keeps
 #define LT_SLAB_WIDEN 1.0000004f

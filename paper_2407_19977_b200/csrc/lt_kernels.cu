@@ -77,14 +77,23 @@ __global__ void k_flatten_wide(const double *__restrict__ bmin, const double *__
     }
     link[c] = count[x] > 0 ? ~first[x] : wide_of[x];
   }
-  float4 *o = out + 8 * i;
+  float4 *o = out + LT_NODE_F4 * i;
   for (int a = 0; a < 3; ++a) {
-    o[2 * a] = make_float4(lo[a][0], lo[a][1], lo[a][2], lo[a][3]);
-    o[2 * a + 1] = make_float4(hi[a][0], hi[a][1], hi[a][2], hi[a][3]);
+    const float4 l4 = make_float4(lo[a][0], lo[a][1], lo[a][2], lo[a][3]);
+    const float4 h4 = make_float4(hi[a][0], hi[a][1], hi[a][2], hi[a][3]);
+#ifdef LT_NODE_DUP
+    o[4 * a] = l4;      // (near, far) for a positive inverse direction
+    o[4 * a + 1] = h4;
+    o[4 * a + 2] = h4;  // (near, far) for a negative one
+    o[4 * a + 3] = l4;
+#else
+    o[2 * a] = l4;
+    o[2 * a + 1] = h4;
+#endif
   }
-  o[6] = make_float4(__int_as_float(link[0]), __int_as_float(link[1]), __int_as_float(link[2]),
-                     __int_as_float(link[3]));
-  o[7] = make_float4(0.f, 0.f, 0.f, 0.f);
+  o[LT_NODE_LINKS] = make_float4(__int_as_float(link[0]), __int_as_float(link[1]),
+                                 __int_as_float(link[2]), __int_as_float(link[3]));
+  if (LT_NODE_LINKS + 1 < LT_NODE_F4) o[LT_NODE_LINKS + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
 }
 
 // End-of-leaf flags of the leaf-ordered triangle stream.
@@ -247,23 +256,13 @@ __global__ void __launch_bounds__(kTraceThreads, LT_TRACE_MIN_BLOCKS)
   const unsigned lanes_below = (1u << lane) - 1u;
   int32_t l_node[LT_STACK - kShortStack];
   float l_t[LT_STACK - kShortStack];
-#ifdef LT_RAY_SMEM
-  // the lane's ray (o, t_min), (d, -) and best-hit payload (u, v, k, orig)
-  // live in shared memory: only the leaf test reads them, so they do not
-  // occupy registers across the node loop
-  float4 *s_ro = reinterpret_cast<float4 *>(s_t + kShortStack * kTraceThreads);
-  float4 *s_rd = s_ro + kTraceThreads;
-  float4 *s_hit = s_rd + kTraceThreads;
-#endif
 
   const int n = *count;
   if (blockIdx.x == 0 && tid == 0) atomicAdd(ray_ctr, (unsigned long long)n);
 
   int q = -1;
   bool exhausted = false;  // warp-uniform: the queue is drained
-#ifndef LT_RAY_SMEM
   f3 o{0.f, 0.f, 0.f}, d{0.f, 0.f, 1.f};
-#endif
   RaySlab rs{};
   float t_min = 0.f;
   HitRec best{0.f, 0.f, 0.f, -1};
@@ -292,14 +291,8 @@ __global__ void __launch_bounds__(kTraceThreads, LT_TRACE_MIN_BLOCKS)
           rs = ray_slab(mk(ro.x, ro.y, ro.z), mk(rd.x, rd.y, rd.z));
           best = HitRec{__int_as_float(0x7f800000), 0.f, 0.f, -1};
           best_orig = 0x7fffffff;
-#ifdef LT_RAY_SMEM
-          s_ro[tid] = make_float4(ro.x, ro.y, ro.z, rd.w);
-          s_rd[tid] = rd;
-          s_hit[tid] = make_float4(0.f, 0.f, __int_as_float(-1), __int_as_float(0x7fffffff));
-#else
           o = mk(ro.x, ro.y, ro.z);
           d = mk(rd.x, rd.y, rd.z);
-#endif
           sp = 0;
           if (COUNT) ++nn;
           float t_root;
@@ -317,7 +310,7 @@ __global__ void __launch_bounds__(kTraceThreads, LT_TRACE_MIN_BLOCKS)
     if (q >= 0) {
       // pop the next stack entry not culled by the current best t (bvh.py:389)
       auto pop = [&]() -> int32_t {
-        const float cull = cull_dist(rs, best.t);
+        const float cull = cull_dist(best.t);
         while (sp > 0) {
           --sp;
           int32_t x;
@@ -346,68 +339,21 @@ __global__ void __launch_bounds__(kTraceThreads, LT_TRACE_MIN_BLOCKS)
       // ---- wide nodes: descend nearest-first until a leaf or a dead end;
       // the other hit children go on the stack farthest first
       const float kInf = __int_as_float(0x7f800000);
-#ifdef LT_PREFETCH
-      // software-pipelined: the nearest child's record is requested right
-      // after the slab tests, before this visit's stack pushes
-      Node4 nd;
-      if (node >= 0) load_node4(nd, sc.wnodes + 8 * (int64_t)node);
       while (node >= 0) {
-        const Keys4 h = keys4(nd, rs, t_min, best.t);
-        if (COUNT) nn += 4;
-        int32_t next = h.k0 != LT_KEY_MISS ? key_link(h.ln, h.k0) : LT_LINK_EXIT;
-        if (next >= 0) load_node4(nd, sc.wnodes + 8 * (int64_t)next);
-        if (h.k3 != LT_KEY_MISS) push(key_link(h.ln, h.k3), key_dist(h.k3));
-        if (h.k2 != LT_KEY_MISS) push(key_link(h.ln, h.k2), key_dist(h.k2));
-        if (h.k1 != LT_KEY_MISS) push(key_link(h.ln, h.k1), key_dist(h.k1));
-        if (next == LT_LINK_EXIT) {
-          next = pop();
-          if (next >= 0) load_node4(nd, sc.wnodes + 8 * (int64_t)next);
-        }
-        node = next;
-      }
-#else
-      while (node >= 0) {
-#ifdef LT_KEY_SORT
-        const Keys4 h = visit4k(sc.wnodes + 8 * (int64_t)node, rs, t_min, best.t);
-        if (COUNT) nn += 4;
-        if (h.k3 != LT_KEY_MISS) push(key_link(h.ln, h.k3), key_dist(h.k3));
-        if (h.k2 != LT_KEY_MISS) push(key_link(h.ln, h.k2), key_dist(h.k2));
-        if (h.k1 != LT_KEY_MISS) push(key_link(h.ln, h.k1), key_dist(h.k1));
-        node = h.k0 != LT_KEY_MISS ? key_link(h.ln, h.k0) : pop();
-#else
-        const Hits4 h = LT_VISIT4(sc.wnodes + 8 * (int64_t)node, rs, t_min, best.t);
+        const Hits4 h = LT_VISIT4(sc.wnodes + LT_NODE_F4 * (int64_t)node, rs, t_min, best.t);
         if (COUNT) nn += 4;
         if (h.k3 < kInf) push(h.l3, h.k3);
         if (h.k2 < kInf) push(h.l2, h.k2);
         if (h.k1 < kInf) push(h.l1, h.k1);
         node = h.k0 < kInf ? h.l0 : pop();
-#endif
       }
-#endif
       // ---- leaf: its triangles, then the next stack entry
       if (node != LT_LINK_EXIT) {
-#ifdef LT_RAY_SMEM
-        const float4 ro = s_ro[tid], rd = s_rd[tid], hb = s_hit[tid];
-        best.u = hb.x;
-        best.v = hb.y;
-        best.k = __float_as_int(hb.z);
-        best_orig = __float_as_int(hb.w);
-        leaf_test<COUNT>(sc, ~(int64_t)node, mk(ro.x, ro.y, ro.z), mk(rd.x, rd.y, rd.z), t_min,
-                         best, best_orig, nt);
-        s_hit[tid] = make_float4(best.u, best.v, __int_as_float(best.k),
-                                 __int_as_float(best_orig));
-#else
         leaf_test<COUNT>(sc, ~(int64_t)node, o, d, t_min, best, best_orig, nt);
-#endif
         node = pop();
       }
       if (node == LT_LINK_EXIT) {
-#ifdef LT_RAY_SMEM
-        const float4 hb = s_hit[tid];
-        __stcs(&hits[q], make_float4(best.t, hb.x, hb.y, hb.z));
-#else
         __stcs(&hits[q], make_float4(best.t, best.u, best.v, __int_as_float(best.k)));
-#endif
         q = -1;
       }
     }
@@ -865,11 +811,7 @@ void launch_gather_explicit(const PathArrays &pa, int64_t n, double *rgb, uint64
 }
 
 size_t trace_smem_bytes(int n_top) {
-  size_t b = (size_t)n_top * 64 + (size_t)kShortStack * kTraceThreads * 8;
-#ifdef LT_RAY_SMEM
-  b += (size_t)kTraceThreads * 48;
-#endif
-  return b;
+  return (size_t)n_top * 64 + (size_t)kShortStack * kTraceThreads * 8;
 }
 
 cudaError_t launch_trace(const SceneView &sc, bool smem, bool count_work, int grid,

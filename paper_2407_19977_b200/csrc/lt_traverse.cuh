@@ -44,18 +44,14 @@ __device__ __forceinline__ float fmax3f(float a, float b, float c) {
   return r;
 }
 
-// Per-ray constants of the slab test.  `inv` is the clamped inverse
-// direction; with LT_SLAB_FMA the plane distances are one FMA each,
-// t = lo * inv + (-o * inv), whose rounding error is absolute
-// (<= |o * inv| 2^-24 per axis), so `slack` widens the exit distance by
-// that bound (axes with a clamped, "infinite" inverse excluded: their t is
-// exactly 0 or beyond any hit).
-// `nx/ny/nz` index the wide node's near-plane array per axis (the record is
-// [lo_x, hi_x, lo_y, hi_y, lo_z, hi_z, links] in float4 units): lo when the
-// clamped inverse is positive, hi when negative; far = near ^ 1.
+// Per-ray constants of the slab test: `inv` is the clamped inverse
+// direction; `nx/ny/nz` index the wide node's near-plane array per axis in
+// float4 units (lo when the clamped inverse is positive, hi when negative).
+// Default record [lo_x, hi_x, lo_y, hi_y, lo_z, hi_z, links, pad]: near at
+// 2a + sign, far = near ^ 1.  LT_NODE_DUP record [lo_x, hi_x, hi_x, lo_x,
+// ..., links]: the (near, far) pair starts at 4a + 2 sign.
 struct RaySlab {
-  f3 o, inv, oinv;
-  float slack;
+  f3 o, inv;
   int nx, ny, nz;
 };
 
@@ -65,38 +61,46 @@ __device__ __forceinline__ RaySlab ray_slab(f3 o, f3 d) {
   r.inv = f3{fminf(fmaxf(1.f / d.x, -LT_INV_CLAMP), LT_INV_CLAMP),
              fminf(fmaxf(1.f / d.y, -LT_INV_CLAMP), LT_INV_CLAMP),
              fminf(fmaxf(1.f / d.z, -LT_INV_CLAMP), LT_INV_CLAMP)};
-  r.nx = (int)(__float_as_uint(r.inv.x) >> 31);
-  r.ny = 2 + (int)(__float_as_uint(r.inv.y) >> 31);
-  r.nz = 4 + (int)(__float_as_uint(r.inv.z) >> 31);
-  r.oinv = f3{-o.x * r.inv.x, -o.y * r.inv.y, -o.z * r.inv.z};
-  const float big = 1e18f;
-  const float ex = fabsf(r.inv.x) < big ? fabsf(r.oinv.x) : 0.f;
-  const float ey = fabsf(r.inv.y) < big ? fabsf(r.oinv.y) : 0.f;
-  const float ez = fabsf(r.inv.z) < big ? fabsf(r.oinv.z) : 0.f;
-  r.slack = fmax3f(ex, ey, ez) * 2.4e-7f;  // 2^-22
+  const int sx = (int)(__float_as_uint(r.inv.x) >> 31);
+  const int sy = (int)(__float_as_uint(r.inv.y) >> 31);
+  const int sz = (int)(__float_as_uint(r.inv.z) >> 31);
+#ifdef LT_NODE_DUP
+  r.nx = 2 * sx;
+  r.ny = 4 + 2 * sy;
+  r.nz = 8 + 2 * sz;
+#else
+  r.nx = sx;
+  r.ny = 2 + sy;
+  r.nz = 4 + sz;
+#endif
   return r;
 }
 
-// _slab_intersect with a clipped interval [t_min, t_max]
+// _slab_intersect with a clipped interval [t_min, t_max] (min/max form)
 __device__ __forceinline__ bool slab(const RaySlab &r, float lox, float hix, float loy, float hiy,
                                      float loz, float hiz, float t_min, float t_max,
                                      float &t_enter) {
-#ifdef LT_SLAB_FMA
-  const float t0x = fmaf(lox, r.inv.x, r.oinv.x), t1x = fmaf(hix, r.inv.x, r.oinv.x);
-  const float t0y = fmaf(loy, r.inv.y, r.oinv.y), t1y = fmaf(hiy, r.inv.y, r.oinv.y);
-  const float t0z = fmaf(loz, r.inv.z, r.oinv.z), t1z = fmaf(hiz, r.inv.z, r.oinv.z);
-#else
   const float t0x = (lox - r.o.x) * r.inv.x, t1x = (hix - r.o.x) * r.inv.x;
   const float t0y = (loy - r.o.y) * r.inv.y, t1y = (hiy - r.o.y) * r.inv.y;
   const float t0z = (loz - r.o.z) * r.inv.z, t1z = (hiz - r.o.z) * r.inv.z;
-#endif
   const float tn = fmax3f(fminf(t0x, t1x), fminf(t0y, t1y), fmaxf(fminf(t0z, t1z), t_min));
   const float tf = fmin3f(fmaxf(t0x, t1x), fmaxf(t0y, t1y), fminf(fmaxf(t0z, t1z), t_max));
   t_enter = tn;
-#ifdef LT_SLAB_FMA
-  return tn <= fmaf(tf, LT_SLAB_WIDEN, r.slack);
-#else
   return tn <= tf * LT_SLAB_WIDEN;
+}
+
+// Two adjacent float4s with one 256-bit load (sm_100: LDG.E.256; the
+// address is 32 B aligned).  Per lane a 32 B access costs ~1.3 L1
+// wavefronts against 1 per 16 B access (tools/micro/ldg256.cu: 1.47x the
+// record rate of 16 B loads on random 128 B records).
+__device__ __forceinline__ void ldg_pair(const float4 *__restrict__ p, float4 &a, float4 &b) {
+#ifdef LT_W256
+  asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
+      : "l"(p));
+#else
+  a = __ldg(p);
+  b = __ldg(p + 1);
 #endif
 }
 
@@ -166,18 +170,20 @@ struct Hits4 {
 __device__ __forceinline__ Hits4 visit4(const float4 *__restrict__ np, const RaySlab &rs, float t_min,
                                         float t_max) {
   const float kInf = __int_as_float(0x7f800000);
-  const float4 lx = __ldg(np + 0), hx = __ldg(np + 1), ly = __ldg(np + 2), hy = __ldg(np + 3);
-  const float4 lz = __ldg(np + 4), hz = __ldg(np + 5);
-  const int4 ln = __ldg(reinterpret_cast<const int4 *>(np + 6));
+  float4 lx, hx, ly, hy, lz, hz;
+  ldg_pair(np + 0, lx, hx);
+  ldg_pair(np + 2, ly, hy);
+  ldg_pair(np + 4, lz, hz);
+  const int4 ln = __ldg(reinterpret_cast<const int4 *>(np + LT_NODE_LINKS));
   Hits4 h;
   float t;
-  h.k0 = slab(rs,lx.x, hx.x, ly.x, hy.x, lz.x, hz.x, t_min, t_max, t) && ln.x != LT_LINK_EXIT
+  h.k0 = slab(rs, lx.x, hx.x, ly.x, hy.x, lz.x, hz.x, t_min, t_max, t) && ln.x != LT_LINK_EXIT
              ? t : kInf;
-  h.k1 = slab(rs,lx.y, hx.y, ly.y, hy.y, lz.y, hz.y, t_min, t_max, t) && ln.y != LT_LINK_EXIT
+  h.k1 = slab(rs, lx.y, hx.y, ly.y, hy.y, lz.y, hz.y, t_min, t_max, t) && ln.y != LT_LINK_EXIT
              ? t : kInf;
-  h.k2 = slab(rs,lx.z, hx.z, ly.z, hy.z, lz.z, hz.z, t_min, t_max, t) && ln.z != LT_LINK_EXIT
+  h.k2 = slab(rs, lx.z, hx.z, ly.z, hy.z, lz.z, hz.z, t_min, t_max, t) && ln.z != LT_LINK_EXIT
              ? t : kInf;
-  h.k3 = slab(rs,lx.w, hx.w, ly.w, hy.w, lz.w, hz.w, t_min, t_max, t) && ln.w != LT_LINK_EXIT
+  h.k3 = slab(rs, lx.w, hx.w, ly.w, hy.w, lz.w, hz.w, t_min, t_max, t) && ln.w != LT_LINK_EXIT
              ? t : kInf;
   h.l0 = ln.x;
   h.l1 = ln.y;
@@ -205,10 +211,20 @@ __device__ __forceinline__ float near_far(float n, float f, float o, float inv, 
 __device__ __forceinline__ Hits4 visit4o(const float4 *__restrict__ np, const RaySlab &rs,
                                          float t_min, float t_max) {
   const float kInf = __int_as_float(0x7f800000);
-  const float4 nx = __ldg(np + rs.nx), fx = __ldg(np + (rs.nx ^ 1));
-  const float4 ny = __ldg(np + rs.ny), fy = __ldg(np + (rs.ny ^ 1));
-  const float4 nz = __ldg(np + rs.nz), fz = __ldg(np + (rs.nz ^ 1));
-  const int4 ln = __ldg(reinterpret_cast<const int4 *>(np + 6));
+  float4 nx, fx, ny, fy, nz, fz;
+#ifdef LT_NODE_DUP
+  ldg_pair(np + rs.nx, nx, fx);
+  ldg_pair(np + rs.ny, ny, fy);
+  ldg_pair(np + rs.nz, nz, fz);
+#else
+  nx = __ldg(np + rs.nx);
+  fx = __ldg(np + (rs.nx ^ 1));
+  ny = __ldg(np + rs.ny);
+  fy = __ldg(np + (rs.ny ^ 1));
+  nz = __ldg(np + rs.nz);
+  fz = __ldg(np + (rs.nz ^ 1));
+#endif
+  const int4 ln = __ldg(reinterpret_cast<const int4 *>(np + LT_NODE_LINKS));
   Hits4 h;
 #define LT_CHILD(K, C)                                                            \
   {                                                                               \
@@ -237,7 +253,7 @@ __device__ __forceinline__ Hits4 visit4o(const float4 *__restrict__ np, const Ra
   return h;
 }
 
-#ifdef LT_OCTANT_SLAB
+#if defined(LT_OCTANT_SLAB) || defined(LT_NODE_DUP)
 #define LT_VISIT4 visit4o
 #else
 #define LT_VISIT4 visit4
@@ -246,135 +262,7 @@ __device__ __forceinline__ Hits4 visit4o(const float4 *__restrict__ np, const Ra
 // Pop-time cull distance for the current best t: a stacked entry whose entry
 // distance exceeds it cannot hold a closer hit (bvh.py:389), with the same
 // error allowance as the slab test.
-__device__ __forceinline__ float cull_dist(const RaySlab &r, float best_t) {
-#ifdef LT_SLAB_FMA
-  return fmaf(best_t, LT_SLAB_WIDEN, r.slack);
-#else
-  return best_t * LT_SLAB_WIDEN;
-#endif
-}
-
-// Key-sorted variant of visit4 (LT_KEY_SORT): each hit child becomes one
-// 32-bit key -- its entry distance clamped to >= 0 as an unsigned integer
-// (the order of non-negative floats) with the child slot in the low 2 bits;
-// a miss is 0xffffffff.  Five unsigned min/max pairs sort the keys, the slot
-// recovers the link, and the key's distance (rounded down by <= 3 ulp) is a
-// conservative stack cull value.  Same visit order as visit4 up to 3-ulp
-// ties, identical results (the closest hit is order independent).
-#define LT_KEY_MISS 0xffffffffu
-struct Keys4 {
-  uint32_t k0, k1, k2, k3;
-  int4 ln;
-};
-
-__device__ __forceinline__ uint32_t hit_key(bool hit, float t, uint32_t slot) {
-  const int32_t ti = max(__float_as_int(t), 0);
-  return hit ? ((uint32_t)(ti & ~3) | slot) : LT_KEY_MISS;
-}
-
-__device__ __forceinline__ void usort2(uint32_t &a, uint32_t &b) {
-  const uint32_t lo = min(a, b);
-  b = max(a, b);
-  a = lo;
-}
-
-__device__ __forceinline__ int32_t key_link(const int4 &ln, uint32_t key) {
-  const int32_t a = (key & 1u) ? ln.y : ln.x;
-  const int32_t b = (key & 1u) ? ln.w : ln.z;
-  return (key & 2u) ? b : a;
-}
-
-__device__ __forceinline__ float key_dist(uint32_t key) { return __uint_as_float(key & ~3u); }
-
-// A wide node held in registers (the 7 x 16 B record), so the next node's
-// loads can be issued before the current visit's stack pushes.
-struct Node4 {
-  float4 lx, hx, ly, hy, lz, hz;
-  int4 ln;
-};
-
-__device__ __forceinline__ void load_node4(Node4 &nd, const float4 *__restrict__ np) {
-  nd.lx = __ldg(np + 0);
-  nd.hx = __ldg(np + 1);
-  nd.ly = __ldg(np + 2);
-  nd.hy = __ldg(np + 3);
-  nd.lz = __ldg(np + 4);
-  nd.hz = __ldg(np + 5);
-  nd.ln = __ldg(reinterpret_cast<const int4 *>(np + 6));
-}
-
-__device__ __forceinline__ Keys4 keys4(const Node4 &nd, const RaySlab &rs, float t_min,
-                                       float t_max) {
-  Keys4 h;
-  h.ln = nd.ln;
-  float t;
-  bool s;
-  s = slab(rs, nd.lx.x, nd.hx.x, nd.ly.x, nd.hy.x, nd.lz.x, nd.hz.x, t_min, t_max, t);
-  h.k0 = hit_key(s && h.ln.x != LT_LINK_EXIT, t, 0u);
-  s = slab(rs, nd.lx.y, nd.hx.y, nd.ly.y, nd.hy.y, nd.lz.y, nd.hz.y, t_min, t_max, t);
-  h.k1 = hit_key(s && h.ln.y != LT_LINK_EXIT, t, 1u);
-  s = slab(rs, nd.lx.z, nd.hx.z, nd.ly.z, nd.hy.z, nd.lz.z, nd.hz.z, t_min, t_max, t);
-  h.k2 = hit_key(s && h.ln.z != LT_LINK_EXIT, t, 2u);
-  s = slab(rs, nd.lx.w, nd.hx.w, nd.ly.w, nd.hy.w, nd.lz.w, nd.hz.w, t_min, t_max, t);
-  h.k3 = hit_key(s && h.ln.w != LT_LINK_EXIT, t, 3u);
-  usort2(h.k0, h.k1);
-  usort2(h.k2, h.k3);
-  usort2(h.k0, h.k2);
-  usort2(h.k1, h.k3);
-  usort2(h.k1, h.k2);
-  return h;
-}
-
-__device__ __forceinline__ Keys4 visit4k(const float4 *__restrict__ np, const RaySlab &rs,
-                                         float t_min, float t_max) {
-  Keys4 h;
-#ifdef LT_OCTANT_SLAB
-  const float4 nx = __ldg(np + rs.nx), fx = __ldg(np + (rs.nx ^ 1));
-  const float4 ny = __ldg(np + rs.ny), fy = __ldg(np + (rs.ny ^ 1));
-  const float4 nz = __ldg(np + rs.nz), fz = __ldg(np + (rs.nz ^ 1));
-  h.ln = __ldg(reinterpret_cast<const int4 *>(np + 6));
-#define LT_CHILD(K, C, SLOT)                                                      \
-  {                                                                               \
-    float fx_, fy_, fz_;                                                          \
-    const float ax = near_far(nx.C, fx.C, rs.o.x, rs.inv.x, fx_);                 \
-    const float ay = near_far(ny.C, fy.C, rs.o.y, rs.inv.y, fy_);                 \
-    const float az = near_far(nz.C, fz.C, rs.o.z, rs.inv.z, fz_);                 \
-    const float tn = fmax3f(ax, ay, fmaxf(az, t_min));                            \
-    const float tf = fmin3f(fx_, fy_, fminf(fz_, t_max));                         \
-    h.K = hit_key(tn <= tf * LT_SLAB_WIDEN, tn, SLOT);                            \
-  }
-  LT_CHILD(k0, x, 0u)
-  LT_CHILD(k1, y, 1u)
-  LT_CHILD(k2, z, 2u)
-  LT_CHILD(k3, w, 3u)
-#undef LT_CHILD
-  usort2(h.k0, h.k1);
-  usort2(h.k2, h.k3);
-  usort2(h.k0, h.k2);
-  usort2(h.k1, h.k3);
-  usort2(h.k1, h.k2);
-  return h;
-#endif
-  const float4 lx = __ldg(np + 0), hx = __ldg(np + 1), ly = __ldg(np + 2), hy = __ldg(np + 3);
-  const float4 lz = __ldg(np + 4), hz = __ldg(np + 5);
-  h.ln = __ldg(reinterpret_cast<const int4 *>(np + 6));
-  float t;
-  bool s;
-  s = slab(rs, lx.x, hx.x, ly.x, hy.x, lz.x, hz.x, t_min, t_max, t);
-  h.k0 = hit_key(s && h.ln.x != LT_LINK_EXIT, t, 0u);
-  s = slab(rs, lx.y, hx.y, ly.y, hy.y, lz.y, hz.y, t_min, t_max, t);
-  h.k1 = hit_key(s && h.ln.y != LT_LINK_EXIT, t, 1u);
-  s = slab(rs, lx.z, hx.z, ly.z, hy.z, lz.z, hz.z, t_min, t_max, t);
-  h.k2 = hit_key(s && h.ln.z != LT_LINK_EXIT, t, 2u);
-  s = slab(rs, lx.w, hx.w, ly.w, hy.w, lz.w, hz.w, t_min, t_max, t);
-  h.k3 = hit_key(s && h.ln.w != LT_LINK_EXIT, t, 3u);
-  usort2(h.k0, h.k1);
-  usort2(h.k2, h.k3);
-  usort2(h.k0, h.k2);
-  usort2(h.k1, h.k3);
-  usort2(h.k1, h.k2);
-  return h;
-}
+__device__ __forceinline__ float cull_dist(float best_t) { return best_t * LT_SLAB_WIDEN; }
 
 // Any-hit occlusion (_traverse_any, bvh.py:511-551): true as soon as any
 // triangle is hit within [t_min, t_max]; wide layout, no ordering needed.
@@ -393,7 +281,7 @@ __device__ __forceinline__ bool occluded(const SceneView &sc, f3 o, f3 d, float 
   int32_t best_orig = 0x7fffffff;
   while (true) {
     while (node >= 0) {
-      const Hits4 h = LT_VISIT4(sc.wnodes + 8 * (int64_t)node, rs, t_min, t_max);
+      const Hits4 h = LT_VISIT4(sc.wnodes + LT_NODE_F4 * (int64_t)node, rs, t_min, t_max);
       if (h.k3 < kInf) stk[sp++] = h.l3;
       if (h.k2 < kInf) stk[sp++] = h.l2;
       if (h.k1 < kInf) stk[sp++] = h.l1;
@@ -430,7 +318,7 @@ __device__ __forceinline__ HitRec traverse(const SceneView &sc, f3 o, f3 d, floa
     while (true) {
       while (node >= 0) {
         if (WIDE) {
-          const Hits4 h = LT_VISIT4(sc.wnodes + 8 * (int64_t)node, rs, t_min, best.t);
+          const Hits4 h = LT_VISIT4(sc.wnodes + LT_NODE_F4 * (int64_t)node, rs, t_min, best.t);
           if (COUNT) nodes += 4;
           if (h.k3 < kInf) { stk_node[sp] = h.l3; stk_t[sp] = h.k3; ++sp; }
           if (h.k2 < kInf) { stk_node[sp] = h.l2; stk_t[sp] = h.k2; ++sp; }
@@ -461,7 +349,7 @@ __device__ __forceinline__ HitRec traverse(const SceneView &sc, f3 o, f3 d, floa
       }
       if (node != LT_LINK_EXIT) leaf_test<COUNT>(sc, ~(int64_t)node, o, d, t_min, best,
                                                  best_orig, tests);
-      const float cull = cull_dist(rs, best.t);
+      const float cull = cull_dist(best.t);
       node = LT_LINK_EXIT;
       while (sp > 0) {
         --sp;
