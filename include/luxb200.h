@@ -129,6 +129,17 @@ int lt_build_bvh(const double *v0, const double *v1, const double *v2, int64_t n
                  int32_t *triangle_count, int32_t *triangle_order, int64_t *n_nodes,
                  int64_t *leaf_count, int64_t *max_depth);
 
+/* ---- GPU BVH build: build_bvh (bvh.py:286-298) on `device`; the same
+ * arrays as lt_build_bvh / the reference (split decisions, bounds, the
+ * two-pointer partition order and the node numbering reproduced; see
+ * csrc/lt_bvh_gpu.cu).  Host buffers as lt_build_bvh; bins <= 32. ---- */
+int lt_build_bvh_device(int32_t device, const double *v0, const double *v1, const double *v2,
+                        int64_t n, int32_t leaf_size, int32_t bins, double *bounds_min,
+                        double *bounds_max, int32_t *left_child, int32_t *right_child,
+                        int32_t *first_triangle, int32_t *triangle_count,
+                        int32_t *triangle_order, int64_t *n_nodes, int64_t *leaf_count,
+                        int64_t *max_depth);
+
 /* ---- scene residency: replaces the per-call `_scene_arrays` packing
  * (integrator.py:284-291); flattens the host BVH into the HBM layout ---- */
 int lt_scene_create(const lt_scene_desc *desc, int32_t device, lt_scene **out);

@@ -104,6 +104,8 @@ SIGNATURES = {
     "lt_device_count": (C.c_int, [_ip]),
     "lt_build_bvh": (C.c_int, [_dp, _dp, _dp, C.c_int64, C.c_int32, C.c_int32, _dp, _dp, _ip,
                                _ip, _ip, _ip, _ip, _lp, _lp, _lp]),
+    "lt_build_bvh_device": (C.c_int, [C.c_int32, _dp, _dp, _dp, C.c_int64, C.c_int32, C.c_int32,
+                                      _dp, _dp, _ip, _ip, _ip, _ip, _ip, _lp, _lp, _lp]),
     "lt_scene_create": (C.c_int, [C.POINTER(SceneDesc), C.c_int32, C.POINTER(C.c_void_p)]),
     "lt_scene_destroy": (C.c_int, [C.c_void_p]),
     "lt_scene_info_get": (C.c_int, [C.c_void_p, C.POINTER(SceneInfo)]),

@@ -27,7 +27,10 @@ NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas"
 CXX_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-fno-fast-math", "-Wall",
              f"-I{INCLUDE}", f"-I{CSRC}"]
 
-CU_SOURCES = ["lt_kernels.cu", "lt_api.cu"]
+CU_SOURCES = ["lt_kernels.cu", "lt_api.cu", "lt_bvh_gpu.cu"]
+# per-source extra nvcc flags: the BVH build must round every float64 operation
+# like the reference (no FMA contraction)
+CU_EXTRA = {"lt_bvh_gpu.cu": ["-fmad=false"]}
 CPP_SOURCES = ["lt_bvh_build.cpp"]
 HEADERS = ["lt_device.cuh", "lt_material.cuh", "lt_traverse.cuh", "lt_kernels.h",
            "lt_internal.h"]
@@ -67,7 +70,8 @@ def build(force: bool = False, verbose: bool = False, variant: str | None = None
             obj = out / (Path(src).stem + ".o")
             objs.append(obj)
             if force or _stale(obj, [CSRC / src] + headers):
-                _run([NVCC, *ARCH, *NVCC_FLAGS, *dflags, "-c", str(CSRC / src), "-o", str(obj)],
+                _run([NVCC, *ARCH, *NVCC_FLAGS, *CU_EXTRA.get(src, []), *dflags, "-c", str(CSRC / src),
+                      "-o", str(obj)],
                      log)
         for src in CPP_SOURCES:
             obj = out / (Path(src).stem + ".o")

@@ -47,12 +47,22 @@ class Bvh:
         return self.triangle_count[node] > 0
 
 
-def build_bvh(triangles, leaf_size: int = LEAF_SIZE, bins: int = SAH_BINS) -> Bvh:
-    """Binned-SAH build on the host (bvh.py:286-298); ValueError on an empty
-    scene."""
+GPU_MAX_BINS = 32
+
+
+def build_bvh(triangles, leaf_size: int = LEAF_SIZE, bins: int = SAH_BINS, *,
+              device="auto") -> Bvh:
+    """Binned-SAH build (bvh.py:286-298); ValueError on an empty scene.
+
+    Both builders return the reference's arrays: `device` = a CUDA ordinal
+    runs csrc/lt_bvh_gpu.cu on that GPU; None runs the host restatement
+    (csrc/lt_bvh_build.cpp); "auto" (default) uses GPU 0 when one is present
+    and bins <= 32, else the host."""
     n = len(triangles)
     if n == 0:
         raise ValueError("empty scene")
+    if device == "auto":
+        device = 0 if bins <= GPU_MAX_BINS and _lib.device_count() > 0 else None
     v0 = np.ascontiguousarray(triangles.v0, dtype=np.float64)
     v1 = np.ascontiguousarray(triangles.v1, dtype=np.float64)
     v2 = np.ascontiguousarray(triangles.v2, dtype=np.float64)
@@ -63,12 +73,15 @@ def build_bvh(triangles, leaf_size: int = LEAF_SIZE, bins: int = SAH_BINS) -> Bv
     order = np.empty(n, np.int32)
     nn, nl, md = C.c_int64(), C.c_int64(), C.c_int64()
     P = _lib.ptr
+    args = (P(v0, C.c_double), P(v1, C.c_double), P(v2, C.c_double), n, int(leaf_size),
+            int(bins), P(bmin, C.c_double), P(bmax, C.c_double), P(left, C.c_int32),
+            P(right, C.c_int32), P(first, C.c_int32), P(count, C.c_int32), P(order, C.c_int32),
+            C.byref(nn), C.byref(nl), C.byref(md))
     t0 = time.perf_counter()
-    _lib.check(_lib.lib().lt_build_bvh(
-        P(v0, C.c_double), P(v1, C.c_double), P(v2, C.c_double), n, int(leaf_size), int(bins),
-        P(bmin, C.c_double), P(bmax, C.c_double), P(left, C.c_int32), P(right, C.c_int32),
-        P(first, C.c_int32), P(count, C.c_int32), P(order, C.c_int32),
-        C.byref(nn), C.byref(nl), C.byref(md)))
+    if device is None:
+        _lib.check(_lib.lib().lt_build_bvh(*args))
+    else:
+        _lib.check(_lib.lib().lt_build_bvh_device(int(device), *args))
     ms = (time.perf_counter() - t0) * 1e3
     k = int(nn.value)
     return Bvh(bmin[:k].copy(), bmax[:k].copy(), left[:k].copy(), right[:k].copy(),

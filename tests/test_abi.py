@@ -75,7 +75,7 @@ def test_host_bvh_build_matches_reference(name):
     """build_bvh (csrc/lt_bvh_build.cpp) == luxtrace.build_bvh, bit for bit."""
     from paper_2407_19977_b200 import build_bvh
     g = golden_scene(name)
-    b = build_bvh(g.triangles)
+    b = build_bvh(g.triangles, device=None)
     assert np.array_equal(b.bounds_min, g["bvh_bounds_min"])
     assert np.array_equal(b.bounds_max, g["bvh_bounds_max"])
     assert np.array_equal(b.left_child, g["bvh_left"])
@@ -90,10 +90,10 @@ def test_host_bvh_build_matches_reference(name):
 def test_host_bvh_leaf_size_and_single_triangle():
     from paper_2407_19977_b200 import TriangleBuffer, build_bvh
     g = golden_scene("sphere2k")
-    big = build_bvh(g.triangles, leaf_size=12)
+    big = build_bvh(g.triangles, leaf_size=12, device=None)
     assert int(big.triangle_count.max()) <= 12
     one = TriangleBuffer(np.array([[0.0, 0, 0]]), np.array([[1.0, 0, 0]]), np.array([[0.0, 1, 0]]),
                          *[np.array([[0.0, 0, 1]])] * 3)
-    b = build_bvh(one)
+    b = build_bvh(one, device=None)
     assert b.stats.node_count == 1 and b.stats.leaf_count == 1
     assert int(b.triangle_count[0]) == 1
