@@ -51,6 +51,10 @@ def parse_args():
     p.add_argument("--seed", type=int, default=0)
     p.add_argument("--tile", type=int, default=16)
     p.add_argument("--flags", type=int, default=0)
+    p.add_argument("--bvh-bins", type=int, default=12,
+                   help="SAH bins of the scene BVH (12 = the reference's build_bvh)")
+    p.add_argument("--bvh-leaf", type=int, default=4,
+                   help="leaf size of the scene BVH (4 = the reference's build_bvh)")
     p.add_argument("--batch-paths", type=int, default=0,
                    help="paths per wavefront batch (0 = library default)")
     p.add_argument("--no-e2e", action="store_true")
@@ -86,7 +90,7 @@ def build_workload(args):
     from paper_2407_19977_b200.procgen import scene_by_name
     from paper_2407_19977_b200 import build_bvh
     scene = scene_by_name(args.workload, width=args.width, height=args.height)
-    bvh = build_bvh(scene.triangles)
+    bvh = build_bvh(scene.triangles, leaf_size=args.bvh_leaf, bins=args.bvh_bins)
     return scene, bvh
 
 

@@ -4,13 +4,16 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -283,6 +286,26 @@ extern "C" int lt_build_bvh(const double *v0, const double *v1, const double *v2
 
 // ------------------------------------------------------------------ scene
 
+// f(i) for i in [0, n) on up to 16 host threads.
+template <class F>
+static void parallel_for(int64_t n, F f) {
+  if (n <= 0) return;
+  const int64_t hw = std::max<int64_t>(1, (int64_t)std::thread::hardware_concurrency());
+  const int64_t nt = std::min<int64_t>({n, hw, 16});
+  if (nt <= 1) {
+    for (int64_t i = 0; i < n; ++i) f(i);
+    return;
+  }
+  std::atomic<int64_t> next{0};  // dynamic: subtree sizes vary widely
+  std::vector<std::thread> th;
+  th.reserve(nt);
+  for (int64_t t = 0; t < nt; ++t)
+    th.emplace_back([&] {
+      for (int64_t i = next++; i < n; i = next++) f(i);
+    });
+  for (auto &x : th) x.join();
+}
+
 static int validate_desc(const lt_scene_desc *d) {
   if (!d) return lt_fail(LT_ERR_INVALID, "null scene description");
   if (d->n_triangles < 1) return lt_fail(LT_ERR_INVALID, "empty scene");
@@ -298,27 +321,51 @@ static int validate_desc(const lt_scene_desc *d) {
       !d->specular_ior || !d->emission_luminance || !d->emission_color)
     return lt_fail(LT_ERR_INVALID, "material arrays must be non-null");
   const int64_t n = d->n_triangles, nn = d->n_nodes;
-  for (int64_t i = 0; i < n; ++i) {
-    const int32_t m = d->material_index[i];
-    if (m < 0 || m >= d->n_materials)
-      return lt_fail(LT_ERR_INVALID, "triangle %lld: material index %d out of range [0, %d)",
-                     (long long)i, m, d->n_materials);
-    const int32_t o = d->triangle_order[i];
-    if (o < 0 || o >= n)
-      return lt_fail(LT_ERR_INVALID, "triangle_order[%lld] = %d out of range", (long long)i, o);
-  }
-  for (int64_t i = 0; i < nn; ++i) {
+  // chunked scans on host threads; the reported failure is the first index,
+  // as a sequential scan would report it
+  auto tri_bad = [&](int64_t i) {
+    const int32_t m = d->material_index[i], o = d->triangle_order[i];
+    return m < 0 || m >= d->n_materials || o < 0 || o >= n;
+  };
+  auto node_bad = [&](int64_t i) {
     if (d->triangle_count[i] > 0) {
       const int64_t f = d->first_triangle[i], c = d->triangle_count[i];
-      if (f < 0 || f + c > n)
-        return lt_fail(LT_ERR_INVALID, "node %lld: leaf range [%lld, %lld) out of bounds",
-                       (long long)i, (long long)f, (long long)(f + c));
-    } else {
-      const int32_t l = d->left_child[i], r = d->right_child[i];
-      if (l <= i || r <= i || l >= nn || r >= nn)
-        return lt_fail(LT_ERR_INVALID, "node %lld: invalid children (%d, %d)", (long long)i, l,
-                       r);
+      return f < 0 || f + c > n;
     }
+    const int32_t l = d->left_child[i], r = d->right_child[i];
+    return l <= i || r <= i || l >= nn || r >= nn;
+  };
+  auto first_bad = [&](int64_t count, auto bad) {
+    const int64_t chunks = 64;
+    std::vector<int64_t> hit(chunks, -1);
+    parallel_for(chunks, [&](int64_t c) {
+      for (int64_t i = count * c / chunks; i < count * (c + 1) / chunks; ++i)
+        if (bad(i)) {
+          hit[c] = i;
+          return;
+        }
+    });
+    for (int64_t h : hit)
+      if (h >= 0) return h;
+    return (int64_t)-1;
+  };
+  const int64_t bt = first_bad(n, tri_bad);
+  if (bt >= 0) {
+    const int32_t m = d->material_index[bt], o = d->triangle_order[bt];
+    if (m < 0 || m >= d->n_materials)
+      return lt_fail(LT_ERR_INVALID, "triangle %lld: material index %d out of range [0, %d)",
+                     (long long)bt, m, d->n_materials);
+    return lt_fail(LT_ERR_INVALID, "triangle_order[%lld] = %d out of range", (long long)bt, o);
+  }
+  const int64_t bn = first_bad(nn, node_bad);
+  if (bn >= 0) {
+    if (d->triangle_count[bn] > 0) {
+      const int64_t f = d->first_triangle[bn], c = d->triangle_count[bn];
+      return lt_fail(LT_ERR_INVALID, "node %lld: leaf range [%lld, %lld) out of bounds",
+                     (long long)bn, (long long)f, (long long)(f + c));
+    }
+    return lt_fail(LT_ERR_INVALID, "node %lld: invalid children (%d, %d)", (long long)bn,
+                   d->left_child[bn], d->right_child[bn]);
   }
   if (d->env_kind < LT_ENV_UNIFORM || d->env_kind > LT_ENV_LATLONG)
     return lt_fail(LT_ERR_INVALID, "unknown environment kind %d", d->env_kind);
@@ -438,29 +485,63 @@ static void destroy_scene(lt_scene *s) {
   delete s;
 }
 
+// Launch geometry that depends only on the device (occupancy of the trace /
+// shade kernels, the default batch from the free memory seen by the first
+// scene), computed once per device: the occupancy and memory queries cost up
+// to ~16 ms per scene otherwise.
+struct LaunchCache {
+  bool ok = false;
+  int trace_grid = 0, shade_grid = 0;
+  int64_t default_batch = 0;
+};
+
 static int configure_launches(lt_scene *s) {
   const char *env = std::getenv("LT_SMEM_NODES");
   const int want = env ? std::atoi(env) : 0;
   s->smem_nodes = (int)std::max<int64_t>(0, std::min<int64_t>(want, s->n_bfs));
-  for (int v = 0; v < 2; ++v) {
-    const bool top = v == 1;
-    const size_t smem = trace_smem_bytes(top ? s->smem_nodes : 0);
+  static std::mutex mu;
+  static std::map<int, LaunchCache> cache;
+  LaunchCache lc;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    lc = cache[s->device];
+  }
+  if (!lc.ok) {
+    const size_t smem = trace_smem_bytes(0);
     for (bool c : {false, true})
-      CK(cudaFuncSetAttribute(trace_kernel_ptr(top, c),
+      CK(cudaFuncSetAttribute(trace_kernel_ptr(false, c),
                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int blocks = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, trace_kernel_ptr(top, false),
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, trace_kernel_ptr(false, false),
                                                      kTraceThreads, smem));
-    s->trace_grid[v] = std::max(1, blocks) * s->sm_count;
+    lc.trace_grid = std::max(1, blocks) * s->sm_count;
+    size_t free_b = 0, total_b = 0;
+    lc.default_batch = kMaxBatchPaths;
+    if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
+      const int64_t by_mem = (int64_t)(free_b / 4 / 128);
+      lc.default_batch = std::max<int64_t>(int64_t(1) << 20, std::min(kMaxBatchPaths, by_mem));
+    }
+    blocks = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, shade_kernel_ptr(), kShadeThreads,
+                                                     0));
+    lc.shade_grid = std::max(1, blocks) * s->sm_count;
+    lc.ok = true;
+    std::lock_guard<std::mutex> lk(mu);
+    cache[s->device] = lc;
   }
-  size_t free_b = 0, total_b = 0;
-  if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
-    const int64_t by_mem = (int64_t)(free_b / 4 / 128);
-    s->default_batch = std::max<int64_t>(int64_t(1) << 20, std::min(kMaxBatchPaths, by_mem));
+  s->trace_grid[0] = lc.trace_grid;
+  s->shade_grid = lc.shade_grid;
+  s->default_batch = lc.default_batch;
+  if (s->smem_nodes > 0) {  // top-level staging variant (scene dependent)
+    const size_t smem = trace_smem_bytes(s->smem_nodes);
+    for (bool c : {false, true})
+      CK(cudaFuncSetAttribute(trace_kernel_ptr(true, c),
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int blocks = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, trace_kernel_ptr(true, false),
+                                                     kTraceThreads, smem));
+    s->trace_grid[1] = std::max(1, blocks) * s->sm_count;
   }
-  int blocks = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, shade_kernel_ptr(), kShadeThreads, 0));
-  s->shade_grid = std::max(1, blocks) * s->sm_count;
   // L2 residency of the traversal set (nodes + leaf-ordered triangles)
   const char *pe = std::getenv("LT_L2_PERSIST");
   int max_persist = 0, max_window = 0;
@@ -540,7 +621,7 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
   // copies (pinned sources: asynchronous DMA) overlap the host-side
   // renumbering and collapse below
   TmpBuf t_v[6], t_mat, t_order, t_end, t_bmin, t_bmax, t_left, t_right, t_first, t_count,
-      t_perm, t_new, t_wch, t_wof;
+      t_perm, t_new, t_wch, t_wof, t_env;
   const double *src[6] = {d->v0, d->v1, d->v2, d->n0, d->n1, d->n2};
   for (int k = 0; k < 6; ++k) RET(upload(t_v[k], src[k], 3 * n, st));
   RET(upload(t_mat, d->material_index, n, st));
@@ -557,7 +638,9 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
   launch_leaf_end(t_first.as<int32_t>(), t_count.as<int32_t>(), nn, t_end.as<uint8_t>(), st);
   pt.mark("uploads enqueue");
 
-  // --- internal-node renumbering: top levels BFS, the rest depth-first
+  // --- internal-node renumbering: top levels BFS, the rest depth-first.
+  // The depth-first part expands the pending subtrees on host threads; bases
+  // follow the sequential order, so the numbering is the sequential one.
   std::vector<int32_t> new_index(nn, -1), perm;
   perm.reserve(nn);
   auto is_leaf = [&](int64_t i) { return d->triangle_count[i] > 0; };
@@ -573,26 +656,37 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
         if (!is_leaf(c)) queue.push_back(c);
     }
     s->n_bfs = (int64_t)perm.size();
-    std::vector<int32_t> stack;
-    for (size_t q = head; q < queue.size(); ++q) {
-      stack.push_back(queue[q]);
+    const std::vector<int32_t> roots(queue.begin() + head, queue.end());
+    std::vector<std::vector<int32_t>> part(roots.size());
+    parallel_for((int64_t)roots.size(), [&](int64_t q) {
+      std::vector<int32_t> stack{roots[q]};
+      std::vector<int32_t> &out = part[q];
       while (!stack.empty()) {
         const int32_t x = stack.back();
         stack.pop_back();
-        new_index[x] = (int32_t)perm.size();
-        perm.push_back(x);
+        out.push_back(x);
         const int32_t l = d->left_child[x], r = d->right_child[x];
         if (!is_leaf(r)) stack.push_back(r);
         if (!is_leaf(l)) stack.push_back(l);
       }
-    }
+    });
+    std::vector<int64_t> base(roots.size() + 1, (int64_t)perm.size());
+    for (size_t q = 0; q < roots.size(); ++q) base[q + 1] = base[q] + (int64_t)part[q].size();
+    perm.resize(base[roots.size()]);
+    parallel_for((int64_t)roots.size(), [&](int64_t q) {
+      for (size_t k = 0; k < part[q].size(); ++k) {
+        perm[base[q] + k] = part[q][k];
+        new_index[part[q][k]] = (int32_t)(base[q] + k);
+      }
+    });
   }
   s->n_internal = (int64_t)perm.size();
   pt.mark("binary renumbering");
   // --- 4-wide collapse of the same tree (render / closest-hit layout): a
   // wide node starts from its binary node's two children and repeatedly
   // replaces the internal child with the largest surface area by its two
-  // children, up to four; wide nodes are numbered depth-first.
+  // children, up to four.  Numbering: the top wide nodes breadth first, then
+  // each pending subtree depth first (collapsed on host threads).
   std::vector<int32_t> wide_children, wide_of(nn, -1);
   if (!is_leaf(0)) {
     auto area = [&](int32_t x) {
@@ -600,11 +694,8 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
       const double dx = hi[0] - lo[0], dy = hi[1] - lo[1], dz = hi[2] - lo[2];
       return dx * dy + dy * dz + dz * dx;
     };
-    std::vector<int32_t> stack{0};
-    while (!stack.empty()) {
-      const int32_t r = stack.back();
-      stack.pop_back();
-      wide_of[r] = (int32_t)(wide_children.size() / 4);
+    // collapse wide node r: its (up to) 4 children, pushing the internal ones
+    auto collapse = [&](int32_t r, std::vector<int32_t> &kids, std::vector<int32_t> &stack) {
       int32_t ch[4] = {d->left_child[r], d->right_child[r], -1, -1};
       int nc = 2;
       while (nc < 4) {
@@ -622,10 +713,42 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
         ch[pick + 1] = d->right_child[x];
         ++nc;
       }
-      for (int i = 0; i < 4; ++i) wide_children.push_back(i < nc ? ch[i] : -1);
+      for (int i = 0; i < 4; ++i) kids.push_back(i < nc ? ch[i] : -1);
       for (int i = nc - 1; i >= 0; --i)
         if (!is_leaf(ch[i])) stack.push_back(ch[i]);
+    };
+    // top of the tree breadth first (the hot wide nodes contiguous) until 256
+    // subtrees are pending; those are collapsed depth first in parallel
+    std::vector<int32_t> queue{0}, top;  // top: binary roots of the top wide nodes
+    size_t qh = 0;
+    while (qh < queue.size() && queue.size() - qh < 256) {
+      const int32_t r = queue[qh++];
+      top.push_back(r);
+      std::vector<int32_t> kids_in;
+      collapse(r, wide_children, kids_in);
+      queue.insert(queue.end(), kids_in.rbegin(), kids_in.rend());
     }
+    const std::vector<int32_t> pending(queue.begin() + qh, queue.end());
+    std::vector<std::vector<int32_t>> roots_of(pending.size()), kids_of(pending.size());
+    parallel_for((int64_t)pending.size(), [&](int64_t q) {
+      std::vector<int32_t> st{pending[q]};
+      while (!st.empty()) {
+        const int32_t r = st.back();
+        st.pop_back();
+        roots_of[q].push_back(r);
+        collapse(r, kids_of[q], st);
+      }
+    });
+    for (size_t k = 0; k < top.size(); ++k) wide_of[top[k]] = (int32_t)k;
+    std::vector<int64_t> base(pending.size() + 1, (int64_t)top.size());
+    for (size_t q = 0; q < pending.size(); ++q)
+      base[q + 1] = base[q] + (int64_t)roots_of[q].size();
+    wide_children.resize(4 * base[pending.size()]);
+    parallel_for((int64_t)pending.size(), [&](int64_t q) {
+      for (size_t k = 0; k < roots_of[q].size(); ++k)
+        wide_of[roots_of[q][k]] = (int32_t)(base[q] + k);
+      std::copy(kids_of[q].begin(), kids_of[q].end(), wide_children.begin() + 4 * base[q]);
+    });
   }
   s->n_wide = (int64_t)(wide_children.size() / 4);
   pt.mark("4-wide collapse");
@@ -673,11 +796,10 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
     // environment
     if (d->env_kind == LT_ENV_LATLONG) {
       const int64_t np = (int64_t)d->env_width * d->env_height;
-      std::vector<float4> tex(np);
-      for (int64_t i = 0; i < np; ++i)
-        tex[i] = make_float4(d->env_texels[3 * i], d->env_texels[3 * i + 1],
-                             d->env_texels[3 * i + 2], 0.f);
-      if ((rc = upload(s->env, tex.data(), tex.size(), st))) break;
+      // float3 texels as given; widened to float4 records on the device
+      if ((rc = upload(t_env, d->env_texels, 3 * (size_t)np, st))) break;
+      if ((rc = s->env.ensure((size_t)np * 16))) break;
+      launch_expand_rgb(t_env.as<float>(), np, s->env.as<float4>(), st);
     }
     pt.mark("materials + env");
     e = cudaStreamSynchronize(st);
@@ -879,20 +1001,28 @@ static int pixel_set(lt_scene *s, const lt_render_params *p, const int32_t **lis
   const int64_t tile_sz = sharded ? p->tile_size : tile_order;
   const int64_t key[5] = {p->width, p->height, tile_sz, rank, n_ranks};
   if (!std::equal(key, key + 5, s->pix_key)) {
+    // per-tile start offsets on the host (<= W*H/T^2 tiles), the per-pixel
+    // scatter on the device (no 2 M-entry host list, no synchronous copy)
     const int64_t W = p->width, H = p->height, T = tile_sz;
     const int64_t ntx = (W + T - 1) / T, nty = (H + T - 1) / T;
-    std::vector<int32_t> pix;
+    std::vector<int32_t> tile_start;
+    tile_start.reserve((size_t)(ntx * nty / n_ranks + 2));
+    int64_t total = 0;
     for (int64_t tile = rank; tile < ntx * nty; tile += n_ranks) {
       const int64_t ty = tile / ntx, tx = tile - ty * ntx;
-      for (int64_t y = ty * T; y < std::min(H, (ty + 1) * T); ++y)
-        for (int64_t x = tx * T; x < std::min(W, (tx + 1) * T); ++x)
-          pix.push_back((int32_t)(y * W + x));
+      tile_start.push_back((int32_t)total);
+      total += (std::min(W, (tx + 1) * T) - tx * T) * (std::min(H, (ty + 1) * T) - ty * T);
     }
-    RET(s->pix_list.ensure(std::max<size_t>(16, pix.size() * 4)));
-    if (!pix.empty())
-      CK(cudaMemcpy(s->pix_list.p, pix.data(), pix.size() * 4, cudaMemcpyHostToDevice));
+    RET(s->pix_list.ensure(std::max<size_t>(16, (size_t)total * 4)));
+    TmpBuf t_start;
+    RET(upload(t_start, tile_start.data(), tile_start.size(), s->stream));
+    launch_pixel_list((int32_t)W, (int32_t)H, (int32_t)T, (int32_t)rank, (int32_t)n_ranks,
+                      t_start.as<int32_t>(), s->pix_list.as<int32_t>(), s->stream);
+    CK(cudaGetLastError());
+    // the render streams fork from the caller's stream: order after the scatter
+    CK(cudaStreamSynchronize(s->stream));
     std::copy(key, key + 5, s->pix_key);
-    s->pix_count = (int64_t)pix.size();
+    s->pix_count = total;
   }
   *list = s->pix_list.as<int32_t>();
   *n = s->pix_count;

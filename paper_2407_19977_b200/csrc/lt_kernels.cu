@@ -557,6 +557,40 @@ __global__ void __launch_bounds__(kShadeThreads, LT_SHADE_MIN_BLOCKS)
   }
 }
 
+// ------------------------------------------------------------------ env map
+
+__global__ void k_expand_rgb(const float *__restrict__ rgb, int64_t n, float4 *__restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = make_float4(rgb[3 * i], rgb[3 * i + 1], rgb[3 * i + 2], 0.f);
+}
+
+void launch_expand_rgb(const float *rgb, int64_t n, float4 *out, cudaStream_t st) {
+  if (n > 0) k_expand_rgb<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(rgb, n, out);
+}
+
+// ------------------------------------------------------------------ pixel order
+
+__global__ void k_pixel_list(int32_t W, int32_t H, int32_t T, int32_t rank, int32_t n_ranks,
+                             const int32_t *__restrict__ tile_start, int32_t *__restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)W * H) return;
+  const int32_t y = (int32_t)(i / W), x = (int32_t)(i - (int64_t)y * W);
+  const int32_t ntx = (W + T - 1) / T;
+  const int32_t tx = x / T, ty = y / T;
+  const int32_t tile = ty * ntx + tx;
+  if (tile % n_ranks != rank) return;
+  const int32_t w = min(W, (tx + 1) * T) - tx * T;
+  out[tile_start[tile / n_ranks] + (y - ty * T) * w + (x - tx * T)] = (int32_t)i;
+}
+
+void launch_pixel_list(int32_t width, int32_t height, int32_t tile, int32_t rank, int32_t n_ranks,
+                       const int32_t *tile_start, int32_t *out, cudaStream_t st) {
+  const int64_t n = (int64_t)width * height;
+  if (n <= 0) return;
+  k_pixel_list<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(width, height, tile, rank, n_ranks,
+                                                            tile_start, out);
+}
+
 // ------------------------------------------------------------------ accumulate
 
 // Per-pixel sum of the batch's finite samples in sample order, plus valid /

@@ -96,6 +96,12 @@ cudaError_t launch_shade(const SceneView &sc, const ShadeArgs &sa, const PathArr
                          const float4 *q_o, const float4 *q_d, const float4 *hits,
                          const int32_t *count_in, float4 *n_o, float4 *n_d, int32_t *count_out,
                          cudaStream_t st);
+// tile-ordered local pixel list: tiles k = rank, rank + n_ranks, ... of the
+// T x T tiling (row-major tiles, row-major pixels inside a tile)
+void launch_pixel_list(int32_t width, int32_t height, int32_t tile, int32_t rank, int32_t n_ranks,
+                       const int32_t *tile_start, int32_t *out, cudaStream_t st);
+// rgb float3 texels -> float4 records (environment map upload)
+void launch_expand_rgb(const float *rgb, int64_t n, float4 *out, cudaStream_t st);
 void launch_accumulate(const AccumArgs &aa, const float4 *L, float *accum, uint32_t *valid,
                        uint32_t *invalid, cudaStream_t st);
 void launch_pack_rays_f32(const float *o, const float *d, int64_t n, float t_min, float t_max,
