@@ -158,6 +158,19 @@ def test_render_image_matches_reference(name):
     assert np.array_equal(res.invalid_samples, g["render_invalid"])
 
 
+@pytest.mark.parametrize("name", ["glossy", "sphere20k"])
+def test_render_without_bvh_builds_the_reference_tree(name):
+    """render_progressive(scene, settings) with no BVH (the reference's
+    default call) builds the tree on the GPU; it is the reference's tree, so
+    the image equals the one rendered with the reference-built BVH bit for
+    bit."""
+    g = golden_scene(name)
+    with_ref = lb().render_progressive(g.scene, g.settings, bvh=g.bvh)
+    built = lb().render_progressive(g.scene, g.settings)
+    assert np.array_equal(built.image, with_ref.image)
+    assert np.array_equal(built.invalid_samples, with_ref.invalid_samples)
+
+
 @pytest.mark.parametrize("name", ["floor", "glossy", "sphere2k", "cornell_c2"])
 def test_trace_radiance_matches_reference(name):
     g = golden_scene(name)
