@@ -554,7 +554,7 @@ static int configure_launches(lt_scene *s) {
   if (s->use_window) {
     // geo = [wide nodes | triangles | shading]; trace launches keep
     // [nodes, triangles] persisting, shade launches [triangles, shading]
-    const size_t tri_bytes = 48 * (size_t)s->n_tris;
+    const size_t tri_bytes = 16 * LT_TRI_F4 * (size_t)s->n_tris;
     const size_t trace_bytes = s->nodes_bytes + tri_bytes;
     const size_t shade_bytes = s->geo_bytes - s->nodes_bytes;
     const char *se = std::getenv("LT_L2_SHADE");
@@ -758,7 +758,7 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
     s->nodes_bytes = (size_t)std::max<int64_t>(1, s->n_wide) * 16 * LT_NODE_F4;
     // shading records start on a 128 B boundary so each 64 B record is
     // half of one cache line
-    s->shade_off = (s->nodes_bytes + 48 * (size_t)n + 127) / 128 * 128;
+    s->shade_off = (s->nodes_bytes + 16 * LT_TRI_F4 * (size_t)n + 127) / 128 * 128;
     s->geo_bytes = s->shade_off + 64 * (size_t)n;
     if ((rc = s->geo.ensure(s->geo_bytes))) break;
     if ((rc = s->nodes2.ensure((size_t)std::max<int64_t>(1, s->n_internal) * 64))) break;

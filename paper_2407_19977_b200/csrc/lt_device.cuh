@@ -1,13 +1,15 @@
 // lt_device.cuh -- device data layout and scalar device functions.
 //
 // HBM layout (all 16-byte aligned):
-//   wnodes : 8 x float4 (128 B, one cache line) per node of the host BVH
-//            collapsed to 4-wide (each wide node absorbs the largest-area
-//            internal children of its binary node until it has 4 children):
-//              f4[0..5] = lo.x[4], hi.x[4], lo.y[4], hi.y[4], lo.z[4], hi.z[4]
-//              f4[6]    = 4 child links (>= 0 wide node, < 0 leaf = ~first,
-//                         INT_MIN empty slot); f4[7] unused
-//            Boxes are the reference's float64 boxes rounded outward.
+//   wnodes : LT_NODE_F4 x float4 per node of the host BVH collapsed to
+//            4-wide (each wide node absorbs the largest-area internal
+//            children of its binary node until it has 4 children); default
+//            (LT_NODE_DUP, 224 B): per axis a = x, y, z the float4s
+//            [4a .. 4a+3] = lo[4], hi[4], hi[4], lo[4] (the (near, far) pair
+//            for a positive / negative inverse direction), f4[12] = 4 child
+//            links (>= 0 wide node, < 0 leaf = ~first, INT_MIN empty slot),
+//            f4[13] unused.  Boxes are the reference's float64 boxes rounded
+//            outward; empty slots carry inverted infinite boxes.
 //   nodes  : 4 x float4 per INTERNAL node of the host BVH; a node holds the
 //            fp32 boxes of both children (rounded outward) and their links.
 //              n0 = (L.lo.x, L.hi.x, L.lo.y, L.hi.y)
@@ -17,7 +19,7 @@
 //                                            link < 0: leaf, first = ~link
 //            Internal nodes are renumbered: the top levels in BFS order
 //            (staged in shared memory), the rest depth-first.
-//   tris   : 3 x float4 per triangle in LEAF order (reference triangle_order)
+//   tris   : LT_TRI_F4 (3) x float4 per triangle in LEAF order (triangle_order)
 //              (v0.xyz, original index), (e1.xyz, last-in-leaf flag),
 //              (e2.xyz, 0); e1/e2 are rounded from the float64 differences.
 //   shade  : 4 x float4 (64 B, one aligned half line) per triangle in leaf
@@ -41,6 +43,13 @@
 // (near, far) pair that one 256-bit load fetches (224 B; the default:
 // +4.5 % on C4, profiles/r01_trace_variants.txt; -DLT_NODE_COMPACT selects
 // the 128 B record).
+// Leaf-ordered triangle record in float4 units: (v0, orig), (e1, leaf-end),
+// (e2, 0) = 48 B; LT_TRI_W256 pads it to 64 B so (v0, e1) is one 256-bit load.
+#ifdef LT_TRI_W256
+#define LT_TRI_F4 4
+#else
+#define LT_TRI_F4 3
+#endif
 #if !defined(LT_NODE_COMPACT) && !defined(LT_NODE_DUP)
 #define LT_NODE_DUP 1
 #endif

@@ -118,11 +118,12 @@ __global__ void k_flatten_tris(const double *__restrict__ v0, const double *__re
   if (k >= n) return;
   const int64_t ti = order[k];
   const double *a = v0 + 3 * ti, *b = v1 + 3 * ti, *c = v2 + 3 * ti;
-  tris[3 * k + 0] = make_float4((float)a[0], (float)a[1], (float)a[2], __int_as_float((int)ti));
-  tris[3 * k + 1] = make_float4((float)(b[0] - a[0]), (float)(b[1] - a[1]), (float)(b[2] - a[2]),
+  float4 *tr = tris + LT_TRI_F4 * k;
+  tr[0] = make_float4((float)a[0], (float)a[1], (float)a[2], __int_as_float((int)ti));
+  tr[1] = make_float4((float)(b[0] - a[0]), (float)(b[1] - a[1]), (float)(b[2] - a[2]),
                                 __int_as_float(leaf_end[k] ? 1 : 0));
-  tris[3 * k + 2] =
-      make_float4((float)(c[0] - a[0]), (float)(c[1] - a[1]), (float)(c[2] - a[2]), 0.f);
+  tr[2] = make_float4((float)(c[0] - a[0]), (float)(c[1] - a[1]), (float)(c[2] - a[2]), 0.f);
+  if (LT_TRI_F4 > 3) tr[3] = make_float4(0.f, 0.f, 0.f, 0.f);
   // geometric normal as _hit_frame computes it (geometry.py:217-224), float64
   const double e1x = b[0] - a[0], e1y = b[1] - a[1], e1z = b[2] - a[2];
   const double e2x = c[0] - a[0], e2y = c[1] - a[1], e2z = c[2] - a[2];
@@ -637,7 +638,7 @@ __global__ void k_unpack_hits(SceneView sc, const float4 *__restrict__ hits, int
   if (i >= n) return;
   const float4 h = hits[i];
   const int32_t k = __float_as_int(h.w);
-  const int32_t orig = k >= 0 ? __float_as_int(__ldg(&sc.tris[3 * (int64_t)k]).w) : -1;
+  const int32_t orig = k >= 0 ? __float_as_int(__ldg(&sc.tris[LT_TRI_F4 * (int64_t)k]).w) : -1;
   const float t = k >= 0 ? h.x : __int_as_float(0x7f800000);
   if (idx32) idx32[i] = orig;
   if (t32) t32[i] = t;

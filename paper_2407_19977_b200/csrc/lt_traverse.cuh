@@ -139,9 +139,17 @@ template <bool COUNT>
 __device__ __forceinline__ void leaf_test(const SceneView &sc, int64_t k, f3 o, f3 d, float t_min,
                                           HitRec &best, int32_t &best_orig, int &tests) {
   while (true) {
-    const float4 t0 = __ldg(&sc.tris[3 * k]);
-    const float4 t1 = __ldg(&sc.tris[3 * k + 1]);
-    const float4 t2 = __ldg(&sc.tris[3 * k + 2]);
+#ifdef LT_TRI_W256
+    float4 t0, t1;
+    asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=f"(t0.x), "=f"(t0.y), "=f"(t0.z), "=f"(t0.w), "=f"(t1.x), "=f"(t1.y), "=f"(t1.z),
+          "=f"(t1.w)
+        : "l"(sc.tris + LT_TRI_F4 * k));
+#else
+    const float4 t0 = __ldg(&sc.tris[LT_TRI_F4 * k]);
+    const float4 t1 = __ldg(&sc.tris[LT_TRI_F4 * k + 1]);
+#endif
+    const float4 t2 = __ldg(&sc.tris[LT_TRI_F4 * k + 2]);
     if (COUNT) ++tests;
     mt_test(o, d, t_min, t0, t1, t2, (int32_t)k, best, best_orig);
     if (__float_as_int(t1.w) != 0) break;
