@@ -18,6 +18,8 @@ from .integrator import (RenderResult, RenderSettings, environment_radiance,
                          generate_camera_ray, render_image, render_pass, render_progressive,
                          trace_radiance, trace_radiance_batch)
 from .procgen import bumpy_sphere, cornell_box, pushbutton, sphere_on_plane, synthetic_hdr
+from .ingest import (MaterialMap, RenderConfig, flatten_scene, generate_smooth_normals, load_gltf,
+                     load_render_config, load_scene, save_glb)
 
 __version__ = "0.1.0"
 
@@ -33,4 +35,6 @@ __all__ = [
     "render_image", "render_pass", "render_progressive", "trace_radiance",
     "trace_radiance_batch",
     "bumpy_sphere", "cornell_box", "pushbutton", "sphere_on_plane", "synthetic_hdr",
+    "MaterialMap", "RenderConfig", "flatten_scene", "generate_smooth_normals", "load_gltf",
+    "load_render_config", "load_scene", "save_glb",
 ]
