@@ -382,6 +382,29 @@ __global__ void __launch_bounds__(kTraceThreads)
 
 // ------------------------------------------------------------------ shade
 
+// Direction bin of a continuation ray for the block-level grouping:
+// LT_DIR_BINS = 8: octant; 24: octant x dominant axis; 64: 4 levels per
+// component (x-major).
+#ifndef LT_DIR_BINS
+#define LT_DIR_BINS 8
+#endif
+__device__ __forceinline__ int dir_bin(const float4 &d) {
+#if LT_DIR_BINS == 64
+  const int qx = min(3, (int)((d.x + 1.f) * 2.f)), qy = min(3, (int)((d.y + 1.f) * 2.f));
+  const int qz = min(3, (int)((d.z + 1.f) * 2.f));
+  return (max(qx, 0) << 4) | (max(qy, 0) << 2) | max(qz, 0);
+#else
+  const int oct = (d.x < 0.f ? 1 : 0) | (d.y < 0.f ? 2 : 0) | (d.z < 0.f ? 4 : 0);
+#if LT_DIR_BINS == 24
+  const float ax = fabsf(d.x), ay = fabsf(d.y), az = fabsf(d.z);
+  const int dom = (ax >= ay && ax >= az) ? 0 : (ay >= az ? 1 : 2);
+  return oct * 3 + dom;
+#else
+  return oct;
+#endif
+#endif
+}
+
 // One bounce of _trace (integrator.py:160-226) for every queued path:
 // miss -> environment; hit -> emission; final segment stops; otherwise hit
 // frame, 3 draws, BSDF sample, throughput, Russian roulette (4th draw), and
@@ -505,26 +528,30 @@ __global__ void __launch_bounds__(kShadeThreads, LT_SHADE_MIN_BLOCKS)
       if (primary && !wrote_l) __stcs(&pa.L[p], L);
     }
     if (sa.octant_sort) {
-      // block-aggregated append grouped by direction octant: the block's
-      // continuation rays (nearby origins) land in the next queue as runs of
-      // equal octant, so a trace warp fetches rays that descend the tree
-      // alike (higher SIMT efficiency for incoherent bounces)
-      __shared__ int s_cnt[8], s_base[8];
-      if (threadIdx.x < 8) s_cnt[threadIdx.x] = 0;
+      // block-aggregated append grouped by direction: one contiguous range
+      // of the next queue per block, laid out bin by bin (counting sort), so
+      // a trace warp fetches rays with nearby origins and similar
+      // directions (higher SIMT efficiency for incoherent bounces)
+      __shared__ int s_cnt[LT_DIR_BINS], s_off[LT_DIR_BINS], s_base;
+      for (int b = threadIdx.x; b < LT_DIR_BINS; b += blockDim.x) s_cnt[b] = 0;
       __syncthreads();
-      int oct = 0, rank = 0;
+      int bin = 0, rank = 0;
       if (emit) {
-        oct = (out_d.x < 0.f ? 1 : 0) | (out_d.y < 0.f ? 2 : 0) | (out_d.z < 0.f ? 4 : 0);
-        rank = atomicAdd(&s_cnt[oct], 1);
+        bin = dir_bin(out_d);
+        rank = atomicAdd(&s_cnt[bin], 1);
       }
       __syncthreads();
-      if (threadIdx.x < 8) {
-        const int c = s_cnt[threadIdx.x];
-        s_base[threadIdx.x] = c ? atomicAdd(count_out, c) : 0;
+      if (threadIdx.x == 0) {
+        int run = 0;
+        for (int b = 0; b < LT_DIR_BINS; ++b) {
+          s_off[b] = run;
+          run += s_cnt[b];
+        }
+        s_base = run ? atomicAdd(count_out, run) : 0;
       }
       __syncthreads();
       if (emit) {
-        const int slot = s_base[oct] + rank;
+        const int slot = s_base + s_off[bin] + rank;
         __stcs(&n_o[slot], out_o);
         __stcs(&n_d[slot], out_d);
       }
