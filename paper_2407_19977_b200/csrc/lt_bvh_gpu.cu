@@ -35,10 +35,11 @@
 // sequential scan met first in the reference and the ordered-integer minimum
 // here; the values compare equal.
 //
-// Structure: nodes larger than kSmall are processed level by level by the
-// whole GPU (block-privatised bins -> one thread per node SAH -> scan-based
-// partition); every smaller subtree is built depth first by one CTA in
-// shared memory.
+// Structure: nodes larger than kSmall (512) are processed level by level by
+// the whole GPU (block-privatised bins -> one thread per node SAH ->
+// scan-based partition); every smaller subtree is built depth first by one
+// 64-thread CTA in shared memory (small CTAs: many subtrees in flight hide
+// the per-node barrier / serial-SAH latency; profiles/r01_bvh_variants.log).
 #include <cub/cub.cuh>
 #include <cuda_runtime.h>
 
@@ -59,8 +60,15 @@ constexpr double kTraversalCost = 1.0;   // bvh.py:24
 constexpr double kIntersectCost = 1.0;   // bvh.py:25
 constexpr int kDepthCap = 60;            // bvh.py:26
 constexpr int kMaxBins = 32;
-constexpr int kSmall = 4096;             // subtrees up to this size: one CTA
+#ifndef LT_BVH_SMALL
+#define LT_BVH_SMALL 512
+#endif
+#ifndef LT_BVH_SMALL_THREADS
+#define LT_BVH_SMALL_THREADS 64
+#endif
+constexpr int kSmall = LT_BVH_SMALL;      // subtrees up to this size: one CTA each
 constexpr int kThreads = 256;
+constexpr int kSmallThreads = LT_BVH_SMALL_THREADS;  // CTA width of the subtree kernel
 constexpr int kChunk = 4096;             // positions per binning CTA (large nodes)
 constexpr unsigned long long kMsb = 0x8000000000000000ull;
 
@@ -589,7 +597,7 @@ struct SmallSmem {
   Job cur, kid[2];
   int sp, done, state, axis, plane, L, total;
   double cmin, scale;
-  int warp_sum[kThreads / 32];
+  int warp_sum[kSmallThreads / 32];
   int32_t ord[kSmall];
   int32_t pre[kSmall + 1];
   int32_t beta[kSmall];
@@ -597,7 +605,7 @@ struct SmallSmem {
   uint8_t flag[kSmall];
 };
 
-__global__ void __launch_bounds__(kThreads) k_small(const Job *__restrict__ jobs,
+__global__ void __launch_bounds__(kSmallThreads) k_small(const Job *__restrict__ jobs,
                                                     int32_t *__restrict__ order,
                                                     const double *__restrict__ tb, int leaf_size,
                                                     int n_bins, Tree t, Counters *ctr) {
@@ -631,15 +639,15 @@ __global__ void __launch_bounds__(kThreads) k_small(const Job *__restrict__ jobs
     if (S.state == ST_LEAF) continue;  // (every thread reads S.state after the barrier)
     const Job J = S.cur;
     if (S.state == ST_BIN) {
-      for (int q = tid; q < n_bins * 12; q += kThreads) {
+      for (int q = tid; q < n_bins * 12; q += kSmallThreads) {
         const int r = q % 12;
         S.bins[q] = (r < 3 || (r >= 6 && r < 9)) ? ~0ull : 0ull;
       }
-      for (int b = tid; b < n_bins; b += kThreads) S.cnt[b] = 0;
+      for (int b = tid; b < n_bins; b += kSmallThreads) S.cnt[b] = 0;
       __syncthreads();
       const int axis = S.axis;
       const double cmin = S.cmin, scale = S.scale;
-      for (int k = tid; k < J.c; k += kThreads) {
+      for (int k = tid; k < J.c; k += kSmallThreads) {
         const int32_t ti = order[J.f + k];
         S.ord[k] = ti;
         const double *tt = tb + 9 * (int64_t)ti;
@@ -663,7 +671,7 @@ __global__ void __launch_bounds__(kThreads) k_small(const Job *__restrict__ jobs
       if (S.state == ST_LEAF) continue;
       // left flags and their exclusive prefix (contiguous segment per thread)
       const int plane = S.plane;
-      const int per = (J.c + kThreads - 1) / kThreads;
+      const int per = (J.c + kSmallThreads - 1) / kSmallThreads;
       const int k0 = min(J.c, tid * per), k1 = min(J.c, k0 + per);
       int cnt = 0;
       for (int k = k0; k < k1; ++k) {
@@ -681,7 +689,7 @@ __global__ void __launch_bounds__(kThreads) k_small(const Job *__restrict__ jobs
       __syncthreads();
       if (tid == 0) {
         int run = 0;
-        for (int w = 0; w < kThreads / 32; ++w) {
+        for (int w = 0; w < kSmallThreads / 32; ++w) {
           const int v = S.warp_sum[w];
           S.warp_sum[w] = run;
           run += v;
@@ -700,7 +708,7 @@ __global__ void __launch_bounds__(kThreads) k_small(const Job *__restrict__ jobs
       }
       __syncthreads();
       const int L = S.L, c = J.c;
-      for (int k = tid; k < c; k += kThreads) {
+      for (int k = tid; k < c; k += kSmallThreads) {
         if (k >= L && S.flag[k]) {
           const int jj = 1 + (S.pre[c] - S.pre[k + 1]);
           S.beta[jj - 1] = c - k;
@@ -710,7 +718,7 @@ __global__ void __launch_bounds__(kThreads) k_small(const Job *__restrict__ jobs
       __syncthreads();
       const int X = L - S.pre[L];
       const int last = X > 0 ? S.beta[X - 1] : 0;
-      for (int k = tid; k < c; k += kThreads)
+      for (int k = tid; k < c; k += kSmallThreads)
         scatter_one(k, S.flag[k], S.ord[k], c, L, last, S.pre[k], S.beta, S.belem,
                     order + J.f);
       __syncthreads();
@@ -939,7 +947,7 @@ static int build_on_device(const double *v0, const double *v1, const double *v2,
   if (c.n_small > 0) {
     const size_t smem = sizeof(SmallSmem);
     GCK(cudaFuncSetAttribute(k_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_small<<<c.n_small, kThreads, smem, st>>>(d_small.as<Job>(), d_order[cur].as<int32_t>(),
+    k_small<<<c.n_small, kSmallThreads, smem, st>>>(d_small.as<Job>(), d_order[cur].as<int32_t>(),
                                                d_tb.as<double>(), leaf_size, n_bins, t,
                                                d_ctr.as<Counters>());
     GCK(cudaGetLastError());
