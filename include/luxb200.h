@@ -38,7 +38,7 @@ extern "C" {
 
 /* lt_render_params.flags */
 #define LT_FLAG_SORT_MATERIALS 1u   /* shade hits in material-sorted order */
-#define LT_FLAG_NO_SMEM_TOP 2u      /* disable shared-memory staging of top BVH nodes */
+#define LT_FLAG_NO_SMEM_TOP 2u      /* reserved (top-node staging was removed); no effect */
 #define LT_FLAG_PROFILE 4u          /* time every trace launch with CUDA events */
 #define LT_FLAG_COUNT 8u            /* count slab / triangle tests in the trace kernel */
 
@@ -76,7 +76,7 @@ typedef struct lt_scene_desc {
 
 typedef struct lt_scene_info {
   int32_t device;
-  int64_t n_triangles, n_nodes, n_internal, n_smem_nodes;
+  int64_t n_triangles, n_nodes, n_internal, n_smem_nodes;  /* n_smem_nodes: always 0 */
   int64_t device_bytes;         /* resident scene bytes in HBM */
   int32_t sm_count;
   int64_t n_wide;               /* 4-wide nodes of the render layout */

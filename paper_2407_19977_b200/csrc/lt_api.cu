@@ -496,9 +496,7 @@ struct LaunchCache {
 };
 
 static int configure_launches(lt_scene *s) {
-  const char *env = std::getenv("LT_SMEM_NODES");
-  const int want = env ? std::atoi(env) : 0;
-  s->smem_nodes = (int)std::max<int64_t>(0, std::min<int64_t>(want, s->n_bfs));
+  s->smem_nodes = 0;  // (top-level shared-memory staging measured slower; removed)
   static std::mutex mu;
   static std::map<int, LaunchCache> cache;
   LaunchCache lc;
@@ -507,12 +505,12 @@ static int configure_launches(lt_scene *s) {
     lc = cache[s->device];
   }
   if (!lc.ok) {
-    const size_t smem = trace_smem_bytes(0);
+    const size_t smem = trace_smem_bytes();
     for (bool c : {false, true})
-      CK(cudaFuncSetAttribute(trace_kernel_ptr(false, c),
-                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      CK(cudaFuncSetAttribute(trace_kernel_ptr(c), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)smem));
     int blocks = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, trace_kernel_ptr(false, false),
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, trace_kernel_ptr(false),
                                                      kTraceThreads, smem));
     lc.trace_grid = std::max(1, blocks) * s->sm_count;
     size_t free_b = 0, total_b = 0;
@@ -532,16 +530,6 @@ static int configure_launches(lt_scene *s) {
   s->trace_grid[0] = lc.trace_grid;
   s->shade_grid = lc.shade_grid;
   s->default_batch = lc.default_batch;
-  if (s->smem_nodes > 0) {  // top-level staging variant (scene dependent)
-    const size_t smem = trace_smem_bytes(s->smem_nodes);
-    for (bool c : {false, true})
-      CK(cudaFuncSetAttribute(trace_kernel_ptr(true, c),
-                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int blocks = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, trace_kernel_ptr(true, false),
-                                                     kTraceThreads, smem));
-    s->trace_grid[1] = std::max(1, blocks) * s->sm_count;
-  }
   // L2 residency of the traversal set (nodes + leaf-ordered triangles)
   const char *pe = std::getenv("LT_L2_PERSIST");
   int max_persist = 0, max_window = 0;
@@ -936,9 +924,7 @@ static int record_event(lt_scene *s, cudaStream_t st) {
 // the primary rays and counters[0] their number (explicit rays).
 static int run_bounces(lt_scene *s, Lane &lane, int32_t max_depth, int32_t rr_start, float t_min,
                        uint32_t flags, cudaStream_t st, const RaygenArgs *primary = nullptr) {
-  const bool smem = !(flags & LT_FLAG_NO_SMEM_TOP) && s->smem_nodes > 0;
   SceneView sc = s->view;
-  sc.n_top = smem ? s->smem_nodes : 0;
   Lane *ws = &lane;
   int32_t *ctr = ws->counters.as<int32_t>();
   int32_t *fetch = ctr + max_depth + 1;
@@ -949,7 +935,7 @@ static int run_bounces(lt_scene *s, Lane &lane, int32_t max_depth, int32_t rr_st
     if (flags & LT_FLAG_PROFILE) RET(record_event(s, st));
     // (in-kernel ray generation for trace measured slower than reading the
     // 32 B ray record: the float64 camera math serializes the refill path)
-    CK(launch_trace(sc, smem, (flags & LT_FLAG_COUNT) != 0, s->trace_grid[smem ? 1 : 0],
+    CK(launch_trace(sc, (flags & LT_FLAG_COUNT) != 0, s->trace_grid[0],
                     s->use_window ? &s->window : nullptr, ws->q_o[cur].as<float4>(),
                     ws->q_d[cur].as<float4>(), ctr + depth, fetch + depth,
                     ws->hits.as<float4>(), s->ray_ctr.as<unsigned long long>(), st));

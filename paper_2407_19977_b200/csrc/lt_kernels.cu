@@ -223,18 +223,15 @@ __global__ void k_gather_explicit(PathArrays pa, int64_t n, double *__restrict__
 //  * traversal stack: the first kShortStack entries of every lane live in
 //    shared memory, laid out [depth][thread] (conflict-free), deeper ones in
 //    local memory;
-//  * optionally the top BFS nodes are staged in shared memory;
 //  * queue reads / hit writes are streaming (__ldcs / __stcs) so they do not
 //    evict the scene from L2.
 // ray_ctr[0] += queue length; with COUNT also ray_ctr[1] += slab tests and
 // ray_ctr[2] += triangle tests.
-template <bool USE_SMEM, bool COUNT>
+template <bool COUNT>
 __global__ void __launch_bounds__(kTraceThreads, LT_TRACE_MIN_BLOCKS)
     k_trace(SceneView sc, const float4 *__restrict__ q_o, const float4 *__restrict__ q_d,
             const int32_t *__restrict__ count, int32_t *__restrict__ fetch,
             float4 *__restrict__ hits, unsigned long long *__restrict__ ray_ctr) {
-  // (USE_SMEM: the top-level staging variant measured slower than L1
-  // caching -- profiles/r01_sweep -- and is kept only as a launch option.)
   extern __shared__ float4 s_mem[];
   int32_t *s_node = reinterpret_cast<int32_t *>(s_mem);
   float *s_t = reinterpret_cast<float *>(s_node + kShortStack * kTraceThreads);
@@ -803,9 +800,8 @@ void launch_read_probe(const float4 *src, int64_t n4, int passes, float *sink, i
 
 // ------------------------------------------------------------------ launchers
 
-const void *trace_kernel_ptr(bool smem, bool count) {
-  if (count) return smem ? (const void *)k_trace<true, true> : (const void *)k_trace<false, true>;
-  return smem ? (const void *)k_trace<true, false> : (const void *)k_trace<false, false>;
+const void *trace_kernel_ptr(bool count) {
+  return count ? (const void *)k_trace<true> : (const void *)k_trace<false>;
 }
 const void *shade_kernel_ptr() { return (const void *)k_shade; }
 
@@ -860,18 +856,16 @@ void launch_gather_explicit(const PathArrays &pa, int64_t n, double *rgb, uint64
   k_gather_explicit<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(pa, n, rgb, state_out);
 }
 
-size_t trace_smem_bytes(int n_top) {
-  return (size_t)n_top * 64 + (size_t)kShortStack * kTraceThreads * 8;
-}
+size_t trace_smem_bytes() { return (size_t)kShortStack * kTraceThreads * 8; }
 
-cudaError_t launch_trace(const SceneView &sc, bool smem, bool count_work, int grid,
+cudaError_t launch_trace(const SceneView &sc, bool count_work, int grid,
                          const cudaAccessPolicyWindow *window, const float4 *q_o,
                          const float4 *q_d, const int32_t *count, int32_t *fetch, float4 *hits,
                          unsigned long long *ray_ctr, cudaStream_t st) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kTraceThreads);
-  cfg.dynamicSmemBytes = trace_smem_bytes(smem ? sc.n_top : 0);
+  cfg.dynamicSmemBytes = trace_smem_bytes();
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   if (window) {
@@ -880,17 +874,9 @@ cudaError_t launch_trace(const SceneView &sc, bool smem, bool count_work, int gr
     cfg.attrs = attr;
     cfg.numAttrs = 1;
   }
-  if (smem && count_work)
-    return cudaLaunchKernelEx(&cfg, k_trace<true, true>, sc, q_o, q_d, count, fetch, hits,
-                              ray_ctr);
-  if (smem)
-    return cudaLaunchKernelEx(&cfg, k_trace<true, false>, sc, q_o, q_d, count, fetch, hits,
-                              ray_ctr);
   if (count_work)
-    return cudaLaunchKernelEx(&cfg, k_trace<false, true>, sc, q_o, q_d, count, fetch, hits,
-                              ray_ctr);
-  return cudaLaunchKernelEx(&cfg, k_trace<false, false>, sc, q_o, q_d, count, fetch, hits,
-                            ray_ctr);
+    return cudaLaunchKernelEx(&cfg, k_trace<true>, sc, q_o, q_d, count, fetch, hits, ray_ctr);
+  return cudaLaunchKernelEx(&cfg, k_trace<false>, sc, q_o, q_d, count, fetch, hits, ray_ctr);
 }
 
 void launch_trace_rays(const SceneView &sc, const float4 *q_o, const float4 *q_d, int64_t n,

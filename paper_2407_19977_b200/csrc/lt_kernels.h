@@ -60,7 +60,7 @@ struct AccumArgs {
   const int32_t *pix_list;
 };
 
-const void *trace_kernel_ptr(bool smem, bool count);
+const void *trace_kernel_ptr(bool count);
 const void *shade_kernel_ptr();
 
 void launch_flatten_nodes(const double *bmin, const double *bmax, const int32_t *left,
@@ -84,8 +84,8 @@ void launch_raygen_explicit(const double *o, const double *d, const uint64_t *st
                             float4 *q_o, float4 *q_d, int32_t *count0, cudaStream_t st);
 void launch_gather_explicit(const PathArrays &pa, int64_t n, double *rgb, uint64_t *state_out,
                             cudaStream_t st);
-size_t trace_smem_bytes(int n_top);
-cudaError_t launch_trace(const SceneView &sc, bool smem, bool count_work, int grid,
+size_t trace_smem_bytes();
+cudaError_t launch_trace(const SceneView &sc, bool count_work, int grid,
                          const cudaAccessPolicyWindow *window, const float4 *q_o,
                          const float4 *q_d, const int32_t *count, int32_t *fetch, float4 *hits,
                          unsigned long long *ray_ctr, cudaStream_t st);
