@@ -149,8 +149,8 @@ __global__ void k_flatten_tris(const double *__restrict__ v0, const double *__re
 // Primary ray of path p = s_local * n_pix + i (sample-major), keyed by the
 // GLOBAL pixel index and sample index (integrator.py:253-258): stream seed,
 // two jitter draws, float64 pinhole direction; returns the PCG state after
-// the two draws.  Raygen writes the ray record the depth-0 trace reads; the
-// depth-0 shade evaluates it again (bit-identical) instead of reading it.
+// the two draws.  Raygen writes the ray record the depth-0 trace and shade
+// read; the depth-0 shade regenerates only the PCG state (primary_rng).
 __device__ __forceinline__ void primary_ray(const RaygenArgs &ra, int64_t p, f3 &o, f3 &d,
                                             uint64_t &state, uint64_t &inc) {
   // batch-local path index and pixel count are < 2^31 (int32 queues): a
@@ -166,6 +166,18 @@ __device__ __forceinline__ void primary_ray(const RaygenArgs &ra, int64_t p, f3 
   const double jy = unit_f64(state, inc);
   d = camera_dir(ra.cam, (double)px, (double)py, jx, jy, ra.width, ra.height);
   o = f3{(float)ra.cam[0], (float)ra.cam[1], (float)ra.cam[2]};
+}
+
+// The PCG state of path p after its two jitter draws (integer only): the
+// depth-0 shade launch regenerates it instead of reading it back.
+__device__ __forceinline__ void primary_rng(const RaygenArgs &ra, int64_t p, uint64_t &state,
+                                            uint64_t &inc) {
+  const int64_t s_local = (int64_t)((uint32_t)p / (uint32_t)ra.n_pix);
+  const int64_t i = p - s_local * ra.n_pix;
+  const int64_t pix = ra.pix_list ? (int64_t)ra.pix_list[ra.pix_offset + i] : ra.pix_offset + i;
+  seed_stream((uint64_t)pix, (uint64_t)(ra.sample_base + s_local), ra.seed, state, inc);
+  (void)pcg_next(state, inc);
+  (void)pcg_next(state, inc);
 }
 
 // Primary rays of a render batch: only the 32 B ray record is written; the
@@ -430,22 +442,23 @@ __global__ void __launch_bounds__(kShadeThreads, LT_SHADE_MIN_BLOCKS)
       f3 o, d;
       float4 T, L;
       ulonglong2 rs{};
-      if (primary) {
-        // depth 0: queue slot q is path q (raygen order), so the camera ray
-        // and the PCG state after the jitter draws are regenerated exactly
-        // (the same float64 code raygen ran) instead of read back
-        p = q;
-        uint64_t st0, inc0;
-        primary_ray(ra, p, o, d, st0, inc0);
-        rs = make_ulonglong2(st0, inc0);
-        T = make_float4(1.f, 1.f, 1.f, 0.f);
-        L = make_float4(0.f, 0.f, 0.f, 0.f);
-      } else {
+      {
+        // the ray record (regenerating the float64 camera ray here instead
+        // measured slower: +17 % instructions on an issue-bound launch,
+        // profiles/r01_v13_ncu_shade.txt)
         const float4 ro = __ldcs(&q_o[q]);
         const float4 rd = __ldcs(&q_d[q]);
         p = __float_as_int(ro.w);
         o = mk(ro.x, ro.y, ro.z);
         d = mk(rd.x, rd.y, rd.z);
+      }
+      if (primary) {
+        uint64_t st0, inc0;
+        primary_rng(ra, p, st0, inc0);
+        rs = make_ulonglong2(st0, inc0);
+        T = make_float4(1.f, 1.f, 1.f, 0.f);
+        L = make_float4(0.f, 0.f, 0.f, 0.f);
+      } else {
         T = __ldcs(&pa.T[p]);
         L = __ldcs(&pa.L[p]);
       }
