@@ -785,7 +785,7 @@ __global__ void k_iota(int32_t *__restrict__ o, int64_t n) {
       return lt_fail(LT_ERR_CUDA, "%s failed: %s", #call, cudaGetErrorString(e_));      \
   } while (0)
 
-static cudaStream_t g_alloc_stream = nullptr;  // set per build (single-threaded use)
+static thread_local cudaStream_t g_alloc_stream = nullptr;  // the calling thread's build stream
 
 static int alloc(DevMem &m, size_t bytes) {
   m.st = g_alloc_stream;
