@@ -86,11 +86,13 @@ def workload_config(args, n_tris: int, world: int) -> dict:
     }
 
 
-def build_workload(args):
+def build_workload(args, device="auto"):
+    """The scene and its BVH (the reference's tree; device=None builds it
+    with the host restatement -- the reference arm never touches the GPU)."""
     from paper_2407_19977_b200.procgen import scene_by_name
     from paper_2407_19977_b200 import build_bvh
     scene = scene_by_name(args.workload, width=args.width, height=args.height)
-    bvh = build_bvh(scene.triangles, leaf_size=args.bvh_leaf, bins=args.bvh_bins)
+    bvh = build_bvh(scene.triangles, leaf_size=args.bvh_leaf, bins=args.bvh_bins, device=device)
     return scene, bvh
 
 
@@ -223,7 +225,7 @@ def run_reference(args, rank: int, world: int) -> None:
         return
     from oracle.oracle import OracleScene, default_threads
     from paper_2407_19977_b200 import camera_pack
-    scene, bvh = build_workload(args)
+    scene, bvh = build_workload(args, device=None)
     oc = OracleScene.from_scene(scene, bvh)
     cam = camera_pack(scene.camera)
     w, h = args.width, args.height
