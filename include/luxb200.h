@@ -52,7 +52,11 @@ typedef struct lt_scene_desc {
   int64_t n_triangles;
   const double *v0, *v1, *v2, *n0, *n1, *n2;
   const int32_t *material_index;
-  /* Bvh (bvh.py:38-50), the host-built tree, consumed unchanged */
+  /* Bvh (bvh.py:38-50), the host-built tree, consumed unchanged.  n_nodes
+   * = 0 with all seven BVH pointers NULL: the scene builds the reference's
+   * tree itself on the device (build_bvh defaults: leaf size 4, 12 bins),
+   * without a host round trip (render_progressive(scene, settings) with no
+   * BVH, integrator.py:321-326). */
   int64_t n_nodes;
   const double *bounds_min, *bounds_max;            /* (n_nodes,3) */
   const int32_t *left_child, *right_child;          /* (n_nodes,) -1 at leaves */

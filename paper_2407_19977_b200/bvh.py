@@ -1,9 +1,10 @@
 """BVH types and closest-hit queries of the drop-in API (bvh.py of the
 reference).
 
-* `build_bvh` runs the native host builder (csrc/lt_bvh_build.cpp), a
-  restatement of the reference's binned SAH that yields bit-identical
-  arrays, so a tree built here equals the reference's host-built tree.
+* `build_bvh` returns the reference's exact arrays from the GPU build
+  (csrc/lt_bvh_gpu.cu) when a device is present, else from the host
+  restatement (csrc/lt_bvh_build.cpp); a `DeviceScene` created without a BVH
+  builds the same tree on the device without a host round trip.
 * `intersect_scene_batch` / `intersect_scene` / `traversal_counts_batch`
   run the sm_100a traversal kernel through the C-ABI.
 """

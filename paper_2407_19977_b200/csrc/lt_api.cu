@@ -1,6 +1,7 @@
 // lt_api.cu -- the C-ABI (include/luxb200.h): scene residency, the render
 // pass orchestration (the wavefront loop), ray queries and host-buffer
 // drop-ins with the reference's dtypes.
+#include <cub/cub.cuh>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -313,8 +314,14 @@ static int validate_desc(const lt_scene_desc *d) {
     return lt_fail(LT_ERR_INVALID, "too many triangles (%lld)", (long long)d->n_triangles);
   if (!d->v0 || !d->v1 || !d->v2 || !d->n0 || !d->n1 || !d->n2 || !d->material_index)
     return lt_fail(LT_ERR_INVALID, "triangle arrays must be non-null");
-  if (d->n_nodes < 1 || !d->bounds_min || !d->bounds_max || !d->left_child ||
-      !d->right_child || !d->first_triangle || !d->triangle_count || !d->triangle_order)
+  // n_nodes == 0 with no BVH arrays: the scene builds the reference's tree on
+  // the device (lt_scene_desc in luxb200.h)
+  const bool build_here = d->n_nodes == 0 && !d->bounds_min && !d->bounds_max &&
+                          !d->left_child && !d->right_child && !d->first_triangle &&
+                          !d->triangle_count && !d->triangle_order;
+  if (!build_here && (d->n_nodes < 1 || !d->bounds_min || !d->bounds_max || !d->left_child ||
+                      !d->right_child || !d->first_triangle || !d->triangle_count ||
+                      !d->triangle_order))
     return lt_fail(LT_ERR_INVALID, "bvh arrays must be non-null");
   if (d->n_materials < 1 || !d->base_weight || !d->base_color || !d->base_metalness ||
       !d->specular_weight || !d->specular_color || !d->specular_roughness ||
@@ -324,8 +331,11 @@ static int validate_desc(const lt_scene_desc *d) {
   // chunked scans on host threads; the reported failure is the first index,
   // as a sequential scan would report it
   auto tri_bad = [&](int64_t i) {
-    const int32_t m = d->material_index[i], o = d->triangle_order[i];
-    return m < 0 || m >= d->n_materials || o < 0 || o >= n;
+    const int32_t m = d->material_index[i];
+    if (m < 0 || m >= d->n_materials) return true;
+    if (build_here) return false;
+    const int32_t o = d->triangle_order[i];
+    return o < 0 || o >= n;
   };
   auto node_bad = [&](int64_t i) {
     if (d->triangle_count[i] > 0) {
@@ -357,7 +367,7 @@ static int validate_desc(const lt_scene_desc *d) {
                      (long long)bt, m, d->n_materials);
     return lt_fail(LT_ERR_INVALID, "triangle_order[%lld] = %d out of range", (long long)bt, o);
   }
-  const int64_t bn = first_bad(nn, node_bad);
+  const int64_t bn = build_here ? -1 : first_bad(nn, node_bad);
   if (bn >= 0) {
     if (d->triangle_count[bn] > 0) {
       const int64_t f = d->first_triangle[bn], c = d->triangle_count[bn];
@@ -570,6 +580,65 @@ static int configure_launches(lt_scene *s) {
   return LT_OK;
 }
 
+// Layout of a device-built BVH without a host round trip: the internal
+// binary nodes in index order (prefix sum) for the counter query, and the
+// 4-wide collapse level by level (the host path's greedy expansion; wide
+// nodes numbered breadth first, deterministically by prefix sums).
+static int device_layout(lt_scene *s, const double *bmin, const double *bmax,
+                         const int32_t *left, const int32_t *right, const int32_t *count,
+                         int64_t nn, bool root_leaf, TmpBuf &t_perm, TmpBuf &t_new,
+                         TmpBuf &t_wch, TmpBuf &t_wof) {
+  cudaStream_t st = s->stream;
+  TmpBuf flags, scan, tmp;
+  RET(flags.alloc((size_t)(nn + 1) * 4, st));
+  RET(scan.alloc((size_t)(nn + 1) * 4, st));
+  CK(cudaMemsetAsync(flags.p, 0, (size_t)(nn + 1) * 4, st));
+  launch_internal_flags(count, nn, flags.as<int32_t>(), st);
+  size_t tmp_bytes = 0;
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, flags.as<int32_t>(), scan.as<int32_t>(),
+                                   (int)(nn + 1), st));
+  RET(tmp.alloc(std::max<size_t>(tmp_bytes, 16), st));
+  CK(cub::DeviceScan::ExclusiveSum(tmp.p, tmp_bytes, flags.as<int32_t>(), scan.as<int32_t>(),
+                                   (int)(nn + 1), st));
+  RET(t_perm.alloc((size_t)std::max<int64_t>(nn, 1) * 4, st));
+  RET(t_new.alloc((size_t)std::max<int64_t>(nn, 1) * 4, st));
+  launch_internal_scatter(flags.as<int32_t>(), scan.as<int32_t>(), nn, t_perm.as<int32_t>(),
+                          t_new.as<int32_t>(), st);
+  int32_t n_internal = 0;
+  CK(cudaMemcpyAsync(&n_internal, scan.as<int32_t>() + nn, 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  s->n_internal = n_internal;
+  s->n_bfs = 0;
+  s->n_wide = 0;
+  RET(t_wch.alloc((size_t)std::max<int64_t>(n_internal, 1) * 16, st));
+  RET(t_wof.alloc((size_t)std::max<int64_t>(nn, 1) * 4, st));
+  if (root_leaf || n_internal == 0) return LT_OK;
+  TmpBuf roots[2], kids, off;
+  for (auto &r : roots) RET(r.alloc((size_t)n_internal * 4, st));
+  RET(kids.alloc((size_t)(n_internal + 1) * 4, st));
+  RET(off.alloc((size_t)(n_internal + 1) * 4, st));
+  CK(cudaMemsetAsync(roots[0].p, 0, 4, st));  // the root (binary node 0)
+  int32_t n_roots = 1, base = 0;
+  int cur = 0;
+  while (n_roots > 0) {
+    launch_collapse_level(bmin, bmax, left, right, count, roots[cur].as<int32_t>(), n_roots, base,
+                          t_wch.as<int32_t>(), t_wof.as<int32_t>(), kids.as<int32_t>(), st);
+    CK(cudaMemsetAsync(kids.as<int32_t>() + n_roots, 0, 4, st));
+    CK(cub::DeviceScan::ExclusiveSum(tmp.p, tmp_bytes, kids.as<int32_t>(), off.as<int32_t>(),
+                                     n_roots + 1, st));
+    launch_collapse_emit(t_wch.as<int32_t>(), count, n_roots, base, off.as<int32_t>(),
+                         roots[cur ^ 1].as<int32_t>(), st);
+    int32_t next = 0;
+    CK(cudaMemcpyAsync(&next, off.as<int32_t>() + n_roots, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    base += n_roots;
+    n_roots = next;
+    cur ^= 1;
+  }
+  s->n_wide = base;
+  return LT_OK;
+}
+
 static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s) {
   PhaseTimer pt;
   s->device = device;
@@ -590,7 +659,7 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
     // keep stream-ordered scene / staging memory mapped between scenes
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-      uint64_t keep = 4ull << 30;
+      uint64_t keep = UINT64_MAX;  // never trim: the pool peaks at the scene + staging + build scratch
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
     }
   }
@@ -600,9 +669,13 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
     b->ast = s->stream;
   }
   cudaStream_t st = s->stream;
-  const int64_t n = d->n_triangles, nn = d->n_nodes;
+  const int64_t n = d->n_triangles;
+  // no host BVH (n_nodes == 0): build the reference's tree (leaf size 4, 12
+  // bins, build_bvh's defaults) on the device from the uploaded vertices and
+  // lay it out without a host round trip
+  const bool build_here = d->n_nodes == 0;
+  int64_t nn = d->n_nodes;
   s->n_tris = n;
-  s->n_nodes = nn;
   pt.mark("stream + attributes");
 
   // --- start every upload that depends only on the description now, so the
@@ -613,23 +686,74 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
   const double *src[6] = {d->v0, d->v1, d->v2, d->n0, d->n1, d->n2};
   for (int k = 0; k < 6; ++k) RET(upload(t_v[k], src[k], 3 * n, st));
   RET(upload(t_mat, d->material_index, n, st));
-  RET(upload(t_order, d->triangle_order, n, st));
-  RET(upload(t_bmin, d->bounds_min, 3 * nn, st));
-  RET(upload(t_bmax, d->bounds_max, 3 * nn, st));
-  RET(upload(t_left, d->left_child, nn, st));
-  RET(upload(t_right, d->right_child, nn, st));
-  RET(upload(t_first, d->first_triangle, nn, st));
-  RET(upload(t_count, d->triangle_count, nn, st));
+  struct TreeGuard {
+    lt_gpu_tree t{};
+    ~TreeGuard() { lt_gpu_tree_free(&t); }
+  } tree;
+  const double *g_bmin, *g_bmax;
+  const int32_t *g_left, *g_right, *g_first, *g_count, *g_order;
+  bool root_leaf;
+  int32_t root_first;
+  double root_lo[3], root_hi[3];
+  if (build_here) {
+    RET(lt_gpu_tree_build(t_v[0].as<double>(), t_v[1].as<double>(), t_v[2].as<double>(), n, 4,
+                          12, st, &tree.t));
+    nn = tree.t.n_nodes;
+    g_bmin = tree.t.bmin;
+    g_bmax = tree.t.bmax;
+    g_left = tree.t.left;
+    g_right = tree.t.right;
+    g_first = tree.t.first;
+    g_count = tree.t.count;
+    g_order = tree.t.order;
+    int32_t rc0[2];
+    CK(cudaMemcpyAsync(&rc0[0], g_count, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&rc0[1], g_first, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(root_lo, g_bmin, 24, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(root_hi, g_bmax, 24, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    root_leaf = rc0[0] > 0;
+    root_first = rc0[1];
+    pt.mark("device BVH build");
+  } else {
+    RET(upload(t_order, d->triangle_order, n, st));
+    RET(upload(t_bmin, d->bounds_min, 3 * nn, st));
+    RET(upload(t_bmax, d->bounds_max, 3 * nn, st));
+    RET(upload(t_left, d->left_child, nn, st));
+    RET(upload(t_right, d->right_child, nn, st));
+    RET(upload(t_first, d->first_triangle, nn, st));
+    RET(upload(t_count, d->triangle_count, nn, st));
+    g_bmin = t_bmin.as<double>();
+    g_bmax = t_bmax.as<double>();
+    g_left = t_left.as<int32_t>();
+    g_right = t_right.as<int32_t>();
+    g_first = t_first.as<int32_t>();
+    g_count = t_count.as<int32_t>();
+    g_order = t_order.as<int32_t>();
+    root_leaf = d->triangle_count[0] > 0;
+    root_first = d->first_triangle[0];
+    for (int a = 0; a < 3; ++a) {
+      root_lo[a] = d->bounds_min[a];
+      root_hi[a] = d->bounds_max[a];
+    }
+  }
+  s->n_nodes = nn;
   // leaf-end flags of the leaf-ordered triangle stream, on the device
   RET(t_end.alloc(std::max<int64_t>(n, 16), st));
   CK(cudaMemsetAsync(t_end.p, 0, (size_t)n, st));
-  launch_leaf_end(t_first.as<int32_t>(), t_count.as<int32_t>(), nn, t_end.as<uint8_t>(), st);
+  launch_leaf_end(g_first, g_count, nn, t_end.as<uint8_t>(), st);
   pt.mark("uploads enqueue");
 
+  std::vector<int32_t> new_index, perm, wide_children, wide_of;
+  if (build_here) {
+    RET(device_layout(s, g_bmin, g_bmax, g_left, g_right, g_count, nn, root_leaf, t_perm, t_new,
+                      t_wch, t_wof));
+    pt.mark("device layout");
+  } else {
   // --- internal-node renumbering: top levels BFS, the rest depth-first.
   // The depth-first part expands the pending subtrees on host threads; bases
   // follow the sequential order, so the numbering is the sequential one.
-  std::vector<int32_t> new_index(nn, -1), perm;
+  new_index.assign(nn, -1);
   perm.reserve(nn);
   auto is_leaf = [&](int64_t i) { return d->triangle_count[i] > 0; };
   if (!is_leaf(0)) {
@@ -675,7 +799,7 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
   // replaces the internal child with the largest surface area by its two
   // children, up to four.  Numbering: the top wide nodes breadth first, then
   // each pending subtree depth first (collapsed on host threads).
-  std::vector<int32_t> wide_children, wide_of(nn, -1);
+  wide_of.assign(nn, -1);
   if (!is_leaf(0)) {
     auto area = [&](int32_t x) {
       const double *lo = d->bounds_min + 3 * (int64_t)x, *hi = d->bounds_max + 3 * (int64_t)x;
@@ -740,6 +864,7 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
   }
   s->n_wide = (int64_t)(wide_children.size() / 4);
   pt.mark("4-wide collapse");
+  }  // host layout
   // --- flatten on the device
   int rc = LT_OK;
   do {
@@ -756,20 +881,20 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
     float4 *g_nodes = s->nodes2.as<float4>();
     launch_flatten_tris(t_v[0].as<double>(), t_v[1].as<double>(), t_v[2].as<double>(),
                         t_v[3].as<double>(), t_v[4].as<double>(), t_v[5].as<double>(),
-                        t_mat.as<int32_t>(), t_order.as<int32_t>(), t_end.as<uint8_t>(), n,
-                        g_tris, g_shade, st);
+                        t_mat.as<int32_t>(), g_order, t_end.as<uint8_t>(), n, g_tris, g_shade,
+                        st);
     if (s->n_internal > 0) {
-      if ((rc = upload(t_perm, perm.data(), perm.size(), st))) break;
-      if ((rc = upload(t_new, new_index.data(), nn, st))) break;
-      launch_flatten_nodes(t_bmin.as<double>(), t_bmax.as<double>(), t_left.as<int32_t>(),
-                           t_right.as<int32_t>(), t_first.as<int32_t>(), t_count.as<int32_t>(),
+      if (!build_here) {
+        if ((rc = upload(t_perm, perm.data(), perm.size(), st))) break;
+        if ((rc = upload(t_new, new_index.data(), nn, st))) break;
+        if ((rc = upload(t_wch, wide_children.data(), wide_children.size(), st))) break;
+        if ((rc = upload(t_wof, wide_of.data(), wide_of.size(), st))) break;
+      }
+      launch_flatten_nodes(g_bmin, g_bmax, g_left, g_right, g_first, g_count,
                            t_perm.as<int32_t>(), t_new.as<int32_t>(), s->n_internal, g_nodes,
                            st);
-      if ((rc = upload(t_wch, wide_children.data(), wide_children.size(), st))) break;
-      if ((rc = upload(t_wof, wide_of.data(), wide_of.size(), st))) break;
-      launch_flatten_wide(t_bmin.as<double>(), t_bmax.as<double>(), t_first.as<int32_t>(),
-                          t_count.as<int32_t>(), t_wch.as<int32_t>(), t_wof.as<int32_t>(),
-                          s->n_wide, g_wide, st);
+      launch_flatten_wide(g_bmin, g_bmax, g_first, g_count, t_wch.as<int32_t>(),
+                          t_wof.as<int32_t>(), s->n_wide, g_wide, st);
     }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
@@ -801,16 +926,16 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
 
   SceneView &v = s->view;
   v.wnodes = s->geo.as<float4>();
-  v.wroot_link = is_leaf(0) ? ~d->first_triangle[0] : 0;
+  v.wroot_link = root_leaf ? ~root_first : 0;
   v.nodes = s->nodes2.as<float4>();
   v.tris = s->geo.as<float4>() + s->nodes_bytes / 16;
   v.shade = s->geo.as<float4>() + s->shade_off / 16;
   v.mats = s->mats.as<GpuMaterial>();
   v.env_map = s->env.as<float4>();
-  v.root_link = is_leaf(0) ? ~d->first_triangle[0] : 0;
+  v.root_link = root_leaf ? ~root_first : 0;
   for (int a = 0; a < 3; ++a) {
-    v.root_lo[a] = f32_down(d->bounds_min[a]);
-    v.root_hi[a] = f32_up(d->bounds_max[a]);
+    v.root_lo[a] = f32_down(root_lo[a]);
+    v.root_hi[a] = f32_up(root_hi[a]);
   }
   v.env_kind = d->env_kind;
   v.env_w = d->env_width;

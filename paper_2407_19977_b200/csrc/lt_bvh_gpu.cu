@@ -801,22 +801,23 @@ static int alloc(DevMem &m, size_t bytes) {
     if (rc_ != LT_OK) return rc_;    \
   } while (0)
 
-static int build_on_device(const double *v0, const double *v1, const double *v2, int64_t n,
-                           int leaf_size, int n_bins, cudaStream_t st,
-                           std::vector<double> &tbmin, std::vector<double> &tbmax,
-                           std::vector<int32_t> &tleft, std::vector<int32_t> &tright,
-                           std::vector<int32_t> &tfirst, std::vector<int32_t> &tcount,
-                           int32_t *order_out, Counters &ctr_h) {
+// Device-resident result of a build: provisional node ids (root = 0), the
+// final triangle order, counters.
+struct TreeOut {
+  DevMem tree_b, tree_i, order;
+  Tree t;
+  Counters ctr{};
+};
+
+// The build on device-resident vertices (float64 (n,3) arrays); the tree
+// stays on the device.
+static int build_tree(const double *dv0, const double *dv1, const double *dv2, int64_t n,
+                      int leaf_size, int n_bins, cudaStream_t st, TreeOut &out) {
   BuildTimer bt;
   const int64_t max_nodes = 2 * n;
-  DevMem d_v, d_tb, d_order[2], d_seg, d_flag, d_pre, d_beta, d_belem, d_tree_b, d_tree_i,
-      d_ctr, d_acc, d_jobs[2], d_small, d_state, d_bins, d_cnt, d_chunks, d_scan_tmp;
-  GRET(alloc(d_v, 3 * 3 * n * sizeof(double)));
-  GCK(cudaMemcpyAsync(d_v.as<double>(), v0, 3 * n * sizeof(double), cudaMemcpyHostToDevice, st));
-  GCK(cudaMemcpyAsync(d_v.as<double>() + 3 * n, v1, 3 * n * sizeof(double),
-                      cudaMemcpyHostToDevice, st));
-  GCK(cudaMemcpyAsync(d_v.as<double>() + 6 * n, v2, 3 * n * sizeof(double),
-                      cudaMemcpyHostToDevice, st));
+  DevMem d_tb, d_order[2], d_seg, d_flag, d_pre, d_beta, d_belem, d_ctr, d_acc, d_jobs[2],
+      d_small, d_state, d_bins, d_cnt, d_chunks, d_scan_tmp;
+  DevMem &d_tree_b = out.tree_b, &d_tree_i = out.tree_i;
   GRET(alloc(d_tb, 9 * n * sizeof(double)));
   for (auto &o : d_order) GRET(alloc(o, n * sizeof(int32_t)));
   GRET(alloc(d_seg, n * sizeof(int32_t)));
@@ -835,8 +836,8 @@ static int build_on_device(const double *v0, const double *v1, const double *v2,
   GRET(alloc(d_bins, 2 * max_large * kMaxBins * 12 * sizeof(unsigned long long)));
   GRET(alloc(d_cnt, 2 * max_large * kMaxBins * sizeof(unsigned int)));
 
-  bt.mark("allocations + vertex upload", st);
-  Tree t;
+  bt.mark("allocations", st);
+  Tree &t = out.t;
   t.bmin = d_tree_b.as<double>();
   t.bmax = t.bmin + 3 * max_nodes;
   t.left = d_tree_i.as<int32_t>();
@@ -848,8 +849,7 @@ static int build_on_device(const double *v0, const double *v1, const double *v2,
   GCK(cudaMemsetAsync(d_ctr.p, 0, sizeof(Counters), st));
   const unsigned blocks_n = (unsigned)((n + kThreads - 1) / kThreads);
   k_iota<<<blocks_n, kThreads, 0, st>>>(d_order[0].as<int32_t>(), n);
-  k_tri_bounds<<<blocks_n, kThreads, 0, st>>>(d_v.as<double>(), d_v.as<double>() + 3 * n,
-                                               d_v.as<double>() + 6 * n, n, d_tb.as<double>());
+  k_tri_bounds<<<blocks_n, kThreads, 0, st>>>(dv0, dv1, dv2, n, d_tb.as<double>());
   {
     unsigned long long init[12];
     for (int q = 0; q < 12; ++q) init[q] = (q < 3 || (q >= 6 && q < 9)) ? ~0ull : 0ull;
@@ -954,9 +954,35 @@ static int build_on_device(const double *v0, const double *v1, const double *v2,
   }
   bt.mark("subtree kernel", st);
   if (bt.on) std::fprintf(stderr, "[luxb200 bvh-gpu] %d large levels, %d subtree jobs\n", levels, c.n_small);
-  GCK(cudaMemcpyAsync(&ctr_h, d_ctr.p, sizeof(Counters), cudaMemcpyDeviceToHost, st));
+  GCK(cudaMemcpyAsync(&out.ctr, d_ctr.p, sizeof(Counters), cudaMemcpyDeviceToHost, st));
   GCK(cudaStreamSynchronize(st));
-  if (ctr_h.error) return lt_fail(LT_ERR_CUDA, "GPU BVH build: partition count mismatch");
+  if (out.ctr.error) return lt_fail(LT_ERR_CUDA, "GPU BVH build: partition count mismatch");
+  std::swap(out.order.p, d_order[cur].p);  // the final permutation outlives the scratch
+  std::swap(out.order.st, d_order[cur].st);
+  return LT_OK;
+}
+
+// Host arrays in, provisional-id tree + order out (for lt_build_bvh_device).
+static int build_on_device(const double *v0, const double *v1, const double *v2, int64_t n,
+                           int leaf_size, int n_bins, cudaStream_t st,
+                           std::vector<double> &tbmin, std::vector<double> &tbmax,
+                           std::vector<int32_t> &tleft, std::vector<int32_t> &tright,
+                           std::vector<int32_t> &tfirst, std::vector<int32_t> &tcount,
+                           int32_t *order_out, Counters &ctr_h) {
+  BuildTimer bt;
+  DevMem d_v;
+  GRET(alloc(d_v, 3 * 3 * n * sizeof(double)));
+  GCK(cudaMemcpyAsync(d_v.as<double>(), v0, 3 * n * sizeof(double), cudaMemcpyHostToDevice, st));
+  GCK(cudaMemcpyAsync(d_v.as<double>() + 3 * n, v1, 3 * n * sizeof(double),
+                      cudaMemcpyHostToDevice, st));
+  GCK(cudaMemcpyAsync(d_v.as<double>() + 6 * n, v2, 3 * n * sizeof(double),
+                      cudaMemcpyHostToDevice, st));
+  bt.mark("vertex upload", st);
+  TreeOut out;
+  GRET(build_tree(d_v.as<double>(), d_v.as<double>() + 3 * n, d_v.as<double>() + 6 * n, n,
+                  leaf_size, n_bins, st, out));
+  ctr_h = out.ctr;
+  const Tree &t = out.t;
   const int64_t nn = ctr_h.nodes;
   tbmin.resize(3 * nn);
   tbmax.resize(3 * nn);
@@ -970,14 +996,51 @@ static int build_on_device(const double *v0, const double *v1, const double *v2,
   GCK(cudaMemcpyAsync(tright.data(), t.right, nn * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   GCK(cudaMemcpyAsync(tfirst.data(), t.first, nn * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   GCK(cudaMemcpyAsync(tcount.data(), t.count, nn * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-  GCK(cudaMemcpyAsync(order_out, d_order[cur].p, n * sizeof(int32_t), cudaMemcpyDeviceToHost,
-                      st));
+  GCK(cudaMemcpyAsync(order_out, out.order.p, n * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   GCK(cudaStreamSynchronize(st));
   bt.mark("tree + order download", st);
   return LT_OK;
 }
 
 }  // namespace
+
+// Device-resident build for lt_scene_create (no host round trip): the
+// reference's tree with provisional ids (root 0).  `stream` is a cudaStream_t.
+extern int lt_gpu_tree_build(const double *dv0, const double *dv1, const double *dv2, int64_t n,
+                             int32_t leaf_size, int32_t bins, void *stream, lt_gpu_tree *out) {
+  if (n <= 0) return lt_fail(LT_ERR_INVALID, "empty scene");
+  if (bins > kMaxBins || bins < 2 || leaf_size < 1)
+    return lt_fail(LT_ERR_INVALID, "unsupported BVH build parameters");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  g_alloc_stream = st;
+  auto *to = new TreeOut;
+  const int rc = build_tree(dv0, dv1, dv2, n, leaf_size, bins, st, *to);
+  if (rc != LT_OK) {
+    delete to;
+    return rc;
+  }
+  const int64_t max_nodes = 2 * n;
+  (void)max_nodes;
+  out->bmin = to->t.bmin;
+  out->bmax = to->t.bmax;
+  out->left = to->t.left;
+  out->right = to->t.right;
+  out->first = to->t.first;
+  out->count = to->t.count;
+  out->order = to->order.as<int32_t>();
+  out->n_nodes = to->ctr.nodes;
+  out->n_leaves = to->ctr.leaves;
+  out->max_depth = to->ctr.max_depth;
+  out->impl = to;
+  return LT_OK;
+}
+
+void lt_gpu_tree_free(lt_gpu_tree *t) {
+  if (t && t->impl) {
+    delete static_cast<TreeOut *>(t->impl);  // frees stream-ordered on the build stream
+    t->impl = nullptr;
+  }
+}
 
 // The reference's numbering: pop depth first (left child first); the k-th
 // internal node popped allocates its children as the next two ids.
@@ -1005,7 +1068,7 @@ extern "C" int lt_build_bvh_device(int32_t device, const double *v0, const doubl
   {
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-      uint64_t keep = 4ull << 30, cur = 0;
+      uint64_t keep = UINT64_MAX, cur = 0;
       cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &cur);
       if (cur < keep) cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
     }

@@ -583,6 +583,118 @@ __global__ void __launch_bounds__(kShadeThreads, LT_SHADE_MIN_BLOCKS)
   }
 }
 
+// ------------------------------------------------------------------ device layout
+// Layout of a BVH built on the device (lt_scene_create without host BVH
+// arrays): the binary-node list for the counter query and the 4-wide
+// collapse, the same greedy largest-area expansion as the host path.
+
+__global__ void k_internal_flags(const int32_t *__restrict__ count, int64_t nn,
+                                 int32_t *__restrict__ flags) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < nn) flags[i] = count[i] == 0 ? 1 : 0;
+}
+
+__global__ void k_internal_scatter(const int32_t *__restrict__ flags,
+                                   const int32_t *__restrict__ scan, int64_t nn,
+                                   int32_t *__restrict__ perm, int32_t *__restrict__ new_index) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= nn) return;
+  if (flags[i]) {
+    new_index[i] = scan[i];
+    perm[scan[i]] = (int32_t)i;
+  } else {
+    new_index[i] = -1;
+  }
+}
+
+__device__ __forceinline__ double node_area(const double *__restrict__ bmin,
+                                            const double *__restrict__ bmax, int32_t x) {
+  const double *lo = bmin + 3 * (int64_t)x, *hi = bmax + 3 * (int64_t)x;
+  const double dx = hi[0] - lo[0], dy = hi[1] - lo[1], dz = hi[2] - lo[2];
+  return dx * dy + dy * dz + dz * dx;
+}
+
+// wide nodes [base, base + n_roots) from their binary roots: children, and
+// the number of internal children (the next level's roots)
+__global__ void k_collapse_level(const double *__restrict__ bmin, const double *__restrict__ bmax,
+                                 const int32_t *__restrict__ left,
+                                 const int32_t *__restrict__ right,
+                                 const int32_t *__restrict__ count,
+                                 const int32_t *__restrict__ roots, int32_t n_roots,
+                                 int32_t base, int32_t *__restrict__ wide_children,
+                                 int32_t *__restrict__ wide_of, int32_t *__restrict__ n_kids) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_roots) return;
+  const int32_t r = roots[i];
+  wide_of[r] = base + i;
+  int32_t ch[4] = {left[r], right[r], -1, -1};
+  int nc = 2;
+  while (nc < 4) {
+    int pick = -1;
+    double best_area = -1.0;
+    for (int k = 0; k < nc; ++k)
+      if (count[ch[k]] == 0) {
+        const double a = node_area(bmin, bmax, ch[k]);
+        if (a > best_area) {
+          best_area = a;
+          pick = k;
+        }
+      }
+    if (pick < 0) break;
+    const int32_t x = ch[pick];
+    for (int k = nc; k > pick + 1; --k) ch[k] = ch[k - 1];
+    ch[pick] = left[x];
+    ch[pick + 1] = right[x];
+    ++nc;
+  }
+  int internal = 0;
+  for (int k = 0; k < 4; ++k) {
+    const int32_t c = k < nc ? ch[k] : -1;
+    wide_children[4 * (int64_t)(base + i) + k] = c;
+    internal += (c >= 0 && count[c] == 0) ? 1 : 0;
+  }
+  n_kids[i] = internal;
+}
+
+__global__ void k_collapse_emit(const int32_t *__restrict__ wide_children,
+                                const int32_t *__restrict__ count, int32_t n_roots, int32_t base,
+                                const int32_t *__restrict__ kid_off,
+                                int32_t *__restrict__ next_roots) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_roots) return;
+  int j = kid_off[i];
+  for (int k = 0; k < 4; ++k) {
+    const int32_t c = wide_children[4 * (int64_t)(base + i) + k];
+    if (c >= 0 && count[c] == 0) next_roots[j++] = c;
+  }
+}
+
+void launch_internal_flags(const int32_t *count, int64_t nn, int32_t *flags, cudaStream_t st) {
+  if (nn > 0) k_internal_flags<<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(count, nn, flags);
+}
+void launch_internal_scatter(const int32_t *flags, const int32_t *scan, int64_t nn,
+                             int32_t *perm, int32_t *new_index, cudaStream_t st) {
+  if (nn > 0)
+    k_internal_scatter<<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(flags, scan, nn, perm,
+                                                                      new_index);
+}
+void launch_collapse_level(const double *bmin, const double *bmax, const int32_t *left,
+                           const int32_t *right, const int32_t *count, const int32_t *roots,
+                           int32_t n_roots, int32_t base, int32_t *wide_children,
+                           int32_t *wide_of, int32_t *n_kids, cudaStream_t st) {
+  if (n_roots > 0)
+    k_collapse_level<<<(n_roots + 127) / 128, 128, 0, st>>>(bmin, bmax, left, right, count, roots,
+                                                            n_roots, base, wide_children, wide_of,
+                                                            n_kids);
+}
+void launch_collapse_emit(const int32_t *wide_children, const int32_t *count, int32_t n_roots,
+                          int32_t base, const int32_t *kid_off, int32_t *next_roots,
+                          cudaStream_t st) {
+  if (n_roots > 0)
+    k_collapse_emit<<<(n_roots + 127) / 128, 128, 0, st>>>(wide_children, count, n_roots, base,
+                                                           kid_off, next_roots);
+}
+
 // ------------------------------------------------------------------ env map
 
 __global__ void k_expand_rgb(const float *__restrict__ rgb, int64_t n, float4 *__restrict__ out) {

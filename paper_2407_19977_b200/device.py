@@ -49,11 +49,10 @@ class DeviceScene:
         return self
 
     def _init(self, triangles, bvh, materials, environment, device):
-        from .bvh import build_bvh
         _lib.require_gpu()
         self.handle = None
-        if bvh is None:
-            bvh = build_bvh(triangles)
+        # bvh None: lt_scene_create builds the reference's tree on the device
+        # (no host round trip); `self.bvh` stays None
         self.bvh = bvh
         n = len(triangles)
         keep = []  # arrays must stay alive until lt_scene_create returns
@@ -73,13 +72,17 @@ class DeviceScene:
         d.v0, d.v1, d.v2 = (p64(triangles.v0), p64(triangles.v1), p64(triangles.v2))
         d.n0, d.n1, d.n2 = (p64(triangles.n0), p64(triangles.n1), p64(triangles.n2))
         d.material_index = p32(triangles.material_index)
-        nn = int(np.asarray(bvh.left_child).shape[0])
-        d.n_nodes = nn
-        d.bounds_min = p64(bvh.bounds_min, (nn, 3))
-        d.bounds_max = p64(bvh.bounds_max, (nn, 3))
-        d.left_child, d.right_child = p32(bvh.left_child), p32(bvh.right_child)
-        d.first_triangle, d.triangle_count = p32(bvh.first_triangle), p32(bvh.triangle_count)
-        d.triangle_order = p32(bvh.triangle_order)
+        if bvh is None:
+            d.n_nodes = 0       # all BVH pointers stay NULL
+        else:
+            nn = int(np.asarray(bvh.left_child).shape[0])
+            d.n_nodes = nn
+            d.bounds_min = p64(bvh.bounds_min, (nn, 3))
+            d.bounds_max = p64(bvh.bounds_max, (nn, 3))
+            d.left_child, d.right_child = p32(bvh.left_child), p32(bvh.right_child)
+            d.first_triangle = p32(bvh.first_triangle)
+            d.triangle_count = p32(bvh.triangle_count)
+            d.triangle_order = p32(bvh.triangle_order)
         table = pack_material_table(materials)
         self.n_materials = len(table["base_weight"])
         d.n_materials = self.n_materials

@@ -171,6 +171,31 @@ def test_render_without_bvh_builds_the_reference_tree(name):
     assert np.array_equal(built.invalid_samples, with_ref.invalid_samples)
 
 
+@pytest.mark.parametrize("name", ["floor", "glossy", "sphere2k", "dup", "cornell_c2", "sphere20k"])
+def test_device_built_scene_equals_host_bvh_scene(name):
+    """DeviceScene without a BVH builds the reference's tree on the device
+    (lt_scene_create, n_nodes = 0): per-sample radiance is bit-identical to
+    the scene made from the reference-built BVH, and so are the reference
+    traversal counters (the same tree under another node numbering)."""
+    g = golden_scene(name)
+    host = device_scene(g)
+    dev = lb().DeviceScene(g.scene)
+    assert dev.bvh is None and dev.info["n_nodes"] == len(g["bvh_left"])
+    for s in range(2):
+        a = gpu_sample_values(host, g.camera, g.settings, s)
+        b = gpu_sample_values(dev, g.camera, g.settings, s)
+        assert np.array_equal(np.nan_to_num(a, nan=-1.0), np.nan_to_num(b, nan=-1.0))
+    rng = np.random.default_rng(3)
+    o = g["rays_o"]
+    d = g["rays_d"]
+    n1, t1 = lb().traversal_counts_batch(g.triangles, None, o, d, scene=host)
+    n2, t2 = lb().traversal_counts_batch(g.triangles, None, o, d, scene=dev)
+    assert np.array_equal(n1, n2) and np.array_equal(t1, t2)
+    i1, _ = lb().intersect_scene_batch(g.triangles, None, o, d, scene=host)
+    i2, _ = lb().intersect_scene_batch(g.triangles, None, o, d, scene=dev)
+    assert np.array_equal(i1, i2)
+
+
 @pytest.mark.parametrize("name", ["floor", "glossy", "sphere2k", "cornell_c2"])
 def test_trace_radiance_matches_reference(name):
     g = golden_scene(name)
