@@ -1116,12 +1116,35 @@ static int pixel_set(lt_scene *s, const lt_render_params *p, const int32_t **lis
     // scatter on the device (no 2 M-entry host list, no synchronous copy)
     const int64_t W = p->width, H = p->height, T = tile_sz;
     const int64_t ntx = (W + T - 1) / T, nty = (H + T - 1) / T;
-    std::vector<int32_t> tile_start;
-    tile_start.reserve((size_t)(ntx * nty / n_ranks + 2));
+    // this rank's tiles (tile = rank, rank + n_ranks, ...); the order in
+    // which they are laid out: row-major, or (LT_TILE_CURVE=morton) along a
+    // Z curve over the tile grid, so consecutive paths cover a compact
+    // square instead of a strip
+    std::vector<int64_t> tiles;
+    for (int64_t tile = rank; tile < ntx * nty; tile += n_ranks) tiles.push_back(tile);
+    const char *curve = std::getenv("LT_TILE_CURVE");
+    if (curve && std::strcmp(curve, "morton") == 0) {
+      auto spread = [](uint64_t v) {
+        uint64_t x = v & 0xffffffffull;
+        x = (x | (x << 16)) & 0x0000ffff0000ffffull;
+        x = (x | (x << 8)) & 0x00ff00ff00ff00ffull;
+        x = (x | (x << 4)) & 0x0f0f0f0f0f0f0f0full;
+        x = (x | (x << 2)) & 0x3333333333333333ull;
+        x = (x | (x << 1)) & 0x5555555555555555ull;
+        return x;
+      };
+      auto key = [&](int64_t tile) {
+        const int64_t ty = tile / ntx, tx = tile - ty * ntx;
+        return spread((uint64_t)tx) | (spread((uint64_t)ty) << 1);
+      };
+      std::stable_sort(tiles.begin(), tiles.end(),
+                       [&](int64_t a, int64_t b) { return key(a) < key(b); });
+    }
+    std::vector<int32_t> tile_start((size_t)(ntx * nty / n_ranks + 2), 0);
     int64_t total = 0;
-    for (int64_t tile = rank; tile < ntx * nty; tile += n_ranks) {
+    for (int64_t tile : tiles) {
       const int64_t ty = tile / ntx, tx = tile - ty * ntx;
-      tile_start.push_back((int32_t)total);
+      tile_start[(size_t)(tile / n_ranks)] = (int32_t)total;
       total += (std::min(W, (tx + 1) * T) - tx * T) * (std::min(H, (ty + 1) * T) - ty * T);
     }
     RET(s->pix_list.ensure(std::max<size_t>(16, (size_t)total * 4)));
