@@ -118,6 +118,10 @@ typedef struct lt_render_stats {
   int64_t tri_tests;            /* triangle tests (LT_FLAG_COUNT only) */
   double trace_ms;              /* sum of CUDA-event times of the trace launches
                                    (LT_FLAG_PROFILE only, else 0) */
+  /* LT_FLAG_COUNT only: shade warps, warps whose active lanes span more than
+   * one material class (miss / last segment / diffuse-only / full BSDF /
+   * coat / glass), and the sum of distinct classes per warp */
+  int64_t shade_warps, shade_mixed_warps, shade_warp_classes;
 } lt_render_stats;
 
 /* ---- library ---- */

@@ -94,6 +94,8 @@ class RenderStats(C.Structure):
         ("kernel_launches", C.c_int64), ("trace_launches", C.c_int64),
         ("slab_tests", C.c_int64), ("tri_tests", C.c_int64),
         ("trace_ms", C.c_double),
+        ("shade_warps", C.c_int64), ("shade_mixed_warps", C.c_int64),
+        ("shade_warp_classes", C.c_int64),
     ]
 
 

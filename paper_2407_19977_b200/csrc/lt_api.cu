@@ -1025,7 +1025,7 @@ static int ensure_lane(lt_scene *s, Lane &ln, int64_t cap, int32_t max_depth) {
     RET(ln.counters.ensure(sizeof(int32_t) * (2 * (size_t)max_depth + 2)));
     ln.depth_cap = max_depth;
   }
-  RET(s->ray_ctr.ensure(3 * sizeof(unsigned long long)));
+  RET(s->ray_ctr.ensure(6 * sizeof(unsigned long long)));
   return LT_OK;
 }
 
@@ -1065,7 +1065,8 @@ static int run_bounces(lt_scene *s, Lane &lane, int32_t max_depth, int32_t rr_st
                     ws->q_d[cur].as<float4>(), ctr + depth, fetch + depth,
                     ws->hits.as<float4>(), s->ray_ctr.as<unsigned long long>(), st));
     if (flags & LT_FLAG_PROFILE) RET(record_event(s, st));
-    ShadeArgs sa{depth, max_depth, rr_start, t_min, 0, s->octant_sort ? 1 : 0};
+    ShadeArgs sa{depth, max_depth, rr_start, t_min, 0, s->octant_sort ? 1 : 0,
+                 (flags & LT_FLAG_COUNT) ? s->ray_ctr.as<unsigned long long>() + 3 : nullptr};
     CK(launch_shade(sc, sa, pa, s->shade_grid,
                     s->use_window && s->use_shade_window ? &s->shade_window : nullptr, prim,
                     ws->q_o[cur].as<float4>(), ws->q_d[cur].as<float4>(),
@@ -1211,7 +1212,7 @@ static int render_impl(lt_scene *s, const lt_render_params *p, float *accum, uin
   }
   WorkspaceLease lease(s->ws, st);
   for (int k = 0; k < n_lanes; ++k) RET(ensure_lane(s, s->ws->lane[k], lane_cap[k], p->max_depth));
-  CK(cudaMemsetAsync(s->ray_ctr.p, 0, 3 * sizeof(unsigned long long), st));
+  CK(cudaMemsetAsync(s->ray_ctr.p, 0, 6 * sizeof(unsigned long long), st));
   // fork the lane streams off the caller's stream
   CK(cudaEventRecord(s->fork_ev, st));
   for (int k = 0; k < n_lanes; ++k) CK(cudaStreamWaitEvent(s->lane_st[k], s->fork_ev, 0));
@@ -1263,11 +1264,14 @@ extern "C" int lt_render_stats_get(const lt_scene *cs, lt_render_stats *out) {
   lt_scene *s = const_cast<lt_scene *>(cs);
   DeviceGuard g(s->device);
   if (s->ray_ctr.p) {
-    unsigned long long c[3] = {0, 0, 0};
+    unsigned long long c[6] = {0, 0, 0, 0, 0, 0};
     CK(cudaMemcpy(c, s->ray_ctr.p, sizeof(c), cudaMemcpyDeviceToHost));
     s->stats.rays = (int64_t)c[0];
     s->stats.slab_tests = (int64_t)c[1];
     s->stats.tri_tests = (int64_t)c[2];
+    s->stats.shade_warps = (int64_t)c[3];
+    s->stats.shade_mixed_warps = (int64_t)c[4];
+    s->stats.shade_warp_classes = (int64_t)c[5];
   }
   // trace launches of concurrent lanes overlap: report the union of their
   // [start, end] intervals (time during which any trace kernel ran)
@@ -1456,7 +1460,7 @@ extern "C" int lt_trace_paths_host(lt_scene *s, const double *origins, const dou
   CK(cudaMemcpyAsync(d_state, state, 8 * n, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(d_inc, inc, 8 * n, cudaMemcpyHostToDevice, st));
   CK(cudaMemsetAsync(ln.counters.p, 0, sizeof(int32_t) * (2 * (size_t)max_depth + 2), st));
-  CK(cudaMemsetAsync(s->ray_ctr.p, 0, 3 * sizeof(unsigned long long), st));
+  CK(cudaMemsetAsync(s->ray_ctr.p, 0, 6 * sizeof(unsigned long long), st));
   const PathArrays pa = path_arrays(ln);
   launch_raygen_explicit(d_o, d_d, d_state, d_inc, n, (float)t_min, pa, ln.q_o[0].as<float4>(),
                          ln.q_d[0].as<float4>(), ln.counters.as<int32_t>(), st);

@@ -433,6 +433,7 @@ __global__ void __launch_bounds__(kShadeThreads, LT_SHADE_MIN_BLOCKS)
     const int q = base + threadIdx.x;
     bool emit = false;
     float4 out_o, out_d;
+    int cls = -1;  // material class of the lane's hit (LT_FLAG_COUNT statistics)
     if (q < n) {
       // queue entries and path state stream through (evict-first) so the
       // L2 keeps the triangle / shading records
@@ -463,6 +464,7 @@ __global__ void __launch_bounds__(kShadeThreads, LT_SHADE_MIN_BLOCKS)
         L = __ldcs(&pa.L[p]);
       }
       bool wrote_l = false;
+      cls = 0;  // miss
       if (k < 0) {
         const f3 e = env_radiance(sc, d);
         L.x += T.x * e.x;
@@ -485,6 +487,13 @@ __global__ void __launch_bounds__(kShadeThreads, LT_SHADE_MIN_BLOCKS)
         }
         const int32_t mi = __float_as_int(s0.w);
         const GpuMaterial &mt = sc.mats[mi];
+        if (sa.warp_ctr)
+          cls = !scatter ? 1
+                         : (mt.flags & MAT_DIFFUSE_ONLY)
+                               ? 2
+                               : (mt.flags & (MAT_COAT | MAT_GLASS)) ? 3 + (int)(mt.flags &
+                                                                            (MAT_COAT | MAT_GLASS))
+                                                                     : 3;
         if (mt.flags & MAT_EMISSIVE) {
           L.x += T.x * mt.el * mt.ec[0];
           L.y += T.y * mt.el * mt.ec[1];
@@ -536,6 +545,20 @@ __global__ void __launch_bounds__(kShadeThreads, LT_SHADE_MIN_BLOCKS)
       // the radiance slot of every path is written by its primary launch
       // (raygen no longer clears it)
       if (primary && !wrote_l) __stcs(&pa.L[p], L);
+    }
+    if (sa.warp_ctr) {
+      // shading divergence: distinct material classes among a warp's lanes
+      const unsigned act = __ballot_sync(kFull, cls >= 0);
+      if (act) {
+        const unsigned same = __match_any_sync(kFull, cls);
+        const bool first_of_class = cls >= 0 && __ffs(same & act) - 1 == lane;
+        const int distinct = __popc(__ballot_sync(kFull, first_of_class));
+        if (lane == __ffs(act) - 1) {
+          atomicAdd(&sa.warp_ctr[0], 1ull);
+          atomicAdd(&sa.warp_ctr[1], distinct > 1 ? 1ull : 0ull);
+          atomicAdd(&sa.warp_ctr[2], (unsigned long long)distinct);
+        }
+      }
     }
     if (sa.octant_sort) {
       // block-aggregated append grouped by direction: one contiguous range

@@ -53,6 +53,9 @@ struct ShadeArgs {
   float t_min;
   int32_t primary;  // depth-0 launch of a render batch: rays from RaygenArgs
   int32_t octant_sort;  // append continuation rays grouped by direction octant
+  // LT_FLAG_COUNT: [warps, warps whose active lanes span > 1 material class,
+  // sum over warps of the distinct classes] (shading divergence evidence)
+  unsigned long long *warp_ctr;
 };
 
 struct AccumArgs {
