@@ -175,6 +175,10 @@ struct Workspace {
   std::mutex mu;
   Lane lane[kLanes];
   cudaEvent_t last_use = nullptr;
+  // the lanes' streams and the fork / join events, created on first use and
+  // shared by every scene on the device (passes are serialized by `mu`)
+  cudaStream_t lane_st[kLanes] = {};
+  cudaEvent_t fork_ev = nullptr, join_ev[kLanes] = {};
 };
 
 static Workspace *workspace_for(int device) {
@@ -244,8 +248,6 @@ struct lt_scene {
   int smem_nodes = 0;
   int64_t default_batch = int64_t(1) << 22;
   int n_lanes = kLanes;
-  cudaStream_t lane_st[kLanes] = {};
-  cudaEvent_t fork_ev = nullptr, join_ev[kLanes] = {};
   bool octant_sort = false;
   // stats of the last pass
   lt_render_stats stats{};
@@ -293,7 +295,7 @@ static void parallel_for(int64_t n, F f) {
   if (n <= 0) return;
   const int64_t hw = std::max<int64_t>(1, (int64_t)std::thread::hardware_concurrency());
   const int64_t nt = std::min<int64_t>({n, hw, 16});
-  if (nt <= 1) {
+  if (nt <= 1 || n < 4) {
     for (int64_t i = 0; i < n; ++i) f(i);
     return;
   }
@@ -346,7 +348,8 @@ static int validate_desc(const lt_scene_desc *d) {
     return l <= i || r <= i || l >= nn || r >= nn;
   };
   auto first_bad = [&](int64_t count, auto bad) {
-    const int64_t chunks = 64;
+    // ~16 K items per chunk: tiny scenes scan inline (no thread start-up)
+    const int64_t chunks = std::max<int64_t>(1, std::min<int64_t>(64, count >> 14));
     std::vector<int64_t> hit(chunks, -1);
     parallel_for(chunks, [&](int64_t c) {
       for (int64_t i = count * c / chunks; i < count * (c + 1) / chunks; ++i)
@@ -485,11 +488,6 @@ static void destroy_scene(lt_scene *s) {
   pt.mark("destroy: device frees");
   s->h_stage.release();
   for (cudaEvent_t e : s->ev_pool) cudaEventDestroy(e);
-  for (int k = 0; k < kLanes; ++k) {
-    if (s->lane_st[k]) cudaStreamDestroy(s->lane_st[k]);
-    if (s->join_ev[k]) cudaEventDestroy(s->join_ev[k]);
-  }
-  if (s->fork_ev) cudaEventDestroy(s->fork_ev);
   if (s->stream) cudaStreamDestroy(s->stream);
   pt.mark("destroy: host + stream");
   delete s;
@@ -646,11 +644,6 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
   CK(cudaDeviceGetAttribute(&s->sm_count, cudaDevAttrMultiProcessorCount, device));
   CK(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
   s->ws = workspace_for(device);
-  for (int k = 0; k < kLanes; ++k) {
-    CK(cudaStreamCreateWithFlags(&s->lane_st[k], cudaStreamNonBlocking));
-    CK(cudaEventCreateWithFlags(&s->join_ev[k], cudaEventDisableTiming));
-  }
-  CK(cudaEventCreateWithFlags(&s->fork_ev, cudaEventDisableTiming));
   {
     const char *ls = std::getenv("LT_LANES");
     s->n_lanes = std::max(1, std::min(kLanes, ls ? std::atoi(ls) : kDefaultLanes));
@@ -1214,12 +1207,20 @@ static int render_impl(lt_scene *s, const lt_render_params *p, float *accum, uin
   for (int k = 0; k < n_lanes; ++k) RET(ensure_lane(s, s->ws->lane[k], lane_cap[k], p->max_depth));
   CK(cudaMemsetAsync(s->ray_ctr.p, 0, 6 * sizeof(unsigned long long), st));
   // fork the lane streams off the caller's stream
-  CK(cudaEventRecord(s->fork_ev, st));
-  for (int k = 0; k < n_lanes; ++k) CK(cudaStreamWaitEvent(s->lane_st[k], s->fork_ev, 0));
+  Workspace &W = *s->ws;
+  if (!W.fork_ev) {
+    for (int k = 0; k < kLanes; ++k) {
+      CK(cudaStreamCreateWithFlags(&W.lane_st[k], cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&W.join_ev[k], cudaEventDisableTiming));
+    }
+    CK(cudaEventCreateWithFlags(&W.fork_ev, cudaEventDisableTiming));
+  }
+  CK(cudaEventRecord(W.fork_ev, st));
+  for (int k = 0; k < n_lanes; ++k) CK(cudaStreamWaitEvent(W.lane_st[k], W.fork_ev, 0));
   const float t_min = (float)p->t_min;
   for (const Batch &b : order) {
     Lane &ln = s->ws->lane[b.lane];
-    cudaStream_t ls = s->lane_st[b.lane];
+    cudaStream_t ls = W.lane_st[b.lane];
     int32_t *ctr = ln.counters.as<int32_t>();
     CK(cudaMemsetAsync(ctr, 0, sizeof(int32_t) * (2 * (size_t)p->max_depth + 2), ls));
     RaygenArgs ra{};
@@ -1245,8 +1246,8 @@ static int render_impl(lt_scene *s, const lt_render_params *p, float *accum, uin
   }
   // join back into the caller's stream
   for (int k = 0; k < n_lanes; ++k) {
-    CK(cudaEventRecord(s->join_ev[k], s->lane_st[k]));
-    CK(cudaStreamWaitEvent(st, s->join_ev[k], 0));
+    CK(cudaEventRecord(W.join_ev[k], W.lane_st[k]));
+    CK(cudaStreamWaitEvent(st, W.join_ev[k], 0));
   }
   CK(cudaGetLastError());
   return LT_OK;
