@@ -59,7 +59,6 @@ namespace {
 // from 452 to 277 ms (profiles/r01_batch_sweep.jsonl).  128 B of queues and
 // path state per path: 64M paths = 8 GB, bounded by a quarter of free HBM.
 constexpr int64_t kMaxBatchPaths = int64_t(1) << 26;
-constexpr int32_t kMaxBfsNodes = 2048;                    // BFS-ordered top of the tree
 
 // Device buffer.  With `ast` set the memory comes stream-ordered from the
 // device's default mempool (cudaMallocAsync / cudaFreeAsync on `ast`), so a
@@ -179,6 +178,9 @@ struct Workspace {
   // shared by every scene on the device (passes are serialized by `mu`)
   cudaStream_t lane_st[kLanes] = {};
   cudaEvent_t fork_ev = nullptr, join_ev[kLanes] = {};
+  // side stream for scene triangle uploads (overlaps the BVH layout)
+  cudaStream_t upload_st = nullptr;
+  std::mutex upload_mu;
 };
 
 static Workspace *workspace_for(int device) {
@@ -671,14 +673,11 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
   s->n_tris = n;
   pt.mark("stream + attributes");
 
-  // --- start every upload that depends only on the description now, so the
-  // copies (pinned sources: asynchronous DMA) overlap the host-side
-  // renumbering and collapse below
+  // --- every upload that depends only on the description, enqueued first
+  // (pinned sources: asynchronous DMA)
   TmpBuf t_v[6], t_mat, t_order, t_end, t_bmin, t_bmax, t_left, t_right, t_first, t_count,
       t_perm, t_new, t_wch, t_wof, t_env;
   const double *src[6] = {d->v0, d->v1, d->v2, d->n0, d->n1, d->n2};
-  for (int k = 0; k < 6; ++k) RET(upload(t_v[k], src[k], 3 * n, st));
-  RET(upload(t_mat, d->material_index, n, st));
   struct TreeGuard {
     lt_gpu_tree t{};
     ~TreeGuard() { lt_gpu_tree_free(&t); }
@@ -688,7 +687,14 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
   bool root_leaf;
   int32_t root_first;
   double root_lo[3], root_hi[3];
+  cudaEvent_t tri_done = nullptr;
+  auto upload_triangles = [&](cudaStream_t ts) -> int {
+    for (int k = 0; k < 6; ++k) RET(upload(t_v[k], src[k], 3 * n, ts));
+    RET(upload(t_mat, d->material_index, n, ts));
+    return LT_OK;
+  };
   if (build_here) {
+    RET(upload_triangles(st));  // the device build reads the vertices
     RET(lt_gpu_tree_build(t_v[0].as<double>(), t_v[1].as<double>(), t_v[2].as<double>(), n, 4,
                           12, st, &tree.t));
     nn = tree.t.n_nodes;
@@ -716,6 +722,20 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
     RET(upload(t_right, d->right_child, nn, st));
     RET(upload(t_first, d->first_triangle, nn, st));
     RET(upload(t_count, d->triangle_count, nn, st));
+    // the triangle arrays follow on the workspace's side stream: the BVH
+    // arrays are enqueued first (the copy engine serves them first) and
+    // their device layout overlaps the larger triangle transfer; the
+    // flatten joins both streams
+    {
+      std::lock_guard<std::mutex> lk(s->ws->upload_mu);
+      if (!s->ws->upload_st)
+        CK(cudaStreamCreateWithFlags(&s->ws->upload_st, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&tri_done, cudaEventDisableTiming));
+      CK(cudaEventRecord(tri_done, st));
+      CK(cudaStreamWaitEvent(s->ws->upload_st, tri_done, 0));
+      RET(upload_triangles(s->ws->upload_st));
+      CK(cudaEventRecord(tri_done, s->ws->upload_st));
+    }
     g_bmin = t_bmin.as<double>();
     g_bmax = t_bmax.as<double>();
     g_left = t_left.as<int32_t>();
@@ -737,127 +757,17 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
   launch_leaf_end(g_first, g_count, nn, t_end.as<uint8_t>(), st);
   pt.mark("uploads enqueue");
 
-  std::vector<int32_t> new_index, perm, wide_children, wide_of;
-  if (build_here) {
-    RET(device_layout(s, g_bmin, g_bmax, g_left, g_right, g_count, nn, root_leaf, t_perm, t_new,
-                      t_wch, t_wof));
-    pt.mark("device layout");
-  } else {
-  // --- internal-node renumbering: top levels BFS, the rest depth-first.
-  // The depth-first part expands the pending subtrees on host threads; bases
-  // follow the sequential order, so the numbering is the sequential one.
-  new_index.assign(nn, -1);
-  perm.reserve(nn);
-  auto is_leaf = [&](int64_t i) { return d->triangle_count[i] > 0; };
-  if (!is_leaf(0)) {
-    std::vector<int32_t> queue;
-    queue.push_back(0);
-    size_t head = 0;
-    while (head < queue.size() && (int64_t)perm.size() < kMaxBfsNodes) {
-      const int32_t x = queue[head++];
-      new_index[x] = (int32_t)perm.size();
-      perm.push_back(x);
-      for (int32_t c : {d->left_child[x], d->right_child[x]})
-        if (!is_leaf(c)) queue.push_back(c);
-    }
-    s->n_bfs = (int64_t)perm.size();
-    const std::vector<int32_t> roots(queue.begin() + head, queue.end());
-    std::vector<std::vector<int32_t>> part(roots.size());
-    parallel_for((int64_t)roots.size(), [&](int64_t q) {
-      std::vector<int32_t> stack{roots[q]};
-      std::vector<int32_t> &out = part[q];
-      while (!stack.empty()) {
-        const int32_t x = stack.back();
-        stack.pop_back();
-        out.push_back(x);
-        const int32_t l = d->left_child[x], r = d->right_child[x];
-        if (!is_leaf(r)) stack.push_back(r);
-        if (!is_leaf(l)) stack.push_back(l);
-      }
-    });
-    std::vector<int64_t> base(roots.size() + 1, (int64_t)perm.size());
-    for (size_t q = 0; q < roots.size(); ++q) base[q + 1] = base[q] + (int64_t)part[q].size();
-    perm.resize(base[roots.size()]);
-    parallel_for((int64_t)roots.size(), [&](int64_t q) {
-      for (size_t k = 0; k < part[q].size(); ++k) {
-        perm[base[q] + k] = part[q][k];
-        new_index[part[q][k]] = (int32_t)(base[q] + k);
-      }
-    });
+  // --- layout on the device for both paths: the internal binary nodes in
+  // index order (prefix sum) for the counter query, and the 4-wide collapse
+  // level by level (greedy largest-area expansion; the host-side version
+  // took ~4.6 ms of host time at 1 M triangles)
+  RET(device_layout(s, g_bmin, g_bmax, g_left, g_right, g_count, nn, root_leaf, t_perm, t_new,
+                    t_wch, t_wof));
+  pt.mark("device layout");
+  if (tri_done) {
+    CK(cudaStreamWaitEvent(st, tri_done, 0));  // the triangle uploads
+    cudaEventDestroy(tri_done);  // released once the recorded work completes
   }
-  s->n_internal = (int64_t)perm.size();
-  pt.mark("binary renumbering");
-  // --- 4-wide collapse of the same tree (render / closest-hit layout): a
-  // wide node starts from its binary node's two children and repeatedly
-  // replaces the internal child with the largest surface area by its two
-  // children, up to four.  Numbering: the top wide nodes breadth first, then
-  // each pending subtree depth first (collapsed on host threads).
-  wide_of.assign(nn, -1);
-  if (!is_leaf(0)) {
-    auto area = [&](int32_t x) {
-      const double *lo = d->bounds_min + 3 * (int64_t)x, *hi = d->bounds_max + 3 * (int64_t)x;
-      const double dx = hi[0] - lo[0], dy = hi[1] - lo[1], dz = hi[2] - lo[2];
-      return dx * dy + dy * dz + dz * dx;
-    };
-    // collapse wide node r: its (up to) 4 children, pushing the internal ones
-    auto collapse = [&](int32_t r, std::vector<int32_t> &kids, std::vector<int32_t> &stack) {
-      int32_t ch[4] = {d->left_child[r], d->right_child[r], -1, -1};
-      int nc = 2;
-      while (nc < 4) {
-        int pick = -1;
-        double best_area = -1.0;
-        for (int i = 0; i < nc; ++i)
-          if (!is_leaf(ch[i]) && area(ch[i]) > best_area) {
-            best_area = area(ch[i]);
-            pick = i;
-          }
-        if (pick < 0) break;
-        const int32_t x = ch[pick];
-        for (int j = nc; j > pick + 1; --j) ch[j] = ch[j - 1];
-        ch[pick] = d->left_child[x];
-        ch[pick + 1] = d->right_child[x];
-        ++nc;
-      }
-      for (int i = 0; i < 4; ++i) kids.push_back(i < nc ? ch[i] : -1);
-      for (int i = nc - 1; i >= 0; --i)
-        if (!is_leaf(ch[i])) stack.push_back(ch[i]);
-    };
-    // top of the tree breadth first (the hot wide nodes contiguous) until 256
-    // subtrees are pending; those are collapsed depth first in parallel
-    std::vector<int32_t> queue{0}, top;  // top: binary roots of the top wide nodes
-    size_t qh = 0;
-    while (qh < queue.size() && queue.size() - qh < 256) {
-      const int32_t r = queue[qh++];
-      top.push_back(r);
-      std::vector<int32_t> kids_in;
-      collapse(r, wide_children, kids_in);
-      queue.insert(queue.end(), kids_in.rbegin(), kids_in.rend());
-    }
-    const std::vector<int32_t> pending(queue.begin() + qh, queue.end());
-    std::vector<std::vector<int32_t>> roots_of(pending.size()), kids_of(pending.size());
-    parallel_for((int64_t)pending.size(), [&](int64_t q) {
-      std::vector<int32_t> st{pending[q]};
-      while (!st.empty()) {
-        const int32_t r = st.back();
-        st.pop_back();
-        roots_of[q].push_back(r);
-        collapse(r, kids_of[q], st);
-      }
-    });
-    for (size_t k = 0; k < top.size(); ++k) wide_of[top[k]] = (int32_t)k;
-    std::vector<int64_t> base(pending.size() + 1, (int64_t)top.size());
-    for (size_t q = 0; q < pending.size(); ++q)
-      base[q + 1] = base[q] + (int64_t)roots_of[q].size();
-    wide_children.resize(4 * base[pending.size()]);
-    parallel_for((int64_t)pending.size(), [&](int64_t q) {
-      for (size_t k = 0; k < roots_of[q].size(); ++k)
-        wide_of[roots_of[q][k]] = (int32_t)(base[q] + k);
-      std::copy(kids_of[q].begin(), kids_of[q].end(), wide_children.begin() + 4 * base[q]);
-    });
-  }
-  s->n_wide = (int64_t)(wide_children.size() / 4);
-  pt.mark("4-wide collapse");
-  }  // host layout
   // --- flatten on the device
   int rc = LT_OK;
   do {
@@ -877,12 +787,6 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
                         t_mat.as<int32_t>(), g_order, t_end.as<uint8_t>(), n, g_tris, g_shade,
                         st);
     if (s->n_internal > 0) {
-      if (!build_here) {
-        if ((rc = upload(t_perm, perm.data(), perm.size(), st))) break;
-        if ((rc = upload(t_new, new_index.data(), nn, st))) break;
-        if ((rc = upload(t_wch, wide_children.data(), wide_children.size(), st))) break;
-        if ((rc = upload(t_wof, wide_of.data(), wide_of.size(), st))) break;
-      }
       launch_flatten_nodes(g_bmin, g_bmax, g_left, g_right, g_first, g_count,
                            t_perm.as<int32_t>(), t_new.as<int32_t>(), s->n_internal, g_nodes,
                            st);

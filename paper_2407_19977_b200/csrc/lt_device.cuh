@@ -17,8 +17,8 @@
 //              n2 = (L.lo.z, L.hi.z, R.lo.z, R.hi.z)
 //              n3 = (link L, link R, -, -)   link >= 0: internal node,
 //                                            link < 0: leaf, first = ~link
-//            Internal nodes are renumbered: the top levels in BFS order
-//            (staged in shared memory), the rest depth-first.
+//            Internal nodes in the order of their index in the source
+//            tree (the reference's numbering, or the device build's).
 //   tris   : LT_TRI_F4 (3) x float4 per triangle in LEAF order (triangle_order)
 //              (v0.xyz, original index), (e1.xyz, last-in-leaf flag),
 //              (e2.xyz, 0); e1/e2 are rounded from the float64 differences.
