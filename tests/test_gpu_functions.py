@@ -125,6 +125,69 @@ def test_sampled_albedo_never_gains_energy_on_device():
         assert np.all(w[ok].sum(axis=0) / len(draws) <= 1.01)
 
 
+def _glossy_probe():
+    import paper_2407_19977_b200 as lb
+    p = lb.OpenPbrParams(base_metalness=0.0, specular_weight=1.0, specular_roughness=0.3)
+    return p, np.array([np.sqrt(1.0 - 0.85 ** 2), 0.0, 0.85])
+
+
+def _grid_dirs(c_lo, c_hi, p_lo, p_hi, nc, nphi):
+    c = c_lo + (np.arange(nc) + 0.5) / nc * (c_hi - c_lo)
+    phi = p_lo + (np.arange(nphi) + 0.5) / nphi * (p_hi - p_lo)
+    cc, pp = np.meshgrid(c, phi, indexing="ij")
+    sn = np.sqrt(1.0 - cc * cc)
+    return np.stack([sn * np.cos(pp), sn * np.sin(pp), cc], axis=-1).reshape(-1, 3)
+
+
+def test_pdf_integrates_to_one_on_device():
+    """test_material.py:253-269: midpoint quadrature of the device pdf over
+    the hemisphere lies in (0.97, 1.005)."""
+    from paper_2407_19977_b200.bsdf import eval_pdf_batch
+    p, wo = _glossy_probe()
+    wi = _grid_dirs(0.0, 1.0, 0.0, 2.0 * np.pi, 200, 200)
+    _, pdf = eval_pdf_batch([p] * len(wi), wo, wi, [0.0, 0.0, 1.0])
+    integral = pdf.sum() / len(wi) * 2.0 * np.pi
+    print("pdf integral", integral)
+    assert 0.97 < integral < 1.005
+
+
+def test_sampler_matches_pdf_histogram_on_device():
+    """test_material.py:272-318: chi-square of 150k device samples against
+    the device pdf integrated over 8 x 8 (cos, phi) bins, the rejected mass
+    as its own bin."""
+    from scipy import stats
+    from paper_2407_19977_b200.bsdf import eval_pdf_batch, sample_batch
+    p, wo = _glossy_probe()
+    n_draws, n_cos, n_phi, sub = 150_000, 8, 8, 24
+    expected = np.zeros(n_cos * n_phi + 1)
+    for bc in range(n_cos):
+        for bp in range(n_phi):
+            wi = _grid_dirs(bc / n_cos, (bc + 1) / n_cos, bp / n_phi * 2 * np.pi,
+                            (bp + 1) / n_phi * 2 * np.pi, sub, sub)
+            _, pdf = eval_pdf_batch([p] * len(wi), wo, wi, [0.0, 0.0, 1.0])
+            expected[bc * n_phi + bp] = pdf.sum() / (n_cos * n_phi * sub * sub) * 2 * np.pi
+    expected[-1] = max(1.0 - expected[:-1].sum(), 0.0)
+    expected *= n_draws
+    draws = np.random.default_rng(31337).uniform(0, 1, (n_draws, 3))
+    ok, wi, _ = sample_batch([p] * n_draws, wo, [0.0, 0.0, 1.0], draws)
+    observed = np.zeros_like(expected)
+    observed[-1] = np.count_nonzero(~ok)
+    c = np.minimum(wi[ok, 2], 1.0 - 1e-12)
+    phi = np.arctan2(wi[ok, 1], wi[ok, 0]) % (2.0 * np.pi)
+    bc = (c * n_cos).astype(int)
+    bp = np.minimum((phi / (2 * np.pi) * n_phi).astype(int), n_phi - 1)
+    np.add.at(observed, bc * n_phi + bp, 1)
+    keep = expected >= 10.0
+    e, o = expected[keep], observed[keep]
+    if not keep.all():
+        e = np.append(e, expected[~keep].sum())
+        o = np.append(o, observed[~keep].sum())
+    e *= o.sum() / e.sum()
+    res = stats.chisquare(o, e)
+    print("chi-square p", res.pvalue)
+    assert res.pvalue > 0.001
+
+
 @pytest.mark.parametrize("name", SCENES)
 def test_any_hit_agrees_with_closest_hit(name):
     import paper_2407_19977_b200 as lb
