@@ -945,8 +945,17 @@ static int record_event(lt_scene *s, cudaStream_t st) {
 // the camera rays themselves (render batches); otherwise queue 0 must hold
 // the primary rays and counters[0] their number (explicit rays).
 static int run_bounces(lt_scene *s, Lane &lane, int32_t max_depth, int32_t rr_start, float t_min,
-                       uint32_t flags, cudaStream_t st, const RaygenArgs *primary = nullptr) {
+                       uint32_t flags, cudaStream_t st, const RaygenArgs *primary,
+                       int64_t max_rays) {
   SceneView sc = s->view;
+  // a batch never holds more than max_rays rays: small batches (tiny frames)
+  // launch only the CTAs that can find work
+  const int trace_grid =
+      (int)std::max<int64_t>(1, std::min<int64_t>(s->trace_grid[0],
+                                                  (max_rays + kTraceThreads - 1) / kTraceThreads));
+  const int shade_grid =
+      (int)std::max<int64_t>(1, std::min<int64_t>(s->shade_grid,
+                                                  (max_rays + kShadeThreads - 1) / kShadeThreads));
   Lane *ws = &lane;
   int32_t *ctr = ws->counters.as<int32_t>();
   int32_t *fetch = ctr + max_depth + 1;
@@ -957,14 +966,14 @@ static int run_bounces(lt_scene *s, Lane &lane, int32_t max_depth, int32_t rr_st
     if (flags & LT_FLAG_PROFILE) RET(record_event(s, st));
     // (in-kernel ray generation for trace measured slower than reading the
     // 32 B ray record: the float64 camera math serializes the refill path)
-    CK(launch_trace(sc, (flags & LT_FLAG_COUNT) != 0, s->trace_grid[0],
+    CK(launch_trace(sc, (flags & LT_FLAG_COUNT) != 0, trace_grid,
                     s->use_window ? &s->window : nullptr, ws->q_o[cur].as<float4>(),
                     ws->q_d[cur].as<float4>(), ctr + depth, fetch + depth,
                     ws->hits.as<float4>(), s->ray_ctr.as<unsigned long long>(), st));
     if (flags & LT_FLAG_PROFILE) RET(record_event(s, st));
     ShadeArgs sa{depth, max_depth, rr_start, t_min, 0, s->octant_sort ? 1 : 0,
                  (flags & LT_FLAG_COUNT) ? s->ray_ctr.as<unsigned long long>() + 3 : nullptr};
-    CK(launch_shade(sc, sa, pa, s->shade_grid,
+    CK(launch_shade(sc, sa, pa, shade_grid,
                     s->use_window && s->use_shade_window ? &s->shade_window : nullptr, prim,
                     ws->q_o[cur].as<float4>(), ws->q_d[cur].as<float4>(),
                     ws->hits.as<float4>(), ctr + depth, ws->q_o[cur ^ 1].as<float4>(),
@@ -1141,7 +1150,7 @@ static int render_impl(lt_scene *s, const lt_render_params *p, float *accum, uin
     // raygen writes only the ray records; the depth-0 shade regenerates
     // throughput / radiance / PCG state
     launch_raygen(ra, path_arrays(ln), ln.q_o[0].as<float4>(), ln.q_d[0].as<float4>(), ctr, ls);
-    RET(run_bounces(s, ln, p->max_depth, p->rr_start, t_min, p->flags, ls, &ra));
+    RET(run_bounces(s, ln, p->max_depth, p->rr_start, t_min, p->flags, ls, &ra, ra.n_paths));
     AccumArgs aa{b.np, b.pc0, b.ns, pix_list};
     launch_accumulate(aa, ln.L.as<float4>(), accum, valid, invalid, ls);
     s->stats.kernel_launches += 2;
@@ -1369,7 +1378,7 @@ extern "C" int lt_trace_paths_host(lt_scene *s, const double *origins, const dou
   const PathArrays pa = path_arrays(ln);
   launch_raygen_explicit(d_o, d_d, d_state, d_inc, n, (float)t_min, pa, ln.q_o[0].as<float4>(),
                          ln.q_d[0].as<float4>(), ln.counters.as<int32_t>(), st);
-  RET(run_bounces(s, ln, max_depth, rr_start, (float)t_min, 0u, st));
+  RET(run_bounces(s, ln, max_depth, rr_start, (float)t_min, 0u, st, nullptr, n));
   RET(s->s_b.ensure(32 * n));
   double *d_rgb = s->s_b.as<double>();
   uint64_t *d_sout = reinterpret_cast<uint64_t *>(d_rgb + 3 * n);
