@@ -245,13 +245,12 @@ __global__ void __launch_bounds__(kTraceThreads, LT_TRACE_MIN_BLOCKS)
             const int32_t *__restrict__ count, int32_t *__restrict__ fetch,
             float4 *__restrict__ hits, unsigned long long *__restrict__ ray_ctr) {
   extern __shared__ float4 s_mem[];
-  int32_t *s_node = reinterpret_cast<int32_t *>(s_mem);
-  float *s_t = reinterpret_cast<float *>(s_node + kShortStack * kTraceThreads);
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const unsigned lanes_below = (1u << lane) - 1u;
-  int32_t l_node[LT_STACK - kShortStack];
-  float l_t[LT_STACK - kShortStack];
+  // stack entry = (node, entry t) in one 64-bit word: one STS.64 / LDS.64
+  uint2 *const s_stk = reinterpret_cast<uint2 *>(s_mem) + tid;
+  uint2 l_stk[LT_STACK - kShortStack];
 
   const int n = *count;
   if (blockIdx.x == 0 && tid == 0) atomicAdd(ray_ctr, (unsigned long long)n);
@@ -309,27 +308,17 @@ __global__ void __launch_bounds__(kTraceThreads, LT_TRACE_MIN_BLOCKS)
         const float cull = cull_dist(best.t);
         while (sp > 0) {
           --sp;
-          int32_t x;
-          float tx;
-          if (sp < kShortStack) {
-            x = s_node[sp * kTraceThreads + tid];
-            tx = s_t[sp * kTraceThreads + tid];
-          } else {
-            x = l_node[sp - kShortStack];
-            tx = l_t[sp - kShortStack];
-          }
-          if (!(tx > cull)) return x;
+          const uint2 e = sp < kShortStack ? s_stk[sp * kTraceThreads] : l_stk[sp - kShortStack];
+          if (!(__uint_as_float(e.y) > cull)) return (int32_t)e.x;
         }
         return LT_LINK_EXIT;
       };
       auto push = [&](int32_t x, float tx) {
-        if (sp < kShortStack) {
-          s_node[sp * kTraceThreads + tid] = x;
-          s_t[sp * kTraceThreads + tid] = tx;
-        } else {
-          l_node[sp - kShortStack] = x;
-          l_t[sp - kShortStack] = tx;
-        }
+        const uint2 e = make_uint2((uint32_t)x, __float_as_uint(tx));
+        if (sp < kShortStack)
+          s_stk[sp * kTraceThreads] = e;
+        else
+          l_stk[sp - kShortStack] = e;
         ++sp;
       };
       // ---- wide nodes: descend nearest-first until a leaf or a dead end;
@@ -338,9 +327,17 @@ __global__ void __launch_bounds__(kTraceThreads, LT_TRACE_MIN_BLOCKS)
       while (node >= 0) {
         const Hits4 h = LT_VISIT4(sc.wnodes + LT_NODE_F4 * (int64_t)node, rs, t_min, best.t);
         if (COUNT) nn += 4;
-        if (h.k3 < kInf) push(h.l3, h.k3);
-        if (h.k2 < kInf) push(h.l2, h.k2);
-        if (h.k1 < kInf) push(h.l1, h.k1);
+        if (sp <= kShortStack - 3) {
+          // common case: all three fit in shared memory (predicated stores)
+          uint2 *top = s_stk + sp * kTraceThreads;
+          if (h.k3 < kInf) { *top = make_uint2((uint32_t)h.l3, __float_as_uint(h.k3)); top += kTraceThreads; ++sp; }
+          if (h.k2 < kInf) { *top = make_uint2((uint32_t)h.l2, __float_as_uint(h.k2)); top += kTraceThreads; ++sp; }
+          if (h.k1 < kInf) { *top = make_uint2((uint32_t)h.l1, __float_as_uint(h.k1)); top += kTraceThreads; ++sp; }
+        } else {
+          if (h.k3 < kInf) push(h.l3, h.k3);
+          if (h.k2 < kInf) push(h.l2, h.k2);
+          if (h.k1 < kInf) push(h.l1, h.k1);
+        }
         node = h.k0 < kInf ? h.l0 : pop();
       }
       // ---- leaf: its triangles, then the next stack entry

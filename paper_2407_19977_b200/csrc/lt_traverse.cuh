@@ -216,6 +216,20 @@ __device__ __forceinline__ float near_far(float n, float f, float o, float inv, 
   return (n - o) * inv;
 }
 
+// (p0 - o) * inv and (p1 - o) * inv as one FADD2 + one FMUL2.
+__device__ __forceinline__ void plane2(float p0, float p1, float o, float inv, float &t0,
+                                       float &t1) {
+  unsigned long long p, r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(p) : "f"(p0), "f"(p1));
+  asm("{\n\t.reg .b64 ob, ib, d;\n\t"
+      "mov.b64 ob, {%2, %2};\n\t"
+      "mov.b64 ib, {%3, %3};\n\t"
+      "sub.rn.f32x2 d, %1, ob;\n\t"
+      "mul.rn.f32x2 %0, d, ib;\n\t}"
+      : "=l"(r) : "l"(p), "f"(o), "f"(inv));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(t0), "=f"(t1) : "l"(r));
+}
+
 __device__ __forceinline__ Hits4 visit4o(const float4 *__restrict__ np, const RaySlab &rs,
                                          float t_min, float t_max) {
   const float kInf = __int_as_float(0x7f800000);
@@ -234,6 +248,37 @@ __device__ __forceinline__ Hits4 visit4o(const float4 *__restrict__ np, const Ra
 #endif
   const int4 ln = __ldg(reinterpret_cast<const int4 *>(np + LT_NODE_LINKS));
   Hits4 h;
+#ifdef LT_PACKED_SLAB
+  // sm_100 packed fp32 (FADD2 / FMUL2, one issue slot per two children;
+  // the scalar origin / inverse are broadcast operands): same IEEE roundings
+  // as the scalar form.
+  float a0x, a1x, a2x, a3x, b0x, b1x, b2x, b3x;
+  float a0y, a1y, a2y, a3y, b0y, b1y, b2y, b3y;
+  float a0z, a1z, a2z, a3z, b0z, b1z, b2z, b3z;
+  plane2(nx.x, nx.y, rs.o.x, rs.inv.x, a0x, a1x);
+  plane2(nx.z, nx.w, rs.o.x, rs.inv.x, a2x, a3x);
+  plane2(fx.x, fx.y, rs.o.x, rs.inv.x, b0x, b1x);
+  plane2(fx.z, fx.w, rs.o.x, rs.inv.x, b2x, b3x);
+  plane2(ny.x, ny.y, rs.o.y, rs.inv.y, a0y, a1y);
+  plane2(ny.z, ny.w, rs.o.y, rs.inv.y, a2y, a3y);
+  plane2(fy.x, fy.y, rs.o.y, rs.inv.y, b0y, b1y);
+  plane2(fy.z, fy.w, rs.o.y, rs.inv.y, b2y, b3y);
+  plane2(nz.x, nz.y, rs.o.z, rs.inv.z, a0z, a1z);
+  plane2(nz.z, nz.w, rs.o.z, rs.inv.z, a2z, a3z);
+  plane2(fz.x, fz.y, rs.o.z, rs.inv.z, b0z, b1z);
+  plane2(fz.z, fz.w, rs.o.z, rs.inv.z, b2z, b3z);
+#define LT_CHILD2(K, I)                                                           \
+  {                                                                               \
+    const float tn = fmax3f(a##I##x, a##I##y, fmaxf(a##I##z, t_min));             \
+    const float tf = fmin3f(b##I##x, b##I##y, fminf(b##I##z, t_max));             \
+    h.K = tn <= tf * LT_SLAB_WIDEN ? tn : kInf;                                   \
+  }
+  LT_CHILD2(k0, 0)
+  LT_CHILD2(k1, 1)
+  LT_CHILD2(k2, 2)
+  LT_CHILD2(k3, 3)
+#undef LT_CHILD2
+#else
 #define LT_CHILD(K, C)                                                            \
   {                                                                               \
     float fx_, fy_, fz_;                                                          \
@@ -249,15 +294,24 @@ __device__ __forceinline__ Hits4 visit4o(const float4 *__restrict__ np, const Ra
   LT_CHILD(k2, z)
   LT_CHILD(k3, w)
 #undef LT_CHILD
+#endif
   h.l0 = ln.x;
   h.l1 = ln.y;
   h.l2 = ln.z;
   h.l3 = ln.w;
+#ifdef LT_PARTIAL_SORT
+  // nearest first; the other three only partially ordered (one comparator less)
+  cswap(h.k0, h.l0, h.k1, h.l1);
+  cswap(h.k2, h.l2, h.k3, h.l3);
+  cswap(h.k0, h.l0, h.k2, h.l2);
+  cswap(h.k1, h.l1, h.k2, h.l2);
+#else
   cswap(h.k0, h.l0, h.k1, h.l1);
   cswap(h.k2, h.l2, h.k3, h.l3);
   cswap(h.k0, h.l0, h.k2, h.l2);
   cswap(h.k1, h.l1, h.k3, h.l3);
   cswap(h.k1, h.l1, h.k2, h.l2);
+#endif
   return h;
 }
 
