@@ -342,7 +342,7 @@ __global__ void __launch_bounds__(kTraceThreads, LT_TRACE_MIN_BLOCKS)
       }
       // ---- leaf: its triangles, then the next stack entry
       if (node != LT_LINK_EXIT) {
-        leaf_test<COUNT>(sc, ~(int64_t)node, o, d, t_min, best, best_orig, nt);
+        leaf_test<COUNT>(sc, ~(uint32_t)node, o, d, t_min, best, best_orig, nt);
         node = pop();
       }
       if (node == LT_LINK_EXIT) {

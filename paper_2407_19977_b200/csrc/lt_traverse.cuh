@@ -136,7 +136,7 @@ __device__ __forceinline__ void mt_test(f3 o, f3 d, float t_min, float4 t0, floa
 // All triangles of the leaf starting at leaf-order position `first` (the
 // last one carries the end-of-leaf flag).
 template <bool COUNT>
-__device__ __forceinline__ void leaf_test(const SceneView &sc, int64_t k, f3 o, f3 d, float t_min,
+__device__ __forceinline__ void leaf_test(const SceneView &sc, uint32_t k, f3 o, f3 d, float t_min,
                                           HitRec &best, int32_t &best_orig, int &tests) {
   while (true) {
 #ifdef LT_TRI_W256
@@ -144,12 +144,12 @@ __device__ __forceinline__ void leaf_test(const SceneView &sc, int64_t k, f3 o, 
     asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
         : "=f"(t0.x), "=f"(t0.y), "=f"(t0.z), "=f"(t0.w), "=f"(t1.x), "=f"(t1.y), "=f"(t1.z),
           "=f"(t1.w)
-        : "l"(sc.tris + LT_TRI_F4 * k));
+        : "l"(sc.tris + LT_TRI_F4 * (size_t)k));
 #else
-    const float4 t0 = __ldg(&sc.tris[LT_TRI_F4 * k]);
-    const float4 t1 = __ldg(&sc.tris[LT_TRI_F4 * k + 1]);
+    const float4 t0 = __ldg(&sc.tris[LT_TRI_F4 * (size_t)k]);
+    const float4 t1 = __ldg(&sc.tris[LT_TRI_F4 * (size_t)k + 1]);
 #endif
-    const float4 t2 = __ldg(&sc.tris[LT_TRI_F4 * k + 2]);
+    const float4 t2 = __ldg(&sc.tris[LT_TRI_F4 * (size_t)k + 2]);
     if (COUNT) ++tests;
     mt_test(o, d, t_min, t0, t1, t2, (int32_t)k, best, best_orig);
     if (__float_as_int(t1.w) != 0) break;
@@ -230,6 +230,17 @@ __device__ __forceinline__ void plane2(float p0, float p1, float o, float inv, f
   asm("mov.b64 {%0, %1}, %2;" : "=f"(t0), "=f"(t1) : "l"(r));
 }
 
+// (a * s, b * s) as one FMUL2.
+__device__ __forceinline__ void scale2(float a, float b, float sc, float &ra, float &rb) {
+  unsigned long long p, r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(p) : "f"(a), "f"(b));
+  asm("{\n\t.reg .b64 sb;\n\t"
+      "mov.b64 sb, {%2, %2};\n\t"
+      "mul.rn.f32x2 %0, %1, sb;\n\t}"
+      : "=l"(r) : "l"(p), "f"(sc));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(ra), "=f"(rb) : "l"(r));
+}
+
 __device__ __forceinline__ Hits4 visit4o(const float4 *__restrict__ np, const RaySlab &rs,
                                          float t_min, float t_max) {
   const float kInf = __int_as_float(0x7f800000);
@@ -267,17 +278,19 @@ __device__ __forceinline__ Hits4 visit4o(const float4 *__restrict__ np, const Ra
   plane2(nz.z, nz.w, rs.o.z, rs.inv.z, a2z, a3z);
   plane2(fz.x, fz.y, rs.o.z, rs.inv.z, b0z, b1z);
   plane2(fz.z, fz.w, rs.o.z, rs.inv.z, b2z, b3z);
-#define LT_CHILD2(K, I)                                                           \
-  {                                                                               \
-    const float tn = fmax3f(a##I##x, a##I##y, fmaxf(a##I##z, t_min));             \
-    const float tf = fmin3f(b##I##x, b##I##y, fminf(b##I##z, t_max));             \
-    h.K = tn <= tf * LT_SLAB_WIDEN ? tn : kInf;                                   \
-  }
-  LT_CHILD2(k0, 0)
-  LT_CHILD2(k1, 1)
-  LT_CHILD2(k2, 2)
-  LT_CHILD2(k3, 3)
-#undef LT_CHILD2
+  const float tn0 = fmax3f(a0x, a0y, fmaxf(a0z, t_min));
+  const float tn1 = fmax3f(a1x, a1y, fmaxf(a1z, t_min));
+  const float tn2 = fmax3f(a2x, a2y, fmaxf(a2z, t_min));
+  const float tn3 = fmax3f(a3x, a3y, fmaxf(a3z, t_min));
+  float tf0, tf1, tf2, tf3;
+  scale2(fmin3f(b0x, b0y, fminf(b0z, t_max)), fmin3f(b1x, b1y, fminf(b1z, t_max)),
+         LT_SLAB_WIDEN, tf0, tf1);
+  scale2(fmin3f(b2x, b2y, fminf(b2z, t_max)), fmin3f(b3x, b3y, fminf(b3z, t_max)),
+         LT_SLAB_WIDEN, tf2, tf3);
+  h.k0 = tn0 <= tf0 ? tn0 : kInf;
+  h.k1 = tn1 <= tf1 ? tn1 : kInf;
+  h.k2 = tn2 <= tf2 ? tn2 : kInf;
+  h.k3 = tn3 <= tf3 ? tn3 : kInf;
 #else
 #define LT_CHILD(K, C)                                                            \
   {                                                                               \
@@ -352,7 +365,7 @@ __device__ __forceinline__ bool occluded(const SceneView &sc, f3 o, f3 d, float 
     }
     if (node == LT_LINK_EXIT) return false;
     int tests = 0;
-    leaf_test<false>(sc, ~(int64_t)node, o, d, t_min, best, best_orig, tests);
+    leaf_test<false>(sc, ~(uint32_t)node, o, d, t_min, best, best_orig, tests);
     if (best.k >= 0) return true;
     if (sp == 0) return false;
     node = stk[--sp];
@@ -409,7 +422,7 @@ __device__ __forceinline__ HitRec traverse(const SceneView &sc, f3 o, f3 d, floa
           }
         }
       }
-      if (node != LT_LINK_EXIT) leaf_test<COUNT>(sc, ~(int64_t)node, o, d, t_min, best,
+      if (node != LT_LINK_EXIT) leaf_test<COUNT>(sc, ~(uint32_t)node, o, d, t_min, best,
                                                  best_orig, tests);
       const float cull = cull_dist(best.t);
       node = LT_LINK_EXIT;
