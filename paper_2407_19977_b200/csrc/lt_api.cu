@@ -854,6 +854,8 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
   s->octant_sort = os_env ? os_env[0] == '1' : true;
   const char *rf = std::getenv("LT_REFILL");
   v.refill_min = std::max(1, std::min(32, rf ? std::atoi(rf) : 16));
+  const char *lm = std::getenv("LT_LEAF_MIN");
+  v.leaf_min = std::max(1, std::min(33, lm ? std::atoi(lm) : 8));
   return LT_OK;
 }
 

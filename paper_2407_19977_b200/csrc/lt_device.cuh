@@ -104,6 +104,7 @@ struct SceneView {
   int32_t root_link;
   int32_t n_top;        // internal nodes [0, n_top) are BFS-ordered top levels
   int32_t refill_min;   // idle lanes that trigger a warp refill in k_trace
+  int32_t leaf_min;     // lanes at a leaf that trigger the warp's leaf tests
   float root_lo[3], root_hi[3];
   int32_t env_kind;
   int32_t env_w, env_h;

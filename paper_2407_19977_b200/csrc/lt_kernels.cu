@@ -232,6 +232,12 @@ __global__ void k_gather_explicit(PathArrays pa, int64_t n, double *__restrict__
 //    it finishes, the warp refills its idle lanes from the queue with one
 //    atomic (ballot + popc ranks) once >= sc.refill_min lanes are idle, so
 //    short rays do not leave lanes dark while long ones finish;
+//  * one loop iteration = refill check, up to LT_NODE_STEPS inner-node
+//    visits per lane, then the leaf phase: lanes that reached a leaf wait
+//    until >= sc.leaf_min of the warp have (or no lane is left at an inner
+//    node) and test their triangles together.  The classic while-while form
+//    (leaves only once every lane has one) left ~12 of 32 lanes active in
+//    the node visits (profiles/r01_v16_trace_source.txt);
 //  * traversal stack: the first kShortStack entries of every lane live in
 //    shared memory, laid out [depth][thread] (conflict-free), deeper ones in
 //    local memory;
@@ -302,53 +308,62 @@ __global__ void __launch_bounds__(kTraceThreads, LT_TRACE_MIN_BLOCKS)
       if (exhausted) break;
       continue;
     }
-    if (q >= 0) {
-      // pop the next stack entry not culled by the current best t (bvh.py:389)
-      auto pop = [&]() -> int32_t {
-        const float cull = cull_dist(best.t);
-        while (sp > 0) {
-          --sp;
-          const uint2 e = sp < kShortStack ? s_stk[sp * kTraceThreads] : l_stk[sp - kShortStack];
-          if (!(__uint_as_float(e.y) > cull)) return (int32_t)e.x;
-        }
-        return LT_LINK_EXIT;
-      };
-      auto push = [&](int32_t x, float tx) {
-        const uint2 e = make_uint2((uint32_t)x, __float_as_uint(tx));
-        if (sp < kShortStack)
-          s_stk[sp * kTraceThreads] = e;
-        else
-          l_stk[sp - kShortStack] = e;
-        ++sp;
-      };
-      // ---- wide nodes: descend nearest-first until a leaf or a dead end;
-      // the other hit children go on the stack farthest first
-      const float kInf = __int_as_float(0x7f800000);
-      while (node >= 0) {
-        const Hits4 h = LT_VISIT4(sc.wnodes + LT_NODE_F4 * (int64_t)node, rs, t_min, best.t);
-        if (COUNT) nn += 4;
-        if (sp <= kShortStack - 3) {
-          // common case: all three fit in shared memory (predicated stores)
-          uint2 *top = s_stk + sp * kTraceThreads;
-          if (h.k3 < kInf) { *top = make_uint2((uint32_t)h.l3, __float_as_uint(h.k3)); top += kTraceThreads; ++sp; }
-          if (h.k2 < kInf) { *top = make_uint2((uint32_t)h.l2, __float_as_uint(h.k2)); top += kTraceThreads; ++sp; }
-          if (h.k1 < kInf) { *top = make_uint2((uint32_t)h.l1, __float_as_uint(h.k1)); top += kTraceThreads; ++sp; }
-        } else {
-          if (h.k3 < kInf) push(h.l3, h.k3);
-          if (h.k2 < kInf) push(h.l2, h.k2);
-          if (h.k1 < kInf) push(h.l1, h.k1);
-        }
-        node = h.k0 < kInf ? h.l0 : pop();
+    // pop the next stack entry not culled by the current best t (bvh.py:389)
+    auto pop = [&]() -> int32_t {
+      const float cull = cull_dist(best.t);
+      while (sp > 0) {
+        --sp;
+        const uint2 e = sp < kShortStack ? s_stk[sp * kTraceThreads] : l_stk[sp - kShortStack];
+        if (!(__uint_as_float(e.y) > cull)) return (int32_t)e.x;
       }
-      // ---- leaf: its triangles, then the next stack entry
-      if (node != LT_LINK_EXIT) {
+      return LT_LINK_EXIT;
+    };
+    auto push = [&](int32_t x, float tx) {
+      const uint2 e = make_uint2((uint32_t)x, __float_as_uint(tx));
+      if (sp < kShortStack)
+        s_stk[sp * kTraceThreads] = e;
+      else
+        l_stk[sp - kShortStack] = e;
+      ++sp;
+    };
+    const float kInf = __int_as_float(0x7f800000);
+    // ---- one wide node per active lane: descend nearest-first; the other
+    // hit children go on the stack farthest first
+#ifndef LT_NODE_STEPS
+#define LT_NODE_STEPS 3
+#endif
+#pragma unroll 1
+    for (int step = 0; step < LT_NODE_STEPS && q >= 0 && node >= 0; ++step) {
+      const Hits4 h = LT_VISIT4(sc.wnodes + LT_NODE_F4 * (int64_t)node, rs, t_min, best.t);
+      if (COUNT) nn += 4;
+      if (sp <= kShortStack - 3) {
+        // common case: all three fit in shared memory (predicated stores)
+        uint2 *top = s_stk + sp * kTraceThreads;
+        if (h.k3 < kInf) { *top = make_uint2((uint32_t)h.l3, __float_as_uint(h.k3)); top += kTraceThreads; ++sp; }
+        if (h.k2 < kInf) { *top = make_uint2((uint32_t)h.l2, __float_as_uint(h.k2)); top += kTraceThreads; ++sp; }
+        if (h.k1 < kInf) { *top = make_uint2((uint32_t)h.l1, __float_as_uint(h.k1)); top += kTraceThreads; ++sp; }
+      } else {
+        if (h.k3 < kInf) push(h.l3, h.k3);
+        if (h.k2 < kInf) push(h.l2, h.k2);
+        if (h.k1 < kInf) push(h.l1, h.k1);
+      }
+      node = h.k0 < kInf ? h.l0 : pop();
+    }
+    // ---- leaves: lanes that reached one wait until enough of the warp has
+    // (or no lane is still at an inner node), then test their triangles
+    // together, so inner-node iterations keep more lanes busy
+    const bool at_leaf = q >= 0 && node < 0 && node != LT_LINK_EXIT;
+    const unsigned leaf_mask = __ballot_sync(kFull, at_leaf);
+    if (leaf_mask && (__popc(leaf_mask) >= sc.leaf_min ||
+                      __ballot_sync(kFull, q >= 0 && node >= 0) == 0)) {
+      if (at_leaf) {
         leaf_test<COUNT>(sc, ~(uint32_t)node, o, d, t_min, best, best_orig, nt);
         node = pop();
       }
-      if (node == LT_LINK_EXIT) {
-        __stcs(&hits[q], make_float4(best.t, best.u, best.v, __int_as_float(best.k)));
-        q = -1;
-      }
+    }
+    if (q >= 0 && node == LT_LINK_EXIT) {
+      __stcs(&hits[q], make_float4(best.t, best.u, best.v, __int_as_float(best.k)));
+      q = -1;
     }
   }
   if (COUNT) {
