@@ -441,6 +441,11 @@ __global__ void __launch_bounds__(kShadeThreads, LT_SHADE_MIN_BLOCKS)
   const bool primary = sa.primary != 0;
   const int n = *count_in;
   const int lane = threadIdx.x & 31;
+  __shared__ int s_cnt[LT_DIR_BINS], s_off[LT_DIR_BINS], s_base;
+  if (sa.octant_sort) {
+    for (int b = threadIdx.x; b < LT_DIR_BINS; b += blockDim.x) s_cnt[b] = 0;
+    __syncthreads();
+  }
   for (int base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
     const int q = base + threadIdx.x;
     bool emit = false;
@@ -577,9 +582,8 @@ __global__ void __launch_bounds__(kShadeThreads, LT_SHADE_MIN_BLOCKS)
       // of the next queue per block, laid out bin by bin (counting sort), so
       // a trace warp fetches rays with nearby origins and similar
       // directions (higher SIMT efficiency for incoherent bounces)
-      __shared__ int s_cnt[LT_DIR_BINS], s_off[LT_DIR_BINS], s_base;
-      for (int b = threadIdx.x; b < LT_DIR_BINS; b += blockDim.x) s_cnt[b] = 0;
-      __syncthreads();
+      // (s_cnt is zeroed before the loop and re-zeroed by thread 0 once it
+      // has read the counts: two barriers per block iteration)
       int bin = 0, rank = 0;
       if (emit) {
         bin = dir_bin(out_d);
@@ -591,6 +595,7 @@ __global__ void __launch_bounds__(kShadeThreads, LT_SHADE_MIN_BLOCKS)
         for (int b = 0; b < LT_DIR_BINS; ++b) {
           s_off[b] = run;
           run += s_cnt[b];
+          s_cnt[b] = 0;
         }
         s_base = run ? atomicAdd(count_out, run) : 0;
       }
