@@ -9,7 +9,7 @@ namespace lt {
 
 constexpr int kTraceThreads = 128;
 #ifndef LT_SHADE_THREADS
-#define LT_SHADE_THREADS 256
+#define LT_SHADE_THREADS 128
 #endif
 constexpr int kShadeThreads = LT_SHADE_THREADS;
 #ifndef LT_SHORT_STACK
@@ -20,7 +20,7 @@ constexpr int kShadeThreads = LT_SHADE_THREADS;
 #define LT_TRACE_MIN_BLOCKS 9
 #endif
 #ifndef LT_SHADE_MIN_BLOCKS
-#define LT_SHADE_MIN_BLOCKS 4
+#define LT_SHADE_MIN_BLOCKS 8
 #endif
 // near/far plane arrays picked by the ray's direction signs (no per-axis
 // min/max in the slab test; profiles/r01_trace_variants.jsonl); build with
