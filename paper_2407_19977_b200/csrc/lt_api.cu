@@ -58,7 +58,10 @@ namespace {
 // lanes while the rest of the GPU idles): 4M -> 64M paths took the C4 step
 // from 452 to 277 ms (profiles/r01_batch_sweep.jsonl).  128 B of queues and
 // path state per path: 64M paths = 8 GB, bounded by a quarter of free HBM.
-constexpr int64_t kMaxBatchPaths = int64_t(1) << 26;
+#ifndef LT_MAX_BATCH_LOG2
+#define LT_MAX_BATCH_LOG2 26
+#endif
+constexpr int64_t kMaxBatchPaths = int64_t(1) << LT_MAX_BATCH_LOG2;
 
 // Device buffer.  With `ast` set the memory comes stream-ordered from the
 // device's default mempool (cudaMallocAsync / cudaFreeAsync on `ast`), so a
