@@ -59,7 +59,7 @@ namespace {
 // from 452 to 277 ms (profiles/r01_batch_sweep.jsonl).  128 B of queues and
 // path state per path: 64M paths = 8 GB, bounded by a quarter of free HBM.
 #ifndef LT_MAX_BATCH_LOG2
-#define LT_MAX_BATCH_LOG2 26
+#define LT_MAX_BATCH_LOG2 28
 #endif
 constexpr int64_t kMaxBatchPaths = int64_t(1) << LT_MAX_BATCH_LOG2;
 
