@@ -194,8 +194,12 @@ __device__ __forceinline__ f3 env_radiance(const SceneView &sc, f3 d) {
   float ax = fx - x0f, ay = fy - y0f;
   int x0 = (int)x0f, y0 = (int)y0f;
   int x1 = x0 + 1, y1 = y0 + 1;
-  x0 = ((x0 % sc.env_w) + sc.env_w) % sc.env_w;
-  x1 = ((x1 % sc.env_w) + sc.env_w) % sc.env_w;
+  // wrap around the seam: u in [0, 1] puts x0 in [-1, w - 1] and x1 in
+  // [0, w]; the integer modulo (~20 instructions each) only for anything else
+  x0 += x0 < 0 ? sc.env_w : 0;
+  x1 -= x1 >= sc.env_w ? sc.env_w : 0;
+  if ((unsigned)x0 >= (unsigned)sc.env_w) x0 = ((x0 % sc.env_w) + sc.env_w) % sc.env_w;
+  if ((unsigned)x1 >= (unsigned)sc.env_w) x1 = ((x1 % sc.env_w) + sc.env_w) % sc.env_w;
   y0 = min(max(y0, 0), sc.env_h - 1);
   y1 = min(max(y1, 0), sc.env_h - 1);
   float4 c00 = __ldg(&sc.env_map[y0 * sc.env_w + x0]);

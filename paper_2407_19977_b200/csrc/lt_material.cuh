@@ -53,17 +53,28 @@ __device__ __forceinline__ void onb(f3 n, f3 &t, f3 &b) {
   b = f3{n.y * tz - n.z * ty, n.z * tx - n.x * tz, n.x * ty - n.y * tx};
 }
 
-// _cosine_sample (material.py:264-274); sincospi(2u) == sincos(2 pi u)
-__device__ __forceinline__ f3 cosine_sample(f3 n, float u1, float u2) {
+// The sampling frame shared by every lobe of one scatter: the tangent frame
+// of n (_onb) and sincos(2 pi u2) -- computed once, before the lobe branch,
+// so a warp whose lanes pick different lobes runs them convergently.
+struct SampleFrame {
   f3 t, b;
-  onb(n, t, b);
-  float r = sqrtf(u1);
   float sphi, cphi;
-  sincospif(2.f * u2, &sphi, &cphi);
-  float x = r * cphi, y = r * sphi;
+};
+
+__device__ __forceinline__ SampleFrame sample_frame(f3 n, float u2) {
+  SampleFrame F;
+  onb(n, F.t, F.b);
+  sincospif(2.f * u2, &F.sphi, &F.cphi);  // sincospi(2u) == sincos(2 pi u)
+  return F;
+}
+
+// _cosine_sample (material.py:264-274)
+__device__ __forceinline__ f3 cosine_sample(const SampleFrame &F, f3 n, float u1) {
+  float r = sqrtf(u1);
+  float x = r * F.cphi, y = r * F.sphi;
   float z = sqrtf(fmaxf(0.f, 1.f - u1));
-  return f3{x * t.x + y * b.x + z * n.x, x * t.y + y * b.y + z * n.y,
-            x * t.z + y * b.z + z * n.z};
+  return f3{x * F.t.x + y * F.b.x + z * n.x, x * F.t.y + y * F.b.y + z * n.y,
+            x * F.t.z + y * F.b.z + z * n.z};
 }
 
 // _ggx_sample_half (material.py:277-290).  The reference's
@@ -71,17 +82,13 @@ __device__ __forceinline__ f3 cosine_sample(f3 n, float u1, float u2) {
 // (a2-1 rounds to -1 for a2 < 2^-25, and 1-ct^2 loses the tangent near the
 // mirror direction); the same angle through tan^2 = a2 u1/(1-u1) has no
 // cancellation (1-u1 is exact for u1 >= 0.5 by Sterbenz).
-__device__ __forceinline__ f3 ggx_sample_half(f3 n, float a2, float u1, float u2) {
-  f3 t, b;
-  onb(n, t, b);
+__device__ __forceinline__ f3 ggx_sample_half(const SampleFrame &F, f3 n, float a2, float u1) {
   float t2 = a2 * u1 / (1.f - u1);
   float ct = 1.f / sqrtf(1.f + t2);
   float st = sqrtf(t2) * ct;
-  float sphi, cphi;
-  sincospif(2.f * u2, &sphi, &cphi);
-  float x = st * cphi, y = st * sphi;
-  return f3{x * t.x + y * b.x + ct * n.x, x * t.y + y * b.y + ct * n.y,
-            x * t.z + y * b.z + ct * n.z};
+  float x = st * F.cphi, y = st * F.sphi;
+  return f3{x * F.t.x + y * F.b.x + ct * n.x, x * F.t.y + y * F.b.y + ct * n.y,
+            x * F.t.z + y * F.b.z + ct * n.z};
 }
 
 // _p_spec_select (material.py:196-213)
@@ -160,13 +167,13 @@ __device__ __forceinline__ float pdf_core(f3 wo, f3 wi, f3 n, const GpuMaterial 
 
 // reference branch of _sample_core (material.py:293-351)
 __device__ __forceinline__ bool sample_reference(f3 wo, f3 n, const GpuMaterial &mt,
-                                                 float opaque, float u_lobe, float u1, float u2,
-                                                 f3 &wi, f3 &wgt) {
+                                                 float opaque, float u_lobe, float u1,
+                                                 const SampleFrame &F, f3 &wi, f3 &wgt) {
   float no = dot(n, wo);
   if ((mt.flags & MAT_DIFFUSE_ONLY) && opaque == 1.f) {
     // diffuse-only: f cos / pdf collapses to the albedo exactly
     if (mt.bw <= 0.f || no <= 0.f) return false;
-    wi = cosine_sample(n, u1, u2);
+    wi = cosine_sample(F, n, u1);
     float ni = dot(n, wi);
     if (ni <= 0.f) return false;
     wgt = f3{mt.bw * mt.bc[0], mt.bw * mt.bc[1], mt.bw * mt.bc[2]};
@@ -182,13 +189,13 @@ __device__ __forceinline__ bool sample_reference(f3 wo, f3 n, const GpuMaterial 
     use_ggx = u_d < p_spec;
   }
   if (use_ggx) {
-    f3 h = ggx_sample_half(n, mt.a2, u1, u2);
+    f3 h = ggx_sample_half(F, n, mt.a2, u1);
     float oh = dot(wo, h);
     if (oh <= 0.f) return false;
     float k = 2.f * oh;
     wi = f3{k * h.x - wo.x, k * h.y - wo.y, k * h.z - wo.z};
   } else {
-    wi = cosine_sample(n, u1, u2);
+    wi = cosine_sample(F, n, u1);
   }
   float ni = dot(n, wi);
   if (ni <= 0.f) return false;
@@ -202,8 +209,9 @@ __device__ __forceinline__ bool sample_reference(f3 wo, f3 n, const GpuMaterial 
 
 // extension: rough dielectric interface (see oracle oc_sample_glass)
 __device__ __forceinline__ bool sample_glass(f3 wo, f3 n, const GpuMaterial &mt, bool front,
-                                             float u_sel, float u1, float u2, f3 &wi, f3 &wgt) {
-  f3 h = ggx_sample_half(n, mt.a2, u1, u2);
+                                             float u_sel, float u1, const SampleFrame &fr, f3 &wi,
+                                             f3 &wgt) {
+  f3 h = ggx_sample_half(fr, n, mt.a2, u1);
   float c = dot(wo, h), no = dot(n, wo), nh = dot(n, h);
   if (c <= 0.f || no <= 0.f || nh <= 0.f) return false;
   float eta = front ? 1.f / mt.ior : mt.ior;
@@ -238,8 +246,8 @@ __device__ __forceinline__ bool sample_glass(f3 wo, f3 n, const GpuMaterial &mt,
 
 // extension: clear-coat GGX lobe (see oracle oc_sample_coat)
 __device__ __forceinline__ bool sample_coat(f3 wo, f3 n, const GpuMaterial &mt, float p_coat,
-                                            float u1, float u2, f3 &wi, f3 &wgt) {
-  f3 h = ggx_sample_half(n, mt.ca2, u1, u2);
+                                            float u1, const SampleFrame &F, f3 &wi, f3 &wgt) {
+  f3 h = ggx_sample_half(F, n, mt.ca2, u1);
   float oh = dot(wo, h);
   if (oh <= 0.f) return false;
   float k = 2.f * oh;
@@ -262,8 +270,9 @@ __device__ __forceinline__ bool sample_coat(f3 wo, f3 n, const GpuMaterial &mt, 
 __device__ __forceinline__ bool sample_material(f3 wo, f3 n, const GpuMaterial &mt, bool front,
                                                 float u_lobe, float u1, float u2, f3 &wi,
                                                 f3 &wgt) {
+  const SampleFrame F = sample_frame(n, u2);
   if (!(mt.flags & (MAT_COAT | MAT_GLASS)))
-    return sample_reference(wo, n, mt, 1.f, u_lobe, u1, u2, wi, wgt);
+    return sample_reference(wo, n, mt, 1.f, u_lobe, u1, F, wi, wgt);
   float under = 1.f;
   if (mt.flags & MAT_COAT) {
     float no = dot(n, wo);
@@ -271,7 +280,7 @@ __device__ __forceinline__ bool sample_material(f3 wo, f3 n, const GpuMaterial &
     float fc = mt.f0c + (1.f - mt.f0c) * pow5f(1.f - no);
     fc = fminf(fmaxf(fc, 0.05f), 0.95f);
     float p_coat = mt.cw * fc;
-    if (u_lobe < p_coat) return sample_coat(wo, n, mt, p_coat, u1, u2, wi, wgt);
+    if (u_lobe < p_coat) return sample_coat(wo, n, mt, p_coat, u1, F, wi, wgt);
     u_lobe = (u_lobe - p_coat) / (1.f - p_coat);
     under = (1.f - mt.cw * mt.cfbar) / (1.f - p_coat);
   }
@@ -279,14 +288,14 @@ __device__ __forceinline__ bool sample_material(f3 wo, f3 n, const GpuMaterial &
   if (mt.flags & MAT_GLASS) {
     float lo = mt.m, hi = mt.m + (1.f - mt.m) * mt.tw;
     if (u_lobe >= lo && u_lobe < hi) {
-      ok = sample_glass(wo, n, mt, front, (u_lobe - lo) / (hi - lo), u1, u2, wi, wgt);
+      ok = sample_glass(wo, n, mt, front, (u_lobe - lo) / (hi - lo), u1, F, wi, wgt);
     } else {
       float u_ref = u_lobe;
       if (u_lobe >= hi) u_ref = fmaxf(mt.m + (u_lobe - hi) / (1.f - hi) * (1.f - mt.m), mt.m);
-      ok = sample_reference(wo, n, mt, 1.f - mt.tw, u_ref, u1, u2, wi, wgt);
+      ok = sample_reference(wo, n, mt, 1.f - mt.tw, u_ref, u1, F, wi, wgt);
     }
   } else {
-    ok = sample_reference(wo, n, mt, 1.f, u_lobe, u1, u2, wi, wgt);
+    ok = sample_reference(wo, n, mt, 1.f, u_lobe, u1, F, wi, wgt);
   }
   if (ok && (mt.flags & MAT_COAT)) {
     wgt.x *= under * (1.f + (mt.cc[0] - 1.f) * mt.cw);
