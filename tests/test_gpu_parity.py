@@ -257,6 +257,25 @@ def test_chunking_batching_and_sharding_are_bit_identical():
     assert np.array_equal(plain, nosmem)
 
 
+@pytest.mark.parametrize("knobs", [{"LT_LEAF_MIN": "1"}, {"LT_LEAF_MIN": "33"},
+                                   {"LT_REFILL": "1"}, {"LT_REFILL": "32", "LT_LEAF_MIN": "4"},
+                                   {"LT_LANES": "1"}, {"LT_OCTANT_SORT": "0"}])
+def test_traversal_schedule_does_not_change_results(knobs, monkeypatch):
+    """The warp scheduling of k_trace (leaf-phase threshold, refill
+    threshold), the lane count and the queue ordering change which lane
+    traces which ray and when -- never a result: closest hits are a
+    lexicographic minimum over (t, triangle index) and per-pixel samples
+    accumulate in index order (scene knobs are read at scene creation)."""
+    m = lb()
+    g = golden_scene("sphere20k")
+    st = m.RenderSettings(samples_per_pixel=5, max_depth=6, seed=11)
+    plain = m.render_progressive(device_scene(g), st).image
+    for k, v in knobs.items():
+        monkeypatch.setenv(k, v)
+    other = m.render_progressive(device_scene(g), st).image
+    assert np.array_equal(plain, other)
+
+
 @pytest.mark.parametrize("size", [(17, 13), (1, 1), (3, 50)])
 def test_odd_image_sizes_against_oracle(size):
     """Partial 4x4 tiles of the tile-ordered pixel list (k_pixel_list) and
