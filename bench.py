@@ -399,8 +399,12 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         pin(scene.triangles, ["v0", "v1", "v2", "n0", "n1", "n2", "material_index"])
         pin(bvh, ["bounds_min", "bounds_max", "left_child", "right_child", "first_triangle",
                   "triangle_count", "triangle_order"])
-        h2d = sum(getattr(scene.triangles, nm).nbytes for nm in
-                  ["v0", "v1", "v2", "n0", "n1", "n2", "material_index"])
+        env = scene.environment
+        if getattr(env, "texels", None) is not None:
+            pin(env, ["texels"])  # the HDR sky (float32 texels)
+        h2d = env.texels.nbytes if getattr(env, "texels", None) is not None else 0
+        h2d += sum(getattr(scene.triangles, nm).nbytes for nm in
+                   ["v0", "v1", "v2", "n0", "n1", "n2", "material_index"])
         h2d += sum(getattr(bvh, nm).nbytes for nm in
                    ["bounds_min", "bounds_max", "left_child", "right_child", "first_triangle",
                     "triangle_count", "triangle_order"])

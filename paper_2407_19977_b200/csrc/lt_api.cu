@@ -334,6 +334,19 @@ static int validate_desc(const lt_scene_desc *d) {
       !d->specular_weight || !d->specular_color || !d->specular_roughness ||
       !d->specular_ior || !d->emission_luminance || !d->emission_color)
     return lt_fail(LT_ERR_INVALID, "material arrays must be non-null");
+  if (d->env_kind < LT_ENV_UNIFORM || d->env_kind > LT_ENV_LATLONG)
+    return lt_fail(LT_ERR_INVALID, "unknown environment kind %d", d->env_kind);
+  if (d->env_kind == LT_ENV_LATLONG &&
+      (!d->env_texels || d->env_width < 1 || d->env_height < 1))
+    return lt_fail(LT_ERR_INVALID, "lat-long environment needs texels and a size");
+  return LT_OK;
+}
+
+// The O(n) index checks of a description (material indices, triangle
+// order, child / leaf ranges): scene creation runs them on host threads
+// while the uploads' DMA is in flight, before any kernel reads an index.
+static int validate_indices(const lt_scene_desc *d) {
+  const bool build_here = d->n_nodes == 0;
   const int64_t n = d->n_triangles, nn = d->n_nodes;
   // chunked scans on host threads; the reported failure is the first index,
   // as a sequential scan would report it
@@ -385,11 +398,6 @@ static int validate_desc(const lt_scene_desc *d) {
     return lt_fail(LT_ERR_INVALID, "node %lld: invalid children (%d, %d)", (long long)bn,
                    d->left_child[bn], d->right_child[bn]);
   }
-  if (d->env_kind < LT_ENV_UNIFORM || d->env_kind > LT_ENV_LATLONG)
-    return lt_fail(LT_ERR_INVALID, "unknown environment kind %d", d->env_kind);
-  if (d->env_kind == LT_ENV_LATLONG &&
-      (!d->env_texels || d->env_width < 1 || d->env_height < 1))
-    return lt_fail(LT_ERR_INVALID, "lat-long environment needs texels and a size");
   return LT_OK;
 }
 
@@ -753,6 +761,17 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
       root_hi[a] = d->bounds_max[a];
     }
   }
+  // index checks on host threads while the DMA runs; nothing on the device
+  // has read an index yet (the device build reads only vertices)
+  if (int rc = validate_indices(d)) {
+    if (tri_done) {
+      cudaEventSynchronize(tri_done);
+      cudaEventDestroy(tri_done);
+    }
+    cudaStreamSynchronize(st);
+    return rc;
+  }
+  pt.mark("validate indices (overlaps DMA)");
   s->n_nodes = nn;
   // leaf-end flags of the leaf-ordered triangle stream, on the device
   RET(t_end.alloc(std::max<int64_t>(n, 16), st));

@@ -471,3 +471,33 @@ def test_accumulator_to_u8():
     ref = tonemap_to_u8(acc.mean().cpu().numpy())
     assert img.shape == (g.camera.height, g.camera.width, 3)
     assert np.array_equal(img, ref)
+
+
+def test_scene_index_errors_are_reported():
+    """Out-of-range indices in the scene arrays are rejected by
+    lt_scene_create (checked on host threads while the uploads are in
+    flight) with the first offending index, as a sequential scan reports it,
+    and the device stays usable."""
+    import copy
+    m = lb()
+    g = golden_scene("sphere2k")
+    bad = copy.deepcopy(g.bvh)
+    k = int(np.flatnonzero(bad.triangle_count == 0)[3])
+    bad.left_child = bad.left_child.copy()
+    bad.left_child[k] = len(bad.left_child) + 5
+    with pytest.raises(ValueError, match=f"node {k}: invalid children"):
+        m.DeviceScene(g.scene, bad)
+    bad = copy.deepcopy(g.bvh)
+    leaf = int(np.flatnonzero(bad.triangle_count > 0)[-1])
+    bad.first_triangle = bad.first_triangle.copy()
+    bad.first_triangle[leaf] = len(bad.triangle_order)
+    with pytest.raises(ValueError, match=f"node {leaf}: leaf range"):
+        m.DeviceScene(g.scene, bad)
+    bad = copy.deepcopy(g.bvh)
+    bad.triangle_order = bad.triangle_order.copy()
+    bad.triangle_order[7] = -2
+    with pytest.raises(ValueError, match=r"triangle_order\[7\] = -2"):
+        m.DeviceScene(g.scene, bad)
+    st = m.RenderSettings(samples_per_pixel=2, max_depth=3, seed=1)
+    img = m.render_progressive(device_scene(g), st).image
+    assert np.isfinite(img).all()

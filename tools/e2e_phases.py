@@ -29,6 +29,8 @@ keep = []
 pin(sc.triangles, ["v0", "v1", "v2", "n0", "n1", "n2", "material_index"], keep)
 pin(bvh, ["bounds_min", "bounds_max", "left_child", "right_child", "first_triangle",
           "triangle_count", "triangle_order"], keep)
+if sc.environment.texels is not None:
+    pin(sc.environment, ["texels"], keep)
 st = RenderSettings(samples_per_pixel=256, max_depth=8, rr_start_depth=3, seed=0)
 for it in range(4):
     torch.cuda.synchronize()
