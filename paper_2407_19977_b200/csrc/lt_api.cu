@@ -593,8 +593,8 @@ static int configure_launches(lt_scene *s) {
 
 // Layout of a device-built BVH without a host round trip: the internal
 // binary nodes in index order (prefix sum) for the counter query, and the
-// 4-wide collapse level by level (the host path's greedy expansion; wide
-// nodes numbered breadth first, deterministically by prefix sums).
+// 4-wide collapse (greedy largest-area expansion) in one single-CTA launch,
+// wide nodes numbered breadth first.
 static int device_layout(lt_scene *s, const double *bmin, const double *bmax,
                          const int32_t *left, const int32_t *right, const int32_t *count,
                          int64_t nn, bool root_leaf, TmpBuf &t_perm, TmpBuf &t_new,
@@ -624,29 +624,16 @@ static int device_layout(lt_scene *s, const double *bmin, const double *bmax,
   RET(t_wch.alloc((size_t)std::max<int64_t>(n_internal, 1) * 16, st));
   RET(t_wof.alloc((size_t)std::max<int64_t>(nn, 1) * 4, st));
   if (root_leaf || n_internal == 0) return LT_OK;
-  TmpBuf roots[2], kids, off;
-  for (auto &r : roots) RET(r.alloc((size_t)n_internal * 4, st));
-  RET(kids.alloc((size_t)(n_internal + 1) * 4, st));
-  RET(off.alloc((size_t)(n_internal + 1) * 4, st));
-  CK(cudaMemsetAsync(roots[0].p, 0, 4, st));  // the root (binary node 0)
-  int32_t n_roots = 1, base = 0;
-  int cur = 0;
-  while (n_roots > 0) {
-    launch_collapse_level(bmin, bmax, left, right, count, roots[cur].as<int32_t>(), n_roots, base,
-                          t_wch.as<int32_t>(), t_wof.as<int32_t>(), kids.as<int32_t>(), st);
-    CK(cudaMemsetAsync(kids.as<int32_t>() + n_roots, 0, 4, st));
-    CK(cub::DeviceScan::ExclusiveSum(tmp.p, tmp_bytes, kids.as<int32_t>(), off.as<int32_t>(),
-                                     n_roots + 1, st));
-    launch_collapse_emit(t_wch.as<int32_t>(), count, n_roots, base, off.as<int32_t>(),
-                         roots[cur ^ 1].as<int32_t>(), st);
-    int32_t next = 0;
-    CK(cudaMemcpyAsync(&next, off.as<int32_t>() + n_roots, 4, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    base += n_roots;
-    n_roots = next;
-    cur ^= 1;
-  }
-  s->n_wide = base;
+  // breadth-first 4-wide collapse in one single-CTA launch
+  TmpBuf fifo, nw;
+  RET(fifo.alloc((size_t)n_internal * 4, st));
+  RET(nw.alloc(4, st));
+  launch_collapse_all(bmin, bmax, left, right, count, fifo.as<int32_t>(), t_wch.as<int32_t>(),
+                      t_wof.as<int32_t>(), nw.as<int32_t>(), st);
+  int32_t n_wide = 0;
+  CK(cudaMemcpyAsync(&n_wide, nw.p, 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  s->n_wide = n_wide;
   return LT_OK;
 }
 
@@ -781,8 +768,9 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
 
   // --- layout on the device for both paths: the internal binary nodes in
   // index order (prefix sum) for the counter query, and the 4-wide collapse
-  // level by level (greedy largest-area expansion; the host-side version
-  // took ~4.6 ms of host time at 1 M triangles)
+  // (greedy largest-area expansion, one single-CTA launch; the host-side
+  // version took ~4.6 ms of host time at 1 M triangles, the level-by-level
+  // launches ~2 ms of per-level synchronizations)
   RET(device_layout(s, g_bmin, g_bmax, g_left, g_right, g_count, nn, root_leaf, t_perm, t_new,
                     t_wch, t_wof));
   pt.mark("device layout");

@@ -654,20 +654,17 @@ __device__ __forceinline__ double node_area(const double *__restrict__ bmin,
   return dx * dy + dy * dz + dz * dx;
 }
 
-// wide nodes [base, base + n_roots) from their binary roots: children, and
-// the number of internal children (the next level's roots)
-__global__ void k_collapse_level(const double *__restrict__ bmin, const double *__restrict__ bmax,
-                                 const int32_t *__restrict__ left,
-                                 const int32_t *__restrict__ right,
-                                 const int32_t *__restrict__ count,
-                                 const int32_t *__restrict__ roots, int32_t n_roots,
-                                 int32_t base, int32_t *__restrict__ wide_children,
-                                 int32_t *__restrict__ wide_of, int32_t *__restrict__ n_kids) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n_roots) return;
-  const int32_t r = roots[i];
-  wide_of[r] = base + i;
-  int32_t ch[4] = {left[r], right[r], -1, -1};
+// Greedy largest-area expansion of binary node r into up to four children
+// (ch, -1 padded); returns how many of them are internal.
+__device__ __forceinline__ int collapse_node(const double *__restrict__ bmin,
+                                             const double *__restrict__ bmax,
+                                             const int32_t *__restrict__ left,
+                                             const int32_t *__restrict__ right,
+                                             const int32_t *__restrict__ count, int32_t r,
+                                             int32_t (&ch)[4]) {
+  ch[0] = left[r];
+  ch[1] = right[r];
+  ch[2] = ch[3] = -1;
   int nc = 2;
   while (nc < 4) {
     int pick = -1;
@@ -688,26 +685,70 @@ __global__ void k_collapse_level(const double *__restrict__ bmin, const double *
     ++nc;
   }
   int internal = 0;
-  for (int k = 0; k < 4; ++k) {
-    const int32_t c = k < nc ? ch[k] : -1;
-    wide_children[4 * (int64_t)(base + i) + k] = c;
-    internal += (c >= 0 && count[c] == 0) ? 1 : 0;
-  }
-  n_kids[i] = internal;
+  for (int k = 0; k < 4; ++k) internal += (ch[k] >= 0 && count[ch[k]] == 0) ? 1 : 0;
+  return internal;
 }
 
-__global__ void k_collapse_emit(const int32_t *__restrict__ wide_children,
-                                const int32_t *__restrict__ count, int32_t n_roots, int32_t base,
-                                const int32_t *__restrict__ kid_off,
-                                int32_t *__restrict__ next_roots) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n_roots) return;
-  int j = kid_off[i];
-  for (int k = 0; k < 4; ++k) {
-    const int32_t c = wide_children[4 * (int64_t)(base + i) + k];
-    if (c >= 0 && count[c] == 0) next_roots[j++] = c;
+// The whole collapse in one CTA: a FIFO of binary roots processed 1024 at a
+// time (wide node id = FIFO position, i.e. breadth-first, the numbering of
+// the level-by-level launches) -- one launch instead of ~4 per level plus a
+// host synchronization per level.
+__global__ void __launch_bounds__(1024)
+    k_collapse_all(const double *__restrict__ bmin, const double *__restrict__ bmax,
+                   const int32_t *__restrict__ left, const int32_t *__restrict__ right,
+                   const int32_t *__restrict__ count, int32_t *__restrict__ fifo,
+                   int32_t *__restrict__ wide_children, int32_t *__restrict__ wide_of,
+                   int32_t *__restrict__ n_wide) {
+  __shared__ int s_warp[32];
+  __shared__ int s_tail;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    fifo[0] = 0;  // the root (binary node 0)
+    s_tail = 1;
   }
+  __syncthreads();
+  int head = 0;
+  while (head < s_tail) {
+    const int tail = s_tail;
+    const int i = head + tid;
+    int32_t ch[4] = {-1, -1, -1, -1};
+    int kids = 0;
+    if (i < tail) {
+      const int32_t r = fifo[i];
+      wide_of[r] = i;
+      kids = collapse_node(bmin, bmax, left, right, count, r, ch);
+      for (int k = 0; k < 4; ++k) wide_children[4 * (int64_t)i + k] = ch[k];
+    }
+    // block exclusive scan of the internal-children counts
+    int x = kids;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s_warp[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      int w = lane < (int)(blockDim.x >> 5) ? s_warp[lane] : 0;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= o) w += y;
+      }
+      s_warp[lane] = w;  // inclusive over warps
+    }
+    __syncthreads();
+    const int excl = x - kids + (warp ? s_warp[warp - 1] : 0);
+    int j = tail + excl;
+    for (int k = 0; k < 4; ++k)
+      if (ch[k] >= 0 && count[ch[k]] == 0) fifo[j++] = ch[k];
+    const int total = s_warp[(blockDim.x >> 5) - 1];
+    __syncthreads();
+    if (tid == 0) s_tail = tail + total;
+    head = min(head + (int)blockDim.x, tail);
+    __syncthreads();
+  }
+  if (tid == 0) *n_wide = s_tail;
 }
+
 
 void launch_internal_flags(const int32_t *count, int64_t nn, int32_t *flags, cudaStream_t st) {
   if (nn > 0) k_internal_flags<<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(count, nn, flags);
@@ -718,21 +759,12 @@ void launch_internal_scatter(const int32_t *flags, const int32_t *scan, int64_t 
     k_internal_scatter<<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(flags, scan, nn, perm,
                                                                       new_index);
 }
-void launch_collapse_level(const double *bmin, const double *bmax, const int32_t *left,
-                           const int32_t *right, const int32_t *count, const int32_t *roots,
-                           int32_t n_roots, int32_t base, int32_t *wide_children,
-                           int32_t *wide_of, int32_t *n_kids, cudaStream_t st) {
-  if (n_roots > 0)
-    k_collapse_level<<<(n_roots + 127) / 128, 128, 0, st>>>(bmin, bmax, left, right, count, roots,
-                                                            n_roots, base, wide_children, wide_of,
-                                                            n_kids);
-}
-void launch_collapse_emit(const int32_t *wide_children, const int32_t *count, int32_t n_roots,
-                          int32_t base, const int32_t *kid_off, int32_t *next_roots,
-                          cudaStream_t st) {
-  if (n_roots > 0)
-    k_collapse_emit<<<(n_roots + 127) / 128, 128, 0, st>>>(wide_children, count, n_roots, base,
-                                                           kid_off, next_roots);
+void launch_collapse_all(const double *bmin, const double *bmax, const int32_t *left,
+                         const int32_t *right, const int32_t *count, int32_t *fifo,
+                         int32_t *wide_children, int32_t *wide_of, int32_t *n_wide,
+                         cudaStream_t st) {
+  k_collapse_all<<<1, 1024, 0, st>>>(bmin, bmax, left, right, count, fifo, wide_children,
+                                     wide_of, n_wide);
 }
 
 // ------------------------------------------------------------------ env map

@@ -109,13 +109,12 @@ void launch_expand_rgb(const float *rgb, int64_t n, float4 *out, cudaStream_t st
 void launch_internal_flags(const int32_t *count, int64_t nn, int32_t *flags, cudaStream_t st);
 void launch_internal_scatter(const int32_t *flags, const int32_t *scan, int64_t nn,
                              int32_t *perm, int32_t *new_index, cudaStream_t st);
-void launch_collapse_level(const double *bmin, const double *bmax, const int32_t *left,
-                           const int32_t *right, const int32_t *count, const int32_t *roots,
-                           int32_t n_roots, int32_t base, int32_t *wide_children,
-                           int32_t *wide_of, int32_t *n_kids, cudaStream_t st);
-void launch_collapse_emit(const int32_t *wide_children, const int32_t *count, int32_t n_roots,
-                          int32_t base, const int32_t *kid_off, int32_t *next_roots,
-                          cudaStream_t st);
+// the whole breadth-first collapse in one single-CTA launch; *n_wide (device)
+// receives the wide-node count
+void launch_collapse_all(const double *bmin, const double *bmax, const int32_t *left,
+                         const int32_t *right, const int32_t *count, int32_t *fifo,
+                         int32_t *wide_children, int32_t *wide_of, int32_t *n_wide,
+                         cudaStream_t st);
 void launch_accumulate(const AccumArgs &aa, const float4 *L, float *accum, uint32_t *valid,
                        uint32_t *invalid, cudaStream_t st);
 void launch_pack_rays_f32(const float *o, const float *d, int64_t n, float t_min, float t_max,
