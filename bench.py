@@ -170,18 +170,19 @@ def measured_peak():
 
 
 def ncu_traffic(workload: str):
-    """dram bytes per trace launch from the committed ncu capture, if any."""
+    """dram bytes per ray (and the measured limiter) from the committed ncu
+    capture of the trace kernel, if any."""
     f = ROOT / "profiles" / "trace_traffic.json"
     if not f.exists():
-        return None, None
+        return None, None, None
     try:
         d = json.loads(f.read_text())
         e = d.get(workload)
         if e:
-            return e.get("dram_bytes_per_ray"), e.get("source")
+            return e.get("dram_bytes_per_ray"), e.get("source"), e.get("ncu_limiter")
     except Exception:
         pass
-    return None, None
+    return None, None, None
 
 
 def cpu_baseline(scene, bvh, args, seconds: float) -> dict:
@@ -366,7 +367,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     trace_ms = st["trace_ms"]
     launches = max(1, st["trace_launches"])
     achieved = (st["rays"] * bytes_per_ray) / (trace_ms / 1e3) / 1e9 if trace_ms > 0 else None
-    traffic_per_ray, traffic_src = ncu_traffic(args.workload)
+    traffic_per_ray, traffic_src, limiter = ncu_traffic(args.workload)
     roofline = {
         "bound": "hbm", "kernel": "k_trace (closest-hit BVH traversal)",
         "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -379,10 +380,13 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         "peak_source": peak_src, "traffic_source": traffic_src,
         "l2_read_gbs_measured": l2_gbs, "frac_of_l2": achieved / l2_gbs if achieved else None,
         "hbm_read_gbs_probe": hbm_probe,
+        "ncu_limiter": limiter,
         "note": "the traversal set (wide nodes + leaf triangles, ~70 MB at 1 M tris) is mostly "
                 "served from L2 (ncu dram traffic per launch is ~5% of the algorithmic bytes), "
                 "so algorithmic bytes per second can exceed the HBM copy peak; frac_of_l2 is "
-                "the fraction of the measured L2 streaming-read rate",
+                "the fraction of the measured L2 streaming-read rate; the unit that bounds "
+                "the kernel is the L1 data pipe (ncu_limiter: ~71-75 % of its wavefront rate, "
+                "one wavefront per lane per node load)",
     }
 
     # end to end through the public API: scene upload (pinned host arrays),

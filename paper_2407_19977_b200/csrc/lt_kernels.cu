@@ -329,9 +329,6 @@ __global__ void __launch_bounds__(kTraceThreads, LT_TRACE_MIN_BLOCKS)
     const float kInf = __int_as_float(0x7f800000);
     // ---- one wide node per active lane: descend nearest-first; the other
     // hit children go on the stack farthest first
-#ifndef LT_NODE_STEPS
-#define LT_NODE_STEPS 3
-#endif
 #pragma unroll 1
     for (int step = 0; step < LT_NODE_STEPS && q >= 0 && node >= 0; ++step) {
       const Hits4 h = LT_VISIT4(sc.wnodes + LT_NODE_F4 * (int64_t)node, rs, t_min, best.t);

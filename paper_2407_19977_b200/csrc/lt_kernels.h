@@ -19,6 +19,10 @@ constexpr int kShadeThreads = LT_SHADE_THREADS;
 #ifndef LT_TRACE_MIN_BLOCKS
 #define LT_TRACE_MIN_BLOCKS 9
 #endif
+// inner-node visits per lane between two leaf phases of k_trace
+#ifndef LT_NODE_STEPS
+#define LT_NODE_STEPS 3
+#endif
 #ifndef LT_SHADE_MIN_BLOCKS
 #define LT_SHADE_MIN_BLOCKS 8
 #endif
