@@ -1097,7 +1097,11 @@ static int render_impl(lt_scene *s, const lt_render_params *p, float *accum, uin
   // lanes: disjoint contiguous ranges of the (tile-ordered) local pixels,
   // each with its own batches on its own stream; per pixel, samples still
   // accumulate in index order, so results do not depend on the lane count
-  const int n_lanes = (int)std::max<int64_t>(1, std::min<int64_t>(s->n_lanes, n_local));
+  // a small pass (< 1 M paths) runs on one lane: a second lane would only
+  // add launches and a stream fork / join to a few-microsecond frame
+  const bool small = n_local * p->sample_count < (int64_t(1) << 20);
+  const int n_lanes =
+      small ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(s->n_lanes, n_local));
   struct Batch {
     int lane;
     int64_t s0, ns, pc0, np;
