@@ -104,13 +104,18 @@ struct DevBuf {
 struct TmpBuf {
   void *p = nullptr;
   cudaStream_t st = nullptr;
+  bool view = false;  // points into another TmpBuf (not freed here)
   int alloc(size_t want, cudaStream_t s) {
     st = s;
     CK(cudaMallocAsync(&p, std::max<size_t>(want, 16), s));
     return LT_OK;
   }
+  void set_view(void *q) {
+    p = q;
+    view = true;
+  }
   ~TmpBuf() {
-    if (p) cudaFreeAsync(p, st);
+    if (p && !view) cudaFreeAsync(p, st);
   }
   template <class T>
   T *as() const {
@@ -184,6 +189,17 @@ struct Workspace {
   // side stream for scene triangle uploads (overlaps the BVH layout)
   cudaStream_t upload_st = nullptr;
   std::mutex upload_mu;
+  // scene streams, reused across scenes (stream creation + destruction cost
+  // ~0.2 ms per scene, most of a tiny scene's set-up); a returned stream may
+  // still carry its last scene's stream-ordered frees, which simply run
+  // before the next scene's work
+  std::vector<cudaStream_t> free_streams;
+  std::mutex stream_mu;
+  bool pool_configured = false;
+  // pinned staging for small scenes: all arrays in one host buffer and one
+  // copy (stage_ev: the last copy out of it; guarded by upload_mu)
+  HostBuf stage;
+  cudaEvent_t stage_ev = nullptr;
 };
 
 static Workspace *workspace_for(int device) {
@@ -501,7 +517,14 @@ static void destroy_scene(lt_scene *s) {
   pt.mark("destroy: device frees");
   s->h_stage.release();
   for (cudaEvent_t e : s->ev_pool) cudaEventDestroy(e);
-  if (s->stream) cudaStreamDestroy(s->stream);
+  if (s->stream) {
+    if (s->ws) {
+      std::lock_guard<std::mutex> lk(s->ws->stream_mu);
+      s->ws->free_streams.push_back(s->stream);
+    } else {
+      cudaStreamDestroy(s->stream);
+    }
+  }
   pt.mark("destroy: host + stream");
   delete s;
 }
@@ -642,18 +665,28 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
   s->device = device;
   CK(cudaSetDevice(device));
   CK(cudaDeviceGetAttribute(&s->sm_count, cudaDevAttrMultiProcessorCount, device));
-  CK(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
   s->ws = workspace_for(device);
+  {
+    std::lock_guard<std::mutex> lk(s->ws->stream_mu);
+    if (!s->ws->free_streams.empty()) {
+      s->stream = s->ws->free_streams.back();
+      s->ws->free_streams.pop_back();
+    }
+  }
+  if (!s->stream) CK(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
   {
     const char *ls = std::getenv("LT_LANES");
     s->n_lanes = std::max(1, std::min(kLanes, ls ? std::atoi(ls) : kDefaultLanes));
   }
   {
-    // keep stream-ordered scene / staging memory mapped between scenes
+    // keep stream-ordered scene / staging memory mapped between scenes (once
+    // per device)
+    std::lock_guard<std::mutex> lk(s->ws->stream_mu);
     cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    if (!s->ws->pool_configured && cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
       uint64_t keep = UINT64_MAX;  // never trim: the pool peaks at the scene + staging + build scratch
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+      s->ws->pool_configured = true;
     }
   }
   for (DevBuf *b : {&s->geo, &s->nodes2, &s->shade, &s->mats, &s->env, &s->ray_ctr,
@@ -686,7 +719,56 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
   int32_t root_first;
   double root_lo[3], root_hi[3];
   cudaEvent_t tri_done = nullptr;
+  // small scenes (<= 4 MB of arrays): every array through the workspace's
+  // pinned staging buffer and ONE copy -- ~15 separate small (pageable)
+  // copies cost more than a tiny scene's whole layout
+  const size_t kSmallUpload = size_t(4) << 20;
+  TmpBuf t_all;
+  bool small_upload = false;
+  {
+    struct Item {
+      TmpBuf *dst;
+      const void *src;
+      size_t bytes;
+    };
+    std::vector<Item> items;
+    for (int k = 0; k < 6; ++k) items.push_back({&t_v[k], src[k], 24 * (size_t)n});
+    items.push_back({&t_mat, d->material_index, 4 * (size_t)n});
+    if (!build_here) {
+      items.push_back({&t_order, d->triangle_order, 4 * (size_t)n});
+      items.push_back({&t_bmin, d->bounds_min, 24 * (size_t)nn});
+      items.push_back({&t_bmax, d->bounds_max, 24 * (size_t)nn});
+      items.push_back({&t_left, d->left_child, 4 * (size_t)nn});
+      items.push_back({&t_right, d->right_child, 4 * (size_t)nn});
+      items.push_back({&t_first, d->first_triangle, 4 * (size_t)nn});
+      items.push_back({&t_count, d->triangle_count, 4 * (size_t)nn});
+    }
+    std::vector<size_t> off(items.size());
+    size_t total = 0;
+    for (size_t i = 0; i < items.size(); ++i) {
+      off[i] = total;
+      total += (items[i].bytes + 255) / 256 * 256;
+    }
+    small_upload = total <= kSmallUpload;
+    if (small_upload) {
+      RET(t_all.alloc(total, st));
+      Workspace &W = *s->ws;
+      std::lock_guard<std::mutex> lk(W.upload_mu);
+      if (W.stage_ev)
+        CK(cudaEventSynchronize(W.stage_ev));  // the previous small scene's copy
+      else
+        CK(cudaEventCreateWithFlags(&W.stage_ev, cudaEventDisableTiming));
+      RET(W.stage.ensure(kSmallUpload));
+      for (size_t i = 0; i < items.size(); ++i)
+        std::memcpy(static_cast<char *>(W.stage.p) + off[i], items[i].src, items[i].bytes);
+      CK(cudaMemcpyAsync(t_all.p, W.stage.p, total, cudaMemcpyHostToDevice, st));
+      CK(cudaEventRecord(W.stage_ev, st));
+      for (size_t i = 0; i < items.size(); ++i)
+        items[i].dst->set_view(static_cast<char *>(t_all.p) + off[i]);
+    }
+  }
   auto upload_triangles = [&](cudaStream_t ts) -> int {
+    if (small_upload) return LT_OK;  // already staged
     for (int k = 0; k < 6; ++k) RET(upload(t_v[k], src[k], 3 * n, ts));
     RET(upload(t_mat, d->material_index, n, ts));
     return LT_OK;
@@ -713,26 +795,28 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
     root_first = rc0[1];
     pt.mark("device BVH build");
   } else {
-    RET(upload(t_order, d->triangle_order, n, st));
-    RET(upload(t_bmin, d->bounds_min, 3 * nn, st));
-    RET(upload(t_bmax, d->bounds_max, 3 * nn, st));
-    RET(upload(t_left, d->left_child, nn, st));
-    RET(upload(t_right, d->right_child, nn, st));
-    RET(upload(t_first, d->first_triangle, nn, st));
-    RET(upload(t_count, d->triangle_count, nn, st));
-    // the triangle arrays follow on the workspace's side stream: the BVH
-    // arrays are enqueued first (the copy engine serves them first) and
-    // their device layout overlaps the larger triangle transfer; the
-    // flatten joins both streams
-    {
-      std::lock_guard<std::mutex> lk(s->ws->upload_mu);
-      if (!s->ws->upload_st)
-        CK(cudaStreamCreateWithFlags(&s->ws->upload_st, cudaStreamNonBlocking));
-      CK(cudaEventCreateWithFlags(&tri_done, cudaEventDisableTiming));
-      CK(cudaEventRecord(tri_done, st));
-      CK(cudaStreamWaitEvent(s->ws->upload_st, tri_done, 0));
-      RET(upload_triangles(s->ws->upload_st));
-      CK(cudaEventRecord(tri_done, s->ws->upload_st));
+    if (!small_upload) {
+      RET(upload(t_order, d->triangle_order, n, st));
+      RET(upload(t_bmin, d->bounds_min, 3 * nn, st));
+      RET(upload(t_bmax, d->bounds_max, 3 * nn, st));
+      RET(upload(t_left, d->left_child, nn, st));
+      RET(upload(t_right, d->right_child, nn, st));
+      RET(upload(t_first, d->first_triangle, nn, st));
+      RET(upload(t_count, d->triangle_count, nn, st));
+      // the triangle arrays follow on the workspace's side stream: the BVH
+      // arrays are enqueued first (the copy engine serves them first) and
+      // their device layout overlaps the larger triangle transfer; the
+      // flatten joins both streams
+      {
+        std::lock_guard<std::mutex> lk(s->ws->upload_mu);
+        if (!s->ws->upload_st)
+          CK(cudaStreamCreateWithFlags(&s->ws->upload_st, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&tri_done, cudaEventDisableTiming));
+        CK(cudaEventRecord(tri_done, st));
+        CK(cudaStreamWaitEvent(s->ws->upload_st, tri_done, 0));
+        RET(upload_triangles(s->ws->upload_st));
+        CK(cudaEventRecord(tri_done, s->ws->upload_st));
+      }
     }
     g_bmin = t_bmin.as<double>();
     g_bmax = t_bmax.as<double>();
