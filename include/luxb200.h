@@ -191,6 +191,13 @@ int lt_trace_paths_host(lt_scene *scene, const double *origins, const double *di
                         int32_t max_depth, int32_t rr_start, double t_min, double *rgb,
                         uint64_t *state_out);
 
+/* ---- result of a device accumulation (lt_render_pass buffers) as the
+ * reference's RenderResult arrays (integrator.py:62-68): per pixel
+ * mean = sum / max(valid, 1) in float64 (h*w*3) and invalid as int64, on
+ * the device, one launch on `stream` ---- */
+int lt_accum_finish(const float *accum_sum, const uint32_t *valid, const uint32_t *invalid,
+                    int64_t n_pixels, double *mean, int64_t *invalid_out, void *stream);
+
 /* ---- display transform (tonemap.py:18-61, the §8(f) next row): linear
  * (h*w*3) float32 device -> sRGB u8 (h*w*3) device ---- */
 int lt_tonemap_u8(const float *linear, int64_t n_pixels, uint8_t *out, void *stream);

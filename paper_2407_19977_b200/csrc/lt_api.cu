@@ -1228,12 +1228,16 @@ static int render_impl(lt_scene *s, const lt_render_params *p, float *accum, uin
     }
     CK(cudaEventCreateWithFlags(&W.fork_ev, cudaEventDisableTiming));
   }
-  CK(cudaEventRecord(W.fork_ev, st));
-  for (int k = 0; k < n_lanes; ++k) CK(cudaStreamWaitEvent(W.lane_st[k], W.fork_ev, 0));
+  // (one lane: its work goes straight onto the caller's stream)
+  const bool fork = n_lanes > 1;
+  if (fork) {
+    CK(cudaEventRecord(W.fork_ev, st));
+    for (int k = 0; k < n_lanes; ++k) CK(cudaStreamWaitEvent(W.lane_st[k], W.fork_ev, 0));
+  }
   const float t_min = (float)p->t_min;
   for (const Batch &b : order) {
     Lane &ln = s->ws->lane[b.lane];
-    cudaStream_t ls = W.lane_st[b.lane];
+    cudaStream_t ls = fork ? W.lane_st[b.lane] : st;
     int32_t *ctr = ln.counters.as<int32_t>();
     CK(cudaMemsetAsync(ctr, 0, sizeof(int32_t) * (2 * (size_t)p->max_depth + 2), ls));
     RaygenArgs ra{};
@@ -1258,7 +1262,7 @@ static int render_impl(lt_scene *s, const lt_render_params *p, float *accum, uin
     s->stats.paths += b.np * b.ns;
   }
   // join back into the caller's stream
-  for (int k = 0; k < n_lanes; ++k) {
+  for (int k = 0; fork && k < n_lanes; ++k) {
     CK(cudaEventRecord(W.join_ev[k], W.lane_st[k]));
     CK(cudaStreamWaitEvent(st, W.join_ev[k], 0));
   }
@@ -1636,6 +1640,18 @@ extern "C" int lt_read_bandwidth(int32_t device, int64_t bytes, int32_t iters, d
   sink.release();
   if (e != cudaSuccess) return lt_fail(LT_ERR_CUDA, "probe failed: %s", cudaGetErrorString(e));
   *gbps = (double)bytes * passes * iters / (ms * 1e-3) / 1e9;
+  return LT_OK;
+}
+
+extern "C" int lt_accum_finish(const float *accum_sum, const uint32_t *valid,
+                               const uint32_t *invalid, int64_t n_pixels, double *mean,
+                               int64_t *invalid_out, void *stream) {
+  if (n_pixels < 0 ||
+      (n_pixels > 0 && (!accum_sum || !valid || !invalid || !mean || !invalid_out)))
+    return lt_fail(LT_ERR_INVALID, "invalid accumulation arguments");
+  launch_accum_finish(accum_sum, valid, invalid, n_pixels, mean, invalid_out,
+                      (cudaStream_t)stream);
+  CK(cudaGetLastError());
   return LT_OK;
 }
 

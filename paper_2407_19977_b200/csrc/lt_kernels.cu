@@ -1130,6 +1130,27 @@ void launch_unpack_hits(const SceneView &sc, const float4 *hits, int64_t n, int3
   k_unpack_hits<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(sc, hits, n, idx32, t32, idx64, t64);
 }
 
+// Final means of an accumulation, as the Python layer's
+// sum.double() / max(valid, 1) and invalid as int64, in one pass.
+__global__ void k_accum_finish(const float *__restrict__ sum, const uint32_t *__restrict__ valid,
+                               const uint32_t *__restrict__ invalid, int64_t n_pix,
+                               double *__restrict__ mean, int64_t *__restrict__ inv) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n_pix) return;
+  const double v = (double)max(valid[i], 1u);
+  mean[3 * i + 0] = (double)sum[3 * i + 0] / v;
+  mean[3 * i + 1] = (double)sum[3 * i + 1] / v;
+  mean[3 * i + 2] = (double)sum[3 * i + 2] / v;
+  inv[i] = (int64_t)invalid[i];
+}
+
+void launch_accum_finish(const float *sum, const uint32_t *valid, const uint32_t *invalid,
+                         int64_t n_pix, double *mean, int64_t *inv, cudaStream_t st) {
+  if (n_pix <= 0) return;
+  k_accum_finish<<<(unsigned)((n_pix + 255) / 256), 256, 0, st>>>(sum, valid, invalid, n_pix,
+                                                                  mean, inv);
+}
+
 void launch_tonemap_u8(const float *lin, int64_t n_pixels, uint8_t *out, cudaStream_t st) {
   if (n_pixels <= 0) return;
   k_tonemap_u8<<<(unsigned)((n_pixels + 255) / 256), 256, 0, st>>>(lin, n_pixels, out);

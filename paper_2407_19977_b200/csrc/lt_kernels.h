@@ -128,6 +128,8 @@ void launch_pack_rays_f64(const double *o, const double *d, int64_t n, float t_m
 void launch_unpack_hits(const SceneView &sc, const float4 *hits, int64_t n, int32_t *idx32,
                         float *t32, int64_t *idx64, double *t64, cudaStream_t st);
 void launch_tonemap_u8(const float *lin, int64_t n_pixels, uint8_t *out, cudaStream_t st);
+void launch_accum_finish(const float *sum, const uint32_t *valid, const uint32_t *invalid,
+                         int64_t n_pix, double *mean, int64_t *inv, cudaStream_t st);
 void launch_bsdf_eval(const GpuMaterial *mats, const double *wo, const double *wi,
                       const double *nrm, int64_t n, double *f, double *pdf, cudaStream_t st);
 void launch_bsdf_sample(const GpuMaterial *mats, const double *wo, const double *nrm,

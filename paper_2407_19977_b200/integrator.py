@@ -212,9 +212,17 @@ def fetch_image(acc: Accumulator, stream=None):
         _PINNED_PRIMED.add(key)
     mean_h = torch.empty((h, w, 3), dtype=torch.float64, pin_memory=True)
     inv_h = torch.empty((h, w), dtype=torch.int64, pin_memory=True)
-    mean_h.copy_(acc.mean(), non_blocking=True)
-    inv_h.copy_(acc.invalid.view(h, w).to(torch.int64), non_blocking=True)
-    (stream or torch.cuda.current_stream(acc.device)).synchronize()
+    st = stream or torch.cuda.current_stream(acc.device)
+    mean_d = torch.empty((h, w, 3), dtype=torch.float64, device=acc.device)
+    inv_d = torch.empty((h, w), dtype=torch.int64, device=acc.device)
+    # sum / max(valid, 1) and the int64 counts in one launch (Accumulator.mean's
+    # arithmetic), then one copy each
+    _lib.check(_lib.lib().lt_accum_finish(*acc.pointers(), h * w, C.c_void_p(mean_d.data_ptr()),
+                                          C.c_void_p(inv_d.data_ptr()),
+                                          C.c_void_p(st.cuda_stream)))
+    mean_h.copy_(mean_d, non_blocking=True)
+    inv_h.copy_(inv_d, non_blocking=True)
+    st.synchronize()
     return mean_h.numpy(), inv_h.numpy()
 
 
