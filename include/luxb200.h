@@ -37,8 +37,12 @@ extern "C" {
 #define LT_ENV_LATLONG 2
 
 /* lt_render_params.flags */
-#define LT_FLAG_SORT_MATERIALS 1u   /* reserved (no effect): continuation rays are grouped by
-                                       direction octant instead (ShadeArgs.octant_sort) */
+#define LT_FLAG_SORT_MATERIALS 1u   /* shade every bounce in material-class order: a
+                                       classify + counting-sort pass groups the hit queue
+                                       by class (miss, final segment, diffuse-only, GGX,
+                                       coat, glass, coat + glass) and the shade kernel
+                                       reads it through that permutation; results are
+                                       unchanged (off by default) */
 #define LT_FLAG_NO_SMEM_TOP 2u      /* reserved (top-node staging was removed); no effect */
 #define LT_FLAG_PROFILE 4u          /* time every trace launch with CUDA events */
 #define LT_FLAG_COUNT 8u            /* count slab / triangle tests in the trace kernel */

@@ -176,6 +176,9 @@ struct Lane {
   int64_t cap = 0;
   int32_t depth_cap = 0;
   DevBuf q_o[2], q_d[2], hits, T, L, rng, counters;
+  // LT_FLAG_SORT_MATERIALS: per-entry class, the class-grouped slot order,
+  // class totals + cursors
+  DevBuf cls, perm, cls_ctr;
 };
 
 struct Workspace {
@@ -1012,6 +1015,9 @@ static int ensure_lane(lt_scene *s, Lane &ln, int64_t cap, int32_t max_depth) {
     RET(ln.T.ensure(16 * cap));
     RET(ln.L.ensure(16 * cap));
     RET(ln.rng.ensure(16 * cap));
+    RET(ln.cls.ensure(cap));
+    RET(ln.perm.ensure(4 * cap));
+    RET(ln.cls_ctr.ensure(sizeof(int32_t) * 2 * kShadeClasses));
     ln.cap = cap;
   }
   if (max_depth > ln.depth_cap) {
@@ -1067,7 +1073,16 @@ static int run_bounces(lt_scene *s, Lane &lane, int32_t max_depth, int32_t rr_st
                     ws->q_d[cur].as<float4>(), ctr + depth, fetch + depth,
                     ws->hits.as<float4>(), s->ray_ctr.as<unsigned long long>(), st));
     if (flags & LT_FLAG_PROFILE) RET(record_event(s, st));
-    ShadeArgs sa{depth, max_depth, rr_start, t_min, 0, s->octant_sort ? 1 : 0,
+    const int32_t *perm = nullptr;
+    if (flags & LT_FLAG_SORT_MATERIALS) {
+      CK(cudaMemsetAsync(ws->cls_ctr.p, 0, sizeof(int32_t) * 2 * kShadeClasses, st));
+      launch_material_sort(sc, ws->hits.as<float4>(), ctr + depth, depth != max_depth - 1,
+                           shade_grid, ws->cls.as<uint8_t>(), ws->cls_ctr.as<int32_t>(),
+                           ws->perm.as<int32_t>(), st);
+      perm = ws->perm.as<int32_t>();
+      s->stats.kernel_launches += 2;
+    }
+    ShadeArgs sa{depth, max_depth, rr_start, t_min, 0, s->octant_sort ? 1 : 0, perm,
                  (flags & LT_FLAG_COUNT) ? s->ray_ctr.as<unsigned long long>() + 3 : nullptr};
     CK(launch_shade(sc, sa, pa, shade_grid,
                     s->use_window && s->use_shade_window ? &s->shade_window : nullptr, prim,

@@ -444,11 +444,12 @@ __global__ void __launch_bounds__(kShadeThreads, LT_SHADE_MIN_BLOCKS)
     __syncthreads();
   }
   for (int base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
-    const int q = base + threadIdx.x;
+    const int qi = base + threadIdx.x;
     bool emit = false;
     float4 out_o, out_d;
     int cls = -1;  // material class of the lane's hit (LT_FLAG_COUNT statistics)
-    if (q < n) {
+    if (qi < n) {
+      const int q = sa.perm ? __ldg(&sa.perm[qi]) : qi;
       // queue entries and path state stream through (evict-first) so the
       // L2 keeps the triangle / shading records
       const float4 h = __ldcs(&hits[q]);
@@ -1128,6 +1129,75 @@ void launch_unpack_hits(const SceneView &sc, const float4 *hits, int64_t n, int3
                         float *t32, int64_t *idx64, double *t64, cudaStream_t st) {
   if (n <= 0) return;
   k_unpack_hits<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(sc, hits, n, idx32, t32, idx64, t64);
+}
+
+// Shading class of queue entry q (k_shade's divergence classes).
+__device__ __forceinline__ int shade_class(const SceneView &sc, const float4 *__restrict__ hits,
+                                           int q, bool scatter) {
+  const int32_t k = __float_as_int(__ldg(&hits[q]).w);
+  if (k < 0) return 0;
+  if (!scatter) return 1;
+  const uint32_t f = sc.mats[__float_as_int(__ldg(&sc.shade[4 * (int64_t)k]).w)].flags;
+  if (f & MAT_DIFFUSE_ONLY) return 2;
+  const uint32_t cg = f & (MAT_COAT | MAT_GLASS);
+  return cg == 0 ? 3 : cg == MAT_COAT ? 4 : cg == MAT_GLASS ? 5 : 6;
+}
+
+__global__ void __launch_bounds__(256)
+    k_class_count(SceneView sc, const float4 *__restrict__ hits, const int32_t *__restrict__ count,
+                  int scatter, uint8_t *__restrict__ cls, int32_t *__restrict__ totals) {
+  __shared__ int s_h[kShadeClasses];
+  if (threadIdx.x < kShadeClasses) s_h[threadIdx.x] = 0;
+  __syncthreads();
+  const int n = *count;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
+    const int c = shade_class(sc, hits, q, scatter != 0);
+    cls[q] = (uint8_t)c;
+    atomicAdd(&s_h[c], 1);
+  }
+  __syncthreads();
+  if (threadIdx.x < kShadeClasses && s_h[threadIdx.x])
+    atomicAdd(&totals[threadIdx.x], s_h[threadIdx.x]);
+}
+
+// perm[class base + cursor] = q, each block reserving one range per class
+__global__ void __launch_bounds__(256)
+    k_class_scatter(const uint8_t *__restrict__ cls, const int32_t *__restrict__ count,
+                    const int32_t *__restrict__ totals, int32_t *__restrict__ cursor,
+                    int32_t *__restrict__ perm) {
+  __shared__ int s_base[kShadeClasses], s_cnt[kShadeClasses], s_off[kShadeClasses];
+  if (threadIdx.x == 0) {
+    int run = 0;
+    for (int c = 0; c < kShadeClasses; ++c) {
+      s_base[c] = run;
+      run += totals[c];
+    }
+  }
+  const int n = *count;
+  for (int b = blockIdx.x * blockDim.x; b < n; b += gridDim.x * blockDim.x) {
+    if (threadIdx.x < kShadeClasses) s_cnt[threadIdx.x] = 0;
+    __syncthreads();
+    const int q = b + threadIdx.x;
+    int c = 0, r = 0;
+    if (q < n) {
+      c = cls[q];
+      r = atomicAdd(&s_cnt[c], 1);
+    }
+    __syncthreads();
+    if (threadIdx.x < kShadeClasses)
+      s_off[threadIdx.x] =
+          s_cnt[threadIdx.x] ? atomicAdd(&cursor[threadIdx.x], s_cnt[threadIdx.x]) : 0;
+    __syncthreads();
+    if (q < n) perm[s_base[c] + s_off[c] + r] = q;
+    __syncthreads();
+  }
+}
+
+void launch_material_sort(const SceneView &sc, const float4 *hits, const int32_t *count,
+                          bool scatter, int grid, uint8_t *cls, int32_t *cls_ctr, int32_t *perm,
+                          cudaStream_t st) {
+  k_class_count<<<grid, 256, 0, st>>>(sc, hits, count, scatter ? 1 : 0, cls, cls_ctr);
+  k_class_scatter<<<grid, 256, 0, st>>>(cls, count, cls_ctr, cls_ctr + kShadeClasses, perm);
 }
 
 // Final means of an accumulation, as the Python layer's

@@ -57,6 +57,9 @@ struct ShadeArgs {
   float t_min;
   int32_t primary;  // depth-0 launch of a render batch: rays from RaygenArgs
   int32_t octant_sort;  // append continuation rays grouped by direction octant
+  // LT_FLAG_SORT_MATERIALS: queue entry i is shaded from slot perm[i] (slots
+  // grouped by material class); nullptr = queue order
+  const int32_t *perm;
   // LT_FLAG_COUNT: [warps, warps whose active lanes span > 1 material class,
   // sum over warps of the distinct classes] (shading divergence evidence)
   unsigned long long *warp_ctr;
@@ -128,6 +131,14 @@ void launch_pack_rays_f64(const double *o, const double *d, int64_t n, float t_m
 void launch_unpack_hits(const SceneView &sc, const float4 *hits, int64_t n, int32_t *idx32,
                         float *t32, int64_t *idx64, double *t64, cudaStream_t st);
 void launch_tonemap_u8(const float *lin, int64_t n_pixels, uint8_t *out, cudaStream_t st);
+// material-class grouping of a hit queue (LT_FLAG_SORT_MATERIALS): per
+// entry class (miss, final segment, diffuse-only, reference GGX, coat,
+// glass, coat + glass), then perm = the queue slots grouped by class.
+// cls_ctr: 16 zeroed ints (class totals, class cursors).
+constexpr int kShadeClasses = 8;
+void launch_material_sort(const SceneView &sc, const float4 *hits, const int32_t *count,
+                          bool scatter, int grid, uint8_t *cls, int32_t *cls_ctr, int32_t *perm,
+                          cudaStream_t st);
 void launch_accum_finish(const float *sum, const uint32_t *valid, const uint32_t *invalid,
                          int64_t n_pix, double *mean, int64_t *inv, cudaStream_t st);
 void launch_bsdf_eval(const GpuMaterial *mats, const double *wo, const double *wi,

@@ -276,6 +276,27 @@ def test_traversal_schedule_does_not_change_results(knobs, monkeypatch):
     assert np.array_equal(plain, other)
 
 
+@pytest.mark.parametrize("name", ["cornell_c2", "sphere20k"])
+def test_material_sorted_shading_does_not_change_results(name):
+    """LT_FLAG_SORT_MATERIALS (the hit queue shaded in material-class order
+    through a permutation) changes which lane shades which path, not a
+    result; the divergence counters show the grouping took effect."""
+    from paper_2407_19977_b200 import _lib
+    m = lb()
+    g = golden_scene(name)
+    st = m.RenderSettings(samples_per_pixel=4, max_depth=6, seed=5)
+    plain = m.render_progressive(device_scene(g), st).image
+    ds = device_scene(g)
+    fl = _lib.LT_FLAG_SORT_MATERIALS | _lib.LT_FLAG_COUNT
+    sorted_img = m.render_progressive(ds, st, flags=fl).image
+    assert np.array_equal(plain, sorted_img)
+    s = ds.stats()
+    assert s["shade_warps"] > 0
+    # grouped queues: almost every warp sees one class (class boundaries
+    # and partial warps only)
+    assert s["shade_warp_classes"] / s["shade_warps"] < 1.1
+
+
 @pytest.mark.parametrize("size", [(17, 13), (1, 1), (3, 50)])
 def test_odd_image_sizes_against_oracle(size):
     """Partial 4x4 tiles of the tile-ordered pixel list (k_pixel_list) and
