@@ -7,7 +7,10 @@
 
 namespace lt {
 
-constexpr int kTraceThreads = 128;
+#ifndef LT_TRACE_THREADS
+#define LT_TRACE_THREADS 128
+#endif
+constexpr int kTraceThreads = LT_TRACE_THREADS;
 #ifndef LT_SHADE_THREADS
 #define LT_SHADE_THREADS 128
 #endif
