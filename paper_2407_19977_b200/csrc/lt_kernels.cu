@@ -426,8 +426,10 @@ __device__ __forceinline__ int dir_bin(const float4 &d) {
 // One bounce of _trace (integrator.py:160-226) for every queued path:
 // miss -> environment; hit -> emission; final segment stops; otherwise hit
 // frame, 3 draws, BSDF sample, throughput, Russian roulette (4th draw), and
-// the continuation ray is appended to the next queue (warp ballot +
-// one atomic per warp).
+// the continuation ray is appended to the next queue: one atomic per block
+// iteration, the block's rays laid out by direction octant (or, with
+// ShadeArgs.octant_sort off, warp ballot + one atomic per warp).  With
+// ShadeArgs.perm the queue is shaded in material-class order.
 __global__ void __launch_bounds__(kShadeThreads, LT_SHADE_MIN_BLOCKS)
     k_shade(SceneView sc, ShadeArgs sa, RaygenArgs ra, PathArrays pa,
             const float4 *__restrict__ q_o, const float4 *__restrict__ q_d,
