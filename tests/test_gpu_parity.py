@@ -562,3 +562,32 @@ def test_axis_aligned_rays_against_oracle(name):
     assert (ref_i >= 0).sum() > len(idx) // 20 or name == "floor"  # geometry is hit
     same = (idx == ref_i) & (ref_i >= 0)
     assert np.all(np.abs(t[same] - ref_t[same]) <= 2e-5 * np.maximum(1.0, ref_t[same]))
+
+
+@pytest.mark.parametrize("max_depth,rr_start,seed,t_min", [
+    (1, 3, 0, 1e-4),      # camera segment only: emission / environment
+    (2, 0, 17, 1e-4),     # roulette from the first scatter
+    (12, 0, 5, 1e-4),     # long paths, roulette everywhere
+    (16, 20, 3, 1e-4),    # no roulette before the last segment
+    (6, 2, 123456789, 1e-3),  # larger t_min, large seed
+])
+def test_render_settings_against_oracle(max_depth, rr_start, seed, t_min):
+    """Per-sample radiance at matched streams vs the float64 oracle across
+    the RenderSettings that change the path loop (integrator.py:178-221):
+    depth limits, the Russian-roulette start (which moves the RNG draw
+    schedule), seeds and t_min."""
+    from oracle.oracle import OracleScene
+    m = lb()
+    g = golden_scene("cornell_c2")
+    cam = g.camera
+    st = m.RenderSettings(samples_per_pixel=1, max_depth=max_depth, rr_start_depth=rr_start,
+                          seed=seed, t_min=t_min)
+    ds = device_scene(g)
+    oc = OracleScene.from_scene(g.scene, g.bvh)
+    pix = np.arange(cam.width * cam.height)
+    fr = []
+    for s in range(2):
+        ref, _ = oc.sample_values(pix, s, m.camera_pack(cam), cam.width, cam.height, st.seed,
+                                  st.max_depth, st.rr_start_depth, st.t_min)
+        fr.append(close_fraction(gpu_sample_values(ds, cam, st, s), ref))
+    assert np.mean(fr) >= (0.999 if max_depth == 1 else 0.98), np.mean(fr)
