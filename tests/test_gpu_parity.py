@@ -621,15 +621,16 @@ def test_cameras_against_oracle(pos, look, up, fov, size):
     assert np.mean(fr) >= 0.98, np.mean(fr)
 
 
+@pytest.mark.parametrize("name", ["sphere20k", "cornell_c2"])
 @pytest.mark.parametrize("seed", [1, 2, 3])
-def test_random_reference_materials_against_oracle(seed):
+def test_random_reference_materials_against_oracle(seed, name):
     """The shade kernel's reference-material branches (diffuse-only fast
     path, metal / dielectric GGX lobes, the alpha clamp at roughness 0,
     specular weight 0 / 1, emission) with random OpenPBR parameters on every
     material slot: per-sample radiance at matched streams vs the oracle."""
     from oracle.oracle import OracleScene
     m = lb()
-    g = golden_scene("sphere20k")
+    g = golden_scene(name)
     rng = np.random.default_rng(seed)
     mats = []
     for i in range(len(g.materials)):
