@@ -656,3 +656,64 @@ def test_random_reference_materials_against_oracle(seed, name):
                                   st.max_depth, st.rr_start_depth, st.t_min)
         fr.append(close_fraction(gpu_sample_values(ds, cam, st, s), ref))
     assert np.mean(fr) >= 0.98, np.mean(fr)
+
+
+def test_large_frame_pixel_subset_against_oracle():
+    """A 4096 x 2048 frame (8.4 M paths in one pass: large tile-ordered pixel
+    lists, two lanes, big batches) checked at 3000 random pixels against the
+    float64 oracle at matched streams."""
+    from dataclasses import replace
+    from paper_2407_19977_b200.integrator import Accumulator, render_pass_device
+    from oracle.oracle import OracleScene
+    m = lb()
+    g = golden_scene("sphere20k")
+    w, h = 4096, 2048
+    cam = replace(g.camera, width=w, height=h)
+    sc = m.SceneDescription(g.triangles, g.materials, cam, g.environment, 0)
+    ds = m.DeviceScene(sc, g.bvh)
+    st = m.RenderSettings(samples_per_pixel=1, max_depth=6, seed=77)
+    acc = Accumulator(w, h, ds.device)
+    render_pass_device(ds, cam, st, acc, 3, 1)
+    got = acc.sum.view(-1, 3).double().cpu().numpy()
+    v = acc.valid.cpu().numpy()
+    got[v == 0] = np.nan
+    pix = np.random.default_rng(0).choice(w * h, 3000, replace=False)
+    oc = OracleScene.from_scene(sc, g.bvh)
+    ref, _ = oc.sample_values(pix, 3, m.camera_pack(cam), w, h, st.seed, st.max_depth,
+                              st.rr_start_depth, st.t_min)
+    assert close_fraction(got[pix], ref) >= 0.99
+
+
+def test_degenerate_triangles_against_oracle():
+    """Zero-area triangles (collapsed vertices, collinear vertices) and
+    sliver triangles mixed into a scene: closest hits vs the oracle (the
+    |det| <= 1e-9 rejection of geometry.py:150-152)."""
+    from oracle.oracle import OracleScene
+    m = lb()
+    g = golden_scene("sphere2k")
+    tb = g.triangles
+    rng = np.random.default_rng(3)
+    k = 200
+    a = rng.uniform(-1, 1, (k, 3))
+    b = a + rng.normal(size=(k, 3)) * 0.3
+    deg_v0 = np.concatenate([a, a, a])
+    deg_v1 = np.concatenate([a, b, b])                    # point, segment, sliver
+    deg_v2 = np.concatenate([a, 2 * b - a, b + 1e-7])
+    n = np.tile([0.0, 1.0, 0.0], (3 * k, 1))
+    tri = m.TriangleBuffer(np.concatenate([tb.v0, deg_v0]), np.concatenate([tb.v1, deg_v1]),
+                           np.concatenate([tb.v2, deg_v2]), np.concatenate([tb.n0, n]),
+                           np.concatenate([tb.n1, n]), np.concatenate([tb.n2, n]),
+                           np.concatenate([tb.material_index,
+                                           np.zeros(3 * k, tb.material_index.dtype)]))
+    bvh = m.build_bvh(tri)
+    sc = m.SceneDescription(tri, g.materials, g.camera, g.environment, 0)
+    ds = m.DeviceScene(sc, bvh)
+    oc = OracleScene.from_scene(sc, bvh)
+    o = rng.uniform(-2, 2, (4000, 3))
+    d = rng.normal(size=(4000, 3))
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    idx, t = m.intersect_scene_batch(tri, bvh, o, d, scene=ds)
+    ref_i, ref_t = oc.intersect_batch(o, d)
+    assert int(np.sum(idx != ref_i)) <= 2
+    same = (idx == ref_i) & (ref_i >= 0)
+    assert np.all(np.abs(t[same] - ref_t[same]) <= 2e-5 * np.maximum(1.0, ref_t[same]))
