@@ -59,6 +59,8 @@ def parse_args():
                    help="paths per wavefront batch (0 = library default)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--no-variant", action="store_true",
+                   help="skip the reference-lobe variant measurement")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--ref-step-seconds", type=float, default=6.0)
     return p.parse_args()
@@ -89,7 +91,7 @@ def workload_config(args, n_tris: int, world: int) -> dict:
 def build_workload(args, device="auto"):
     """The scene and its BVH (the reference's tree; device=None builds it
     with the host restatement -- the reference arm never touches the GPU)."""
-    from paper_2407_19977_b200.procgen import scene_by_name
+    from workloads import scene_by_name
     from paper_2407_19977_b200 import build_bvh
     scene = scene_by_name(args.workload, width=args.width, height=args.height)
     bvh = build_bvh(scene.triangles, leaf_size=args.bvh_leaf, bins=args.bvh_bins, device=device)
@@ -169,32 +171,15 @@ def measured_peak():
     return HBM_FALLBACK_GBS, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(workload: str):
-    """dram bytes per ray (and the measured limiter) from the committed ncu
-    capture of the trace kernel, if any."""
-    f = ROOT / "profiles" / "trace_traffic.json"
-    if not f.exists():
-        return None, None, None
-    try:
-        d = json.loads(f.read_text())
-        e = d.get(workload)
-        if e:
-            return e.get("dram_bytes_per_ray"), e.get("source"), e.get("ncu_limiter")
-    except Exception:
-        pass
-    return None, None, None
-
-
-def cpu_baseline(scene, bvh, args, seconds: float) -> dict:
+def cpu_baseline(args, seconds: float) -> dict:
     """The float64 oracle (the reference's algorithm restated in C) on a
-    bounded pixel sample of the same frame, all host threads."""
-    from oracle.oracle import OracleScene, default_threads
-    from paper_2407_19977_b200 import camera_pack
-    oc = OracleScene.from_scene(scene, bvh)
-    cam = camera_pack(scene.camera)
+    bounded pixel sample of the workload's reference-lobe variant (what the
+    reference can render), all host threads."""
+    from oracle.oracle import default_threads
+    name, _, oc, cam = reference_setup(args)
     w, h = args.width, args.height
     threads = default_threads()
-    n = max(threads * 256, 8192)
+    n = min(w * h, max(threads * 256, 8192))
     paths = 0
     segs = 0
     t_total = 0.0
@@ -214,33 +199,53 @@ def cpu_baseline(scene, bvh, args, seconds: float) -> dict:
             n = min(w * h, n * 2)
     return {"value": paths / t_total, "unit": UNIT, "cores": threads, "kind": "port",
             "mrays_per_s": segs / t_total / 1e6,
-            "sample": f"{paths} random (pixel, sample) paths of the same frame and settings "
+            "sample": f"{paths} random (pixel, sample) paths of the {name!r} frame (same settings) "
                       f"over {sample} sample indices, {t_total:.1f} s on {threads} threads "
                       f"(oracle/lt_oracle.c, float64 restatement of the reference)"}
 
 
 # ------------------------------------------------------------------ arms
 
+# The reference (luxtrace) has no coat / transmission lobe and no HDR
+# environment: it renders a workload's reference-lobe
+# variant -- same geometry and camera, coat -> base, glass -> dielectric
+# specular, HDR sky -> the bench gradient.
+REFERENCE_VARIANT = {"pushbutton": "pushbutton_ref", "cornell_c2x": "cornell_c2"}
+
+
+def reference_setup(args):
+    """The CPU reference's inputs: the workload's reference-lobe variant from
+    workloads.py, its tree from oc_build_bvh (= build_bvh, bvh.py:286-298),
+    the oracle scene and the packed camera; the product is not involved."""
+    import workloads
+    from oracle.oracle import OracleScene, camera_pack
+    from oracle.oracle import build_bvh as oracle_build_bvh
+    name = REFERENCE_VARIANT.get(args.workload, args.workload)
+    scene = workloads.scene_by_name(name, width=args.width, height=args.height)
+    bvh = oracle_build_bvh(scene.triangles, leaf_size=args.bvh_leaf, bins=args.bvh_bins)
+    return name, scene, OracleScene.from_scene(scene, bvh), camera_pack(scene.camera)
+
+
 def run_reference(args, rank: int, world: int) -> None:
+    """The reference's algorithm on the host cores: the float64 C
+    restatement in oracle/, all threads; the product package is never
+    imported."""
     if rank != 0:
         return
-    from oracle.oracle import OracleScene, default_threads
-    from paper_2407_19977_b200 import camera_pack
-    scene, bvh = build_workload(args, device=None)
-    oc = OracleScene.from_scene(scene, bvh)
-    cam = camera_pack(scene.camera)
+    from oracle.oracle import default_threads
+    name, scene, oc, cam = reference_setup(args)
     w, h = args.width, args.height
     threads = default_threads()
     rng = np.random.default_rng(2)
     # calibrate the per-step pixel sample to about --ref-step-seconds
-    n = 4096
+    n = min(4096, w * h)
     while True:
         pix = np.sort(rng.choice(w * h, size=n, replace=False))
         t0 = time.perf_counter()
         oc.sample_values(pix, 0, cam, w, h, args.seed, args.depth, args.rr_start, 1e-4, threads)
         dt = time.perf_counter() - t0
         if dt > 0.5 or n >= w * h:
-            n = int(min(w * h, max(1024, n * args.ref_step_seconds / max(dt, 1e-3))))
+            n = int(min(w * h, max(min(1024, w * h), n * args.ref_step_seconds / max(dt, 1e-3))))
             break
         n = min(w * h, n * 4)
     times, segs = [], []
@@ -256,6 +261,11 @@ def run_reference(args, rank: int, world: int) -> None:
     total = sum(times)
     value = n * args.steps / total
     cfg = workload_config(args, len(scene.triangles), world)
+    if name != args.workload:
+        cfg["scene"] = name
+        cfg["workload"] = (f"{cfg['workload']} -- rendered as its reference-lobe variant "
+                           f"{name!r} (same geometry and camera; the reference has no coat, "
+                           f"glass or HDR environment)")
     sample = (f"each step: {n} random pixels x 1 sample of the {w}x{h} frame "
               f"({n / (w * h) / args.spp:.2e} of the full {args.spp}-spp workload)")
     line = {
@@ -271,21 +281,38 @@ def run_reference(args, rank: int, world: int) -> None:
     print(json.dumps(line), flush=True)
 
 
-def pinned_copy(a):
-    import torch
-    a = np.ascontiguousarray(a)
-    t = torch.empty(a.shape, dtype=torch.from_numpy(a[:0]).dtype, pin_memory=True)
-    out = t.numpy()
-    out[...] = a
-    return out, t
+def trace_source_sha() -> str:
+    """Hash of the trace kernel's sources: ties committed ncu figures to the
+    kernel version that is timed."""
+    import hashlib
+    h = hashlib.sha256()
+    for f in ("lt_traverse.cuh", "lt_device.cuh", "lt_kernels.cu", "lt_kernels.h"):
+        h.update((ROOT / "paper_2407_19977_b200" / "csrc" / f).read_bytes())
+    return h.hexdigest()[:16]
+
+
+def ncu_trace_figures(workload: str):
+    """Per-ray traffic per memory level and unit utilisations of k_trace
+    from the committed ncu capture (profiles/trace_ncu.json, written by
+    tools/trace_ncu.py), if it was taken on the kernel sources timed here."""
+    f = ROOT / "profiles" / "trace_ncu.json"
+    if not f.exists():
+        return None, "no profiles/trace_ncu.json"
+    d = json.loads(f.read_text()).get(workload)
+    if not d:
+        return None, f"no ncu capture for {workload!r}"
+    if d.get("source_sha") != trace_source_sha():
+        return None, (f"stale: ncu capture of kernel sources {d.get('source_sha')}, timed "
+                      f"{trace_source_sha()}")
+    return d, d.get("source")
 
 
 def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     import torch
     import torch.distributed as dist
 
-    from paper_2407_19977_b200 import RenderSettings, render_progressive
-    from paper_2407_19977_b200._lib import LT_FLAG_COUNT, LT_FLAG_PROFILE
+    from paper_2407_19977_b200 import RenderSettings, build_bvh, render_progressive
+    from paper_2407_19977_b200._lib import LT_FLAG_COUNT, LT_FLAG_PROFILE, read_bandwidth
     from paper_2407_19977_b200.device import DeviceScene
     from paper_2407_19977_b200.distributed import merge_tiles, render_distributed
     from paper_2407_19977_b200.integrator import Accumulator, render_pass_device
@@ -295,156 +322,192 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     scene, bvh = build_workload(args)
     settings = RenderSettings(samples_per_pixel=args.spp, max_depth=args.depth,
                               rr_start_depth=args.rr_start, seed=args.seed)
-    # bandwidth probes before any scene sets a persisting-L2 carve-out
-    from paper_2407_19977_b200._lib import read_bandwidth
     l2_gbs = read_bandwidth(local_rank, 32 << 20, 10)      # 32 MB: L2-resident
     hbm_probe = read_bandwidth(local_rank, 4 << 30, 5)      # 4 GB: HBM
-    ds = DeviceScene(scene, bvh, device=local_rank)
-    cam = scene.camera
-    acc = Accumulator(cam.width, cam.height, local_rank)
     shard = (rank, world, args.tile) if world > 1 else None
     stream = torch.cuda.current_stream(dev)
+    samples_per_step = args.width * args.height * args.spp
 
     def barrier():
         if world > 1:
             dist.barrier()
 
-    def step(flags, spp=None):
-        acc.sum.zero_()
-        acc.valid.zero_()
-        acc.invalid.zero_()
-        render_pass_device(ds, cam, settings, acc, 0, spp or args.spp, flags=flags | args.flags,
-                           shard=shard, max_batch_paths=args.batch_paths, stream=stream)
+    def max_over_ranks(x: float) -> float:
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
         if world > 1:
-            merge_tiles(acc, dst=0)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
 
-    # untimed: work counters for the roofline (same paths, reduced spp)
-    count_spp = min(args.spp, 16)
-    step(LT_FLAG_COUNT, count_spp)
+    def sum_over_ranks(x: float) -> float:
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    def stepper(ds_, acc_):
+        def step(flags, spp=None):
+            acc_.sum.zero_()
+            acc_.valid.zero_()
+            acc_.invalid.zero_()
+            render_pass_device(ds_, ds_.camera, settings, acc_, 0, spp or args.spp,
+                               flags=flags | args.flags, shard=shard,
+                               max_batch_paths=args.batch_paths, stream=stream)
+            if world > 1:
+                merge_tiles(acc_, dst=0)
+        return step
+
+    def timed(step, n, flags, sampler=None):
+        """n steps between CUDA events on the launching stream, barrier +
+        synchronize on both sides; returns the max over ranks in ms."""
+        torch.cuda.synchronize(dev)
+        barrier()
+        if sampler:
+            sampler.start()
+            time.sleep(0.3)
+        torch.cuda.synchronize(dev)
+        barrier()
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for _ in range(n):
+            step(flags)
+        ev1.record(stream)
+        torch.cuda.synchronize(dev)
+        barrier()
+        clocks = sampler.stop() if sampler else None
+        return max_over_ranks(ev0.elapsed_time(ev1)), clocks
+
+    def e2e_of(scene_, bvh_, n):
+        """The metric through the public API, as a luxtrace caller makes it:
+        the scene's plain (pageable) numpy arrays uploaded by every call,
+        the image back as float64 means; wall clock, max over ranks."""
+        def call():
+            if world > 1:
+                return render_distributed(scene_, settings, bvh_, tile_size=args.tile,
+                                          device=local_rank)
+            return render_progressive(scene_, settings, bvh=bvh_, device=local_rank)
+        call()
+        torch.cuda.synchronize(dev)
+        barrier()
+        t0 = time.perf_counter()
+        phases = []
+        for _ in range(n):
+            res = call()
+            if res is not None and hasattr(res, "timings"):
+                phases.append(res.timings)
+        torch.cuda.synchronize(dev)
+        el = max_over_ranks(time.perf_counter() - t0)
+        env = scene_.environment
+        h2d = env.texels.nbytes if getattr(env, "texels", None) is not None else 0
+        h2d += sum(getattr(scene_.triangles, nm).nbytes for nm in
+                   ["v0", "v1", "v2", "n0", "n1", "n2", "material_index"])
+        h2d += sum(getattr(bvh_, nm).nbytes for nm in
+                   ["bounds_min", "bounds_max", "left_child", "right_child", "first_triangle",
+                    "triangle_count", "triangle_order"])
+        return {"value": samples_per_step * n / el, "unit": UNIT,
+                "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(args.width * args.height * (3 * 8 + 8))
+                if rank == 0 else 0,
+                "steps": n, "ms_per_step": 1e3 * el / n,
+                "phases_ms": {k: statistics.mean(p[k] for p in phases) for k in phases[0]}
+                if phases else None,
+                "api": "render_progressive(scene, settings, bvh) (render_distributed for N>1): "
+                       "scene upload from the caller's pageable numpy arrays + BVH flatten + "
+                       "render + image D2H, wall clock"}
+
+    ds = DeviceScene(scene, bvh, device=local_rank)
+    acc = Accumulator(scene.camera.width, scene.camera.height, local_rank)
+    step = stepper(ds, acc)
+
+    # untimed: work counters (same paths, reduced spp)
+    step(LT_FLAG_COUNT, min(args.spp, 16))
     torch.cuda.synchronize(dev)
     cst = ds.stats()
     slab_per_ray = cst["slab_tests"] / max(1, cst["rays"])
     tri_per_ray = cst["tri_tests"] / max(1, cst["rays"])
-    # 32 B per child-box test (a 64 B node = 2 tests), 48 B per
-    # triangle test, and the ray record: 32 B in + 16 B hit out
+    # SURVEY §8(d): 32 B per child-box test, 48 B per triangle test, 32 B ray
+    # in + 16 B hit out
     bytes_per_ray = 32.0 * slab_per_ray + 48.0 * tri_per_ray + 48.0
 
     for _ in range(args.warmup):
         step(0)
-    torch.cuda.synchronize(dev)
-    barrier()
-    sampler = ClockSampler(local_rank) if rank == 0 else None
-    if sampler:
-        sampler.start()
-        time.sleep(0.3)
-    torch.cuda.synchronize(dev)
-    barrier()
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
-    ev0.record(stream)
-    for _ in range(args.steps):
-        step(LT_FLAG_PROFILE)
-    ev1.record(stream)
-    torch.cuda.synchronize(dev)
-    barrier()
-    clocks = sampler.stop() if sampler else None
-    ms = ev0.elapsed_time(ev1)
+    ms_max, clocks = timed(step, args.steps, LT_FLAG_PROFILE,
+                           ClockSampler(local_rank) if rank == 0 else None)
     st = ds.stats()    # the last timed step on this rank
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    rays = torch.tensor([st["rays"]], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dist.all_reduce(rays, op=dist.ReduceOp.SUM)
-    ms_max = float(t.item())
-    rays_per_step = float(rays.item())
-    samples_per_step = args.width * args.height * args.spp
+    rays_per_step = sum_over_ranks(st["rays"])
     value = samples_per_step * args.steps / (ms_max / 1e3)
     mrays = rays_per_step * args.steps / (ms_max / 1e3) / 1e6
 
-    # roofline of the dominant kernel (closest-hit traversal), this rank
+    # roofline of the dominant kernel (closest-hit traversal), this rank:
+    # measured bytes per memory level (ncu, same kernel sources) over the
+    # live trace time, against the measured HBM and L2 rates
     peak, peak_src = measured_peak()
-    from paper_2407_19977_b200._lib import read_bandwidth
     trace_ms = st["trace_ms"]
     launches = max(1, st["trace_launches"])
-    achieved = (st["rays"] * bytes_per_ray) / (trace_ms / 1e3) / 1e9 if trace_ms > 0 else None
-    traffic_per_ray, traffic_src, limiter = ncu_traffic(args.workload)
+    rays_s = st["rays"] / (trace_ms / 1e3) if trace_ms > 0 else None
+    ncu, ncu_src = ncu_trace_figures(args.workload)
+    level = {}
+    if ncu and rays_s:
+        level = {
+            "hbm": {"achieved": ncu["dram_bytes_per_ray"] * rays_s / 1e9, "peak": peak,
+                    "unit": "GB/s", "peak_source": peak_src},
+            "l2": {"achieved": ncu["l2_bytes_per_ray"] * rays_s / 1e9, "peak": l2_gbs,
+                   "unit": "GB/s", "peak_source": "measured in this run (32 MB streaming "
+                                                 "read, lt_read_bandwidth)"},
+        }
+        for v in level.values():
+            v["frac"] = v["achieved"] / v["peak"]
     roofline = {
-        "bound": "hbm", "kernel": "k_trace (closest-hit BVH traversal)",
-        "achieved": achieved, "peak": peak, "unit": "GB/s",
-        "frac": achieved / peak if achieved else None,
-        "traffic": (traffic_per_ray * st["rays"] / launches) if traffic_per_ray else None,
-        "algorithmic_bytes_per_launch": st["rays"] * bytes_per_ray / launches,
-        "bytes_per_ray": bytes_per_ray, "slab_tests_per_ray": slab_per_ray,
+        "bound": "l2", "kernel": "k_trace (closest-hit BVH traversal)",
+        "achieved": level["l2"]["achieved"] if level else None,
+        "peak": l2_gbs, "unit": "GB/s",
+        "frac": level["l2"]["frac"] if level else None,
+        "traffic": (ncu["dram_bytes_per_ray"] * st["rays"] / launches) if ncu else None,
+        "levels": level or None,
+        "binding_unit": ({"unit": "L1 data pipe (LSU wavefronts)",
+                          "l1_wavefront_pct": ncu.get("l1_wavefront_pct"),
+                          "fma_pipe_pct": ncu.get("fma_pipe_pct"),
+                          "alu_pipe_pct": ncu.get("alu_pipe_pct"),
+                          "issue_active_pct": ncu.get("issue_active_pct"),
+                          "simt_threads_per_warp_instruction": ncu.get("simt_threads")}
+                         if ncu else None),
+        "ncu_source": ncu_src, "kernel_source_sha": trace_source_sha(),
+        "algorithmic_bytes_per_ray": bytes_per_ray, "slab_tests_per_ray": slab_per_ray,
         "tri_tests_per_ray": tri_per_ray, "trace_launches_per_step": launches,
-        "trace_ms_per_step": trace_ms, "trace_share_of_step": trace_ms / (ms / args.steps),
-        "peak_source": peak_src, "traffic_source": traffic_src,
-        "l2_read_gbs_measured": l2_gbs, "frac_of_l2": achieved / l2_gbs if achieved else None,
+        "trace_ms_per_step": trace_ms, "trace_share_of_step": trace_ms / (ms_max / args.steps),
         "hbm_read_gbs_probe": hbm_probe,
-        "ncu_limiter": limiter,
-        "note": "the traversal set (wide nodes + leaf triangles, ~70 MB at 1 M tris) is mostly "
-                "served from L2 (ncu dram traffic per launch is ~5% of the algorithmic bytes), "
-                "so algorithmic bytes per second can exceed the HBM copy peak; frac_of_l2 is "
-                "the fraction of the measured L2 streaming-read rate; the unit that bounds "
-                "the kernel is the L1 data pipe (ncu_limiter: ~71-75 % of its wavefront rate, "
-                "one wavefront per lane per node load)",
+        "note": "frac = measured L2 bytes (ncu lts__t_bytes per ray x live ray rate) over the "
+                "measured L2 streaming-read rate; the traversal set is served from L2/L1, so HBM "
+                "carries little of it (levels.hbm); the unit that bounds k_trace is the L1 data "
+                "pipe: one wavefront per lane per divergent node load (binding_unit)",
     }
 
-    # end to end through the public API: scene upload (pinned host arrays),
-    # render, merge, image back to the host
-    e2e = None
-    if not args.no_e2e:
-        keep = []
+    e2e = e2e_of(scene, bvh, max(1, min(args.steps, 5))) if not args.no_e2e else None
 
-        def pin(obj, names):
-            for nm in names:
-                arr, t_ = pinned_copy(getattr(obj, nm))
-                keep.append(t_)
-                setattr(obj, nm, arr)
-        pin(scene.triangles, ["v0", "v1", "v2", "n0", "n1", "n2", "material_index"])
-        pin(bvh, ["bounds_min", "bounds_max", "left_child", "right_child", "first_triangle",
-                  "triangle_count", "triangle_order"])
-        env = scene.environment
-        if getattr(env, "texels", None) is not None:
-            pin(env, ["texels"])  # the HDR sky (float32 texels)
-        h2d = env.texels.nbytes if getattr(env, "texels", None) is not None else 0
-        h2d += sum(getattr(scene.triangles, nm).nbytes for nm in
-                   ["v0", "v1", "v2", "n0", "n1", "n2", "material_index"])
-        h2d += sum(getattr(bvh, nm).nbytes for nm in
-                   ["bounds_min", "bounds_max", "left_child", "right_child", "first_triangle",
-                    "triangle_count", "triangle_order"])
-        d2h = args.width * args.height * (3 * 8 + 8) if rank == 0 else 0
-
-        def e2e_step():
-            if world > 1:
-                return render_distributed(scene, settings, bvh, tile_size=args.tile,
-                                          device=local_rank)
-            return render_progressive(scene, settings, bvh=bvh, device=local_rank)
-        e2e_step()
-        torch.cuda.synchronize(dev)
-        barrier()
-        t0 = time.perf_counter()
-        n_e2e = max(1, min(args.steps, 3))
-        phases = []
-        for _ in range(n_e2e):
-            res = e2e_step()
-            if res is not None and hasattr(res, "timings"):
-                phases.append(res.timings)
-        torch.cuda.synchronize(dev)
-        el = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(el, op=dist.ReduceOp.MAX)
-        e2e = {"value": samples_per_step * n_e2e / float(el.item()), "unit": UNIT,
-               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "steps": n_e2e, "ms_per_step": 1e3 * float(el.item()) / n_e2e,
-               "phases_ms": {k: statistics.mean(p[k] for p in phases) for k in phases[0]}
-               if phases else None,
-               "api": "render_progressive(scene, settings, bvh) (render_distributed for N>1): "
-                      "scene upload from pinned host arrays + BVH flatten + render + image "
-                      "D2H, wall clock"}
+    # the same frame on the scene the CPU reference renders (the workload's
+    # reference-lobe variant), device-timed and end to end: the like-for-like
+    # comparison with `--impl reference`
+    variant = None
+    vname = REFERENCE_VARIANT.get(args.workload)
+    if vname and not args.no_variant:
+        import workloads
+        vscene = workloads.scene_by_name(vname, width=args.width, height=args.height)
+        vbvh = build_bvh(vscene.triangles, leaf_size=args.bvh_leaf, bins=args.bvh_bins)
+        vds = DeviceScene(vscene, vbvh, device=local_rank)
+        vstep = stepper(vds, acc)
+        for _ in range(2):
+            vstep(0)
+        n_v = max(1, min(args.steps, 10))
+        vms, _ = timed(vstep, n_v, 0)
+        variant = {"workload": vname, "value": samples_per_step * n_v / (vms / 1e3),
+                   "unit": UNIT, "steps": n_v, "ms_per_step": vms / n_v,
+                   "e2e": e2e_of(vscene, vbvh, max(1, min(args.steps, 3)))
+                   if not args.no_e2e else None}
+        vds.close()
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_baseline(scene, bvh, args, args.cpu_seconds)
+        cpu = cpu_baseline(args, args.cpu_seconds)
 
     if rank == 0:
         line = {
@@ -454,10 +517,23 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
             "dtype": "fp32", "data": "synthetic",
             "config": workload_config(args, len(scene.triangles), world),
             "mrays_per_s": mrays, "rays_per_step": rays_per_step,
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "reference_variant": variant, "parity": parity_summary(), "clocks": clocks,
             "gpu_launches": int(st["kernel_launches"] * args.steps),
         }
         print(json.dumps(line), flush=True)
+
+
+def parity_summary():
+    """The committed parity record (profiles/parity_r02.json, written by the
+    -m gpu parity tests on the B200): agreement fractions and id-mismatch
+    counts per fixture."""
+    f = ROOT / "profiles" / "parity_r02.json"
+    if not f.exists():
+        return None
+    d = json.loads(f.read_text())
+    return {"source": "profiles/parity_r02.json", "entries": len(d.get("entries", {})),
+            "headline": d.get("headline")}
 
 
 def main():

@@ -11,7 +11,7 @@ import numpy as np
 import luxtrace as lx
 sys.path.insert(0, "/root/repo/tests/golden")
 from make_golden import to_ref_scene
-from paper_2407_19977_b200.procgen import scene_by_name
+from workloads import scene_by_name
 from paper_2407_19977_b200 import camera_pack
 from oracle.oracle import OracleScene
 W, H, SPP = 240, 135, 8

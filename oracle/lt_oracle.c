@@ -951,3 +951,202 @@ void oc_primary_rays(const int64_t *pixels, int64_t n, int64_t sample, const dou
     origins[3 * i + 2] = cam[2];
   }
 }
+
+/* ---------------------------------------------------------- bvh.py build */
+
+/* _triangle_bounds_arrays (bvh.py:57-77) + _build_kernel (bvh.py:85-262):
+ * the reference's single-threaded binned-SAH build restated in C so the CPU
+ * baseline (bench.py --impl reference) builds its tree without the product
+ * library.  Output arrays are caller-owned, sized for 2n nodes; returns the
+ * node count, or -1 on an allocation failure. */
+static double oc_half_area(double dx, double dy, double dz) { return dx * dy + dx * dz + dy * dz; }
+
+#define OC_BOUNDS_PADDING 1e-7  /* geometry.py:19 */
+#define OC_MAX_TREE_DEPTH 60    /* bvh.py:26 */
+
+int64_t oc_build_bvh(const double *v0, const double *v1, const double *v2, int64_t n,
+                     int32_t leaf_size, int32_t n_bins, double *bmin, double *bmax,
+                     int32_t *left, int32_t *right, int32_t *first, int32_t *count,
+                     int32_t *order, int64_t *leaf_count_out, int64_t *max_depth_out) {
+  double *tb_min = malloc(sizeof(double) * 3 * (size_t)(n > 0 ? n : 1));
+  double *tb_max = malloc(sizeof(double) * 3 * (size_t)(n > 0 ? n : 1));
+  double *cent = malloc(sizeof(double) * 3 * (size_t)(n > 0 ? n : 1));
+  int64_t *bin_count = malloc(sizeof(int64_t) * (size_t)n_bins);
+  double *bin_min = malloc(sizeof(double) * 3 * (size_t)n_bins);
+  double *bin_max = malloc(sizeof(double) * 3 * (size_t)n_bins);
+  double *sweep_area = malloc(sizeof(double) * (size_t)n_bins);
+  int64_t *sweep_count = malloc(sizeof(int64_t) * (size_t)n_bins);
+  int64_t (*stack)[4] = malloc(sizeof(int64_t) * 4 * (OC_MAX_TREE_DEPTH + 8));
+  int64_t n_nodes = -1;
+  if (!tb_min || !tb_max || !cent || !bin_count || !bin_min || !bin_max || !sweep_area ||
+      !sweep_count || !stack)
+    goto done;
+  for (int64_t i = 0; i < n; ++i) {
+    double ext = 0.0;
+    for (int a = 0; a < 3; ++a) {
+      double p = v0[3 * i + a], q = v1[3 * i + a], r = v2[3 * i + a];
+      double lo = p < (q < r ? q : r) ? p : (q < r ? q : r);
+      double hi = p > (q > r ? q : r) ? p : (q > r ? q : r);
+      tb_min[3 * i + a] = lo;
+      tb_max[3 * i + a] = hi;
+      if (hi - lo > ext) ext = hi - lo;
+    }
+    double pad = OC_BOUNDS_PADDING * ext;
+    for (int a = 0; a < 3; ++a) {
+      tb_min[3 * i + a] -= pad;
+      tb_max[3 * i + a] += pad;
+      cent[3 * i + a] = 0.5 * (tb_min[3 * i + a] + tb_max[3 * i + a]);
+    }
+  }
+  for (int64_t i = 0; i < 2 * n; ++i) {
+    left[i] = -1;
+    right[i] = -1;
+    first[i] = 0;
+    count[i] = 0;
+  }
+  for (int64_t i = 0; i < n; ++i) order[i] = (int32_t)i;
+  int64_t sp = 0, leaf_count = 0, max_depth = 0;
+  stack[0][0] = 0; stack[0][1] = 0; stack[0][2] = n; stack[0][3] = 0;
+  sp = 1;
+  n_nodes = 1;
+  while (sp > 0) {
+    --sp;
+    const int64_t node = stack[sp][0], f = stack[sp][1], c = stack[sp][2], depth = stack[sp][3];
+    if (depth > max_depth) max_depth = depth;
+    double nmin[3] = {INFINITY, INFINITY, INFINITY}, nmax[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int64_t k = f; k < f + c; ++k) {
+      const int64_t ti = order[k];
+      for (int a = 0; a < 3; ++a) {
+        if (tb_min[3 * ti + a] < nmin[a]) nmin[a] = tb_min[3 * ti + a];
+        if (tb_max[3 * ti + a] > nmax[a]) nmax[a] = tb_max[3 * ti + a];
+      }
+    }
+    for (int a = 0; a < 3; ++a) {
+      bmin[3 * node + a] = nmin[a];
+      bmax[3 * node + a] = nmax[a];
+    }
+    const double parent_area =
+        2.0 * oc_half_area(nmax[0] - nmin[0], nmax[1] - nmin[1], nmax[2] - nmin[2]);
+    int make_leaf = c <= leaf_size || depth >= OC_MAX_TREE_DEPTH || parent_area <= 0.0;
+    int64_t mid = -1;
+    if (!make_leaf) {
+      double cmin[3] = {INFINITY, INFINITY, INFINITY}, cmax[3] = {-INFINITY, -INFINITY, -INFINITY};
+      for (int64_t k = f; k < f + c; ++k) {
+        const int64_t ti = order[k];
+        for (int a = 0; a < 3; ++a) {
+          if (cent[3 * ti + a] < cmin[a]) cmin[a] = cent[3 * ti + a];
+          if (cent[3 * ti + a] > cmax[a]) cmax[a] = cent[3 * ti + a];
+        }
+      }
+      int axis = 0;
+      double ext = cmax[0] - cmin[0];
+      if (cmax[1] - cmin[1] > ext) { axis = 1; ext = cmax[1] - cmin[1]; }
+      if (cmax[2] - cmin[2] > ext) { axis = 2; ext = cmax[2] - cmin[2]; }
+      const double cmin_axis = cmin[axis];
+      if (ext > 0.0) {
+        const double scale = n_bins / ext;
+        for (int b = 0; b < n_bins; ++b) {
+          bin_count[b] = 0;
+          for (int a = 0; a < 3; ++a) {
+            bin_min[3 * b + a] = INFINITY;
+            bin_max[3 * b + a] = -INFINITY;
+          }
+        }
+        for (int64_t k = f; k < f + c; ++k) {
+          const int64_t ti = order[k];
+          int64_t b = (int64_t)((cent[3 * ti + axis] - cmin_axis) * scale);
+          if (b >= n_bins) b = n_bins - 1;
+          bin_count[b] += 1;
+          for (int a = 0; a < 3; ++a) {
+            if (tb_min[3 * ti + a] < bin_min[3 * b + a]) bin_min[3 * b + a] = tb_min[3 * ti + a];
+            if (tb_max[3 * ti + a] > bin_max[3 * b + a]) bin_max[3 * b + a] = tb_max[3 * ti + a];
+          }
+        }
+        double a0[3] = {INFINITY, INFINITY, INFINITY}, a1[3] = {-INFINITY, -INFINITY, -INFINITY};
+        int64_t acc_n = 0;
+        for (int b = 0; b < n_bins - 1; ++b) {
+          if (bin_count[b] > 0) {
+            for (int a = 0; a < 3; ++a) {
+              if (bin_min[3 * b + a] < a0[a]) a0[a] = bin_min[3 * b + a];
+              if (bin_max[3 * b + a] > a1[a]) a1[a] = bin_max[3 * b + a];
+            }
+            acc_n += bin_count[b];
+          }
+          sweep_count[b] = acc_n;
+          sweep_area[b] = acc_n > 0 ? 2.0 * oc_half_area(a1[0] - a0[0], a1[1] - a0[1], a1[2] - a0[2])
+                                    : 0.0;
+        }
+        double best_cost = INFINITY;
+        int best_plane = -1;
+        for (int a = 0; a < 3; ++a) {
+          a0[a] = INFINITY;
+          a1[a] = -INFINITY;
+        }
+        acc_n = 0;
+        for (int b = n_bins - 1; b > 0; --b) {
+          if (bin_count[b] > 0) {
+            for (int a = 0; a < 3; ++a) {
+              if (bin_min[3 * b + a] < a0[a]) a0[a] = bin_min[3 * b + a];
+              if (bin_max[3 * b + a] > a1[a]) a1[a] = bin_max[3 * b + a];
+            }
+            acc_n += bin_count[b];
+          }
+          const int plane = b - 1;
+          const int64_t ln = sweep_count[plane], rn = acc_n;
+          if (ln > 0 && rn > 0) {
+            const double right_area = 2.0 * oc_half_area(a1[0] - a0[0], a1[1] - a0[1], a1[2] - a0[2]);
+            /* TRAVERSAL_COST + INTERSECT_COST * (...) / parent_area, both costs 1.0 */
+            const double cost = 1.0 + 1.0 * (sweep_area[plane] * (double)ln + right_area * (double)rn) /
+                                          parent_area;
+            if (cost < best_cost) {
+              best_cost = cost;
+              best_plane = plane;
+            }
+          }
+        }
+        if (best_plane >= 0 && best_cost < 1.0 * (double)c) {
+          int64_t i = f, j = f + c - 1;
+          while (i <= j) {
+            const int64_t ti = order[i];
+            int64_t b = (int64_t)((cent[3 * ti + axis] - cmin_axis) * scale);
+            if (b >= n_bins) b = n_bins - 1;
+            if (b <= best_plane) {
+              ++i;
+            } else {
+              const int32_t tmp = order[i];
+              order[i] = order[j];
+              order[j] = tmp;
+              --j;
+            }
+          }
+          mid = i;
+          if (mid <= f || mid >= f + c) mid = f + c / 2;
+        } else {
+          make_leaf = 1;
+        }
+      } else {
+        mid = f + c / 2;
+      }
+    }
+    if (make_leaf) {
+      first[node] = (int32_t)f;
+      count[node] = (int32_t)c;
+      ++leaf_count;
+      continue;
+    }
+    const int64_t lchild = n_nodes, rchild = n_nodes + 1;
+    n_nodes += 2;
+    left[node] = (int32_t)lchild;
+    right[node] = (int32_t)rchild;
+    stack[sp][0] = rchild; stack[sp][1] = mid; stack[sp][2] = f + c - mid; stack[sp][3] = depth + 1;
+    ++sp;
+    stack[sp][0] = lchild; stack[sp][1] = f; stack[sp][2] = mid - f; stack[sp][3] = depth + 1;
+    ++sp;
+  }
+  if (leaf_count_out) *leaf_count_out = leaf_count;
+  if (max_depth_out) *max_depth_out = max_depth;
+done:
+  free(tb_min); free(tb_max); free(cent); free(bin_count); free(bin_min); free(bin_max);
+  free(sweep_area); free(sweep_count); free(stack);
+  return n_nodes;
+}

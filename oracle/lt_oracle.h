@@ -73,6 +73,13 @@ void oc_brute_force_batch(const oc_scene *s, const double *origins, const double
                           int64_t n, double t_min, double t_max, int64_t *idx, double *t,
                           int n_threads);
 
+/* ---- bvh.py build: _triangle_bounds_arrays + _build_kernel (bvh.py:57-262);
+ * node arrays sized 2n (bounds 2n*3), order n; returns the node count ---- */
+int64_t oc_build_bvh(const double *v0, const double *v1, const double *v2, int64_t n,
+                     int32_t leaf_size, int32_t n_bins, double *bmin, double *bmax,
+                     int32_t *left, int32_t *right, int32_t *first, int32_t *count,
+                     int32_t *order, int64_t *leaf_count, int64_t *max_depth);
+
 /* ---- material.py ---- */
 /* params: [bw, bcr, bcg, bcb, m, sw, scr, scg, scb, rough, ior,
  *          coat_w, coat_rough, coat_ior, ccr, ccg, ccb, tr_w, tcr, tcg, tcb] (21) */

@@ -9,6 +9,7 @@ itself (tests/golden/make_golden.py).
 from __future__ import annotations
 
 import ctypes as C
+import math
 import os
 import subprocess
 from pathlib import Path
@@ -92,6 +93,9 @@ def lib():
                                        C.c_int]
         h.oc_primary_rays.argtypes = [_lp, C.c_int64, C.c_int64, _dp, C.c_int32, C.c_int32,
                                       C.c_uint64, _dp, _dp]
+        h.oc_build_bvh.restype = C.c_int64
+        h.oc_build_bvh.argtypes = [_dp, _dp, _dp, C.c_int64, C.c_int32, C.c_int32, _dp, _dp,
+                                   _ip, _ip, _ip, _ip, _ip, _lp, _lp]
         _lib = h
     return _lib
 
@@ -122,6 +126,58 @@ def seed_stream(pixel: int, sample: int, seed: int) -> tuple[int, int]:
     s, i = C.c_uint64(), C.c_uint64()
     lib().oc_seed_stream(pixel, sample, seed & (2**64 - 1), C.byref(s), C.byref(i))
     return s.value, i.value
+
+
+# ------------------------------------------------------------------ camera
+
+def camera_pack(camera) -> np.ndarray:
+    """_camera_pack (integrator.py:75-83): [position, forward, right, up,
+    tan(fov/2), aspect], the reference's numpy operations in order."""
+    def unit(v):
+        return v / np.linalg.norm(v)
+    position = np.asarray(camera.position, dtype=np.float64)
+    forward = unit(np.asarray(camera.look_at, dtype=np.float64) - position)
+    right = unit(np.cross(forward, np.asarray(camera.up, dtype=np.float64)))
+    up = np.cross(right, forward)
+    tan_half = math.tan(math.radians(camera.vertical_fov_deg) * 0.5)
+    return np.ascontiguousarray(np.concatenate([position, forward, right, up,
+                                                [tan_half, camera.width / camera.height]]))
+
+
+# ------------------------------------------------------------------ bvh build
+
+class OracleBvh:
+    """The reference's Bvh arrays (bvh.py:38-50) from oc_build_bvh, the C
+    restatement of build_bvh (bvh.py:286-298)."""
+
+    def __init__(self, bounds_min, bounds_max, left_child, right_child, first_triangle,
+                 triangle_count, triangle_order, leaf_count, max_depth):
+        self.bounds_min, self.bounds_max = bounds_min, bounds_max
+        self.left_child, self.right_child = left_child, right_child
+        self.first_triangle, self.triangle_count = first_triangle, triangle_count
+        self.triangle_order = triangle_order
+        self.leaf_count, self.max_depth = leaf_count, max_depth
+
+
+def build_bvh(triangles, leaf_size: int = 4, bins: int = 12) -> OracleBvh:
+    v0, v1, v2 = (np.ascontiguousarray(getattr(triangles, k), dtype=np.float64).reshape(-1, 3)
+                  for k in ("v0", "v1", "v2"))
+    n = v0.shape[0]
+    if n == 0:
+        raise ValueError("empty scene")
+    m = 2 * n
+    bmin, bmax = np.empty((m, 3)), np.empty((m, 3))
+    ints = [np.empty(m, np.int32) for _ in range(4)]
+    order = np.empty(n, np.int32)
+    leaves, depth = C.c_int64(), C.c_int64()
+    nn = lib().oc_build_bvh(_p(v0, C.c_double), _p(v1, C.c_double), _p(v2, C.c_double), n,
+                            int(leaf_size), int(bins), _p(bmin, C.c_double),
+                            _p(bmax, C.c_double), *[_p(a, C.c_int32) for a in ints],
+                            _p(order, C.c_int32), C.byref(leaves), C.byref(depth))
+    if nn < 0:
+        raise MemoryError("oc_build_bvh: allocation failed")
+    return OracleBvh(bmin[:nn].copy(), bmax[:nn].copy(), *[a[:nn].copy() for a in ints], order,
+                     int(leaves.value), int(depth.value))
 
 
 # ------------------------------------------------------------------ materials

@@ -17,7 +17,7 @@ from .device import DeviceScene
 from .integrator import (RenderResult, RenderSettings, environment_radiance,
                          generate_camera_ray, render_image, render_pass, render_progressive,
                          trace_radiance, trace_radiance_batch)
-from .procgen import bumpy_sphere, cornell_box, pushbutton, sphere_on_plane, synthetic_hdr
+from .procgen import bumpy_sphere, bumpy_sphere_glb, icosphere, icosphere_glb
 from .ingest import (MaterialMap, RenderConfig, flatten_scene, generate_smooth_normals, load_gltf,
                      load_render_config, load_scene, save_glb)
 
@@ -34,7 +34,7 @@ __all__ = [
     "RenderResult", "RenderSettings", "environment_radiance", "generate_camera_ray",
     "render_image", "render_pass", "render_progressive", "trace_radiance",
     "trace_radiance_batch",
-    "bumpy_sphere", "cornell_box", "pushbutton", "sphere_on_plane", "synthetic_hdr",
+    "bumpy_sphere", "bumpy_sphere_glb", "icosphere", "icosphere_glb",
     "MaterialMap", "RenderConfig", "flatten_scene", "generate_smooth_normals", "load_gltf",
     "load_render_config", "load_scene", "save_glb",
 ]

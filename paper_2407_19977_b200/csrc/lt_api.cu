@@ -171,6 +171,13 @@ struct DeviceGuard {
 // overlaps the other lane's work; each lane owns its queues.
 constexpr int kLanes = 4;          // upper bound; LT_LANES picks 1..kLanes (default 2)
 constexpr int kDefaultLanes = 2;
+// pinned staging ring for pageable scene arrays: kRingWorkers host threads,
+// two kRingSlot slots each
+constexpr int kRingWorkers = 6;
+constexpr int kRingSlots = 2 * kRingWorkers;
+constexpr size_t kRingSlot = size_t(4) << 20;
+// resident buffers of destroyed scenes kept for reuse
+constexpr size_t kCacheBytes = size_t(2) << 30;
 
 struct Lane {
   int64_t cap = 0;
@@ -203,7 +210,173 @@ struct Workspace {
   // copy (stage_ev: the last copy out of it; guarded by upload_mu)
   HostBuf stage;
   cudaEvent_t stage_ev = nullptr;
+  // scene creation is serialized per device (create_mu): the float64 / int32
+  // upload temporaries live in one grow-only device scratch buffer (no
+  // stream-ordered pool growth per scene: a pool that had to map new memory
+  // for a 150 MB scene stalled creation by up to ~0.5 s on the B200 box), and
+  // pageable caller arrays are staged through a pinned ring (ring_ev[k]: the
+  // last copy out of slot k)
+  std::mutex create_mu;
+  DevBuf scratch;
+  HostBuf ring;
+  cudaEvent_t ring_ev[kRingSlots] = {};
+  // resident buffers of destroyed scenes, reused by the next scene of a
+  // similar size (ev: the destroyed scene's last use); bounded by kCacheBytes
+  struct Cached {
+    void *p;
+    size_t bytes;
+    cudaEvent_t ev;
+  };
+  std::vector<Cached> cache;
+  std::mutex cache_mu;
+  cudaEvent_t scratch_ev = nullptr;  // the last read of `scratch`
 };
+
+// ---- host -> device copies for scene creation
+
+struct CopyItem {
+  void *dst;
+  const void *src;
+  size_t bytes;
+};
+
+// Page-locked host memory (cudaHostAlloc'd or registered): the copy engine
+// reads it directly.
+static bool host_pinned(const void *p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+// Host -> device copies of `items` on `st`.  Page-locked sources go straight
+// to the copy engine; pageable ones (plain numpy arrays, as luxtrace callers
+// pass them) are cut into kRingSlot chunks that kRingWorkers host threads
+// copy into the pinned ring, two slots per worker, each slot's copy-out
+// issued as soon as it is filled -- the host memcpy of one chunk overlaps
+// the DMA of the previous ones (~45 GB/s against 11 GB/s for the driver's
+// own pageable path, tools/h2d_probe.py).  Returns after the last copy is
+// enqueued.
+static int staged_h2d(Workspace &W, int device, const std::vector<CopyItem> &items,
+                      cudaStream_t st, int worker0 = 0, int max_workers = kRingWorkers) {
+  struct Chunk {
+    char *dst;
+    const char *src;
+    size_t bytes;
+  };
+  std::vector<Chunk> chunks;
+  for (const CopyItem &it : items) {
+    if (!it.bytes) continue;
+    if (host_pinned(it.src)) {
+      CK(cudaMemcpyAsync(it.dst, it.src, it.bytes, cudaMemcpyHostToDevice, st));
+      continue;
+    }
+    for (size_t off = 0; off < it.bytes; off += kRingSlot)
+      chunks.push_back(Chunk{static_cast<char *>(it.dst) + off,
+                             static_cast<const char *>(it.src) + off,
+                             std::min(kRingSlot, it.bytes - off)});
+  }
+  if (chunks.empty()) return LT_OK;
+  const int n_workers = (int)std::min<size_t>(max_workers, chunks.size());
+  std::vector<int> rc(n_workers, LT_OK);
+  std::vector<std::string> msg(n_workers);
+  auto work = [&](int w) {
+    cudaSetDevice(device);
+    int i = 0;
+    for (size_t c = w; c < chunks.size(); c += n_workers, ++i) {
+      const int slot = 2 * (worker0 + w) + (i & 1);
+      char *buf = W.ring.as<char>() + kRingSlot * slot;
+      cudaError_t e = cudaEventSynchronize(W.ring_ev[slot]);  // slot drained
+      if (e == cudaSuccess) {
+        std::memcpy(buf, chunks[c].src, chunks[c].bytes);
+        e = cudaMemcpyAsync(chunks[c].dst, buf, chunks[c].bytes, cudaMemcpyHostToDevice, st);
+      }
+      if (e == cudaSuccess) e = cudaEventRecord(W.ring_ev[slot], st);
+      if (e != cudaSuccess) {
+        rc[w] = lt_fail(LT_ERR_CUDA, "staged upload failed: %s", cudaGetErrorString(e));
+        msg[w] = g_last_error;
+        return;
+      }
+    }
+  };
+  std::vector<std::thread> th;
+  for (int w = 1; w < n_workers; ++w) th.emplace_back(work, w);
+  work(0);
+  for (auto &t : th) t.join();
+  for (int w = 0; w < n_workers; ++w)
+    if (rc[w] != LT_OK) {
+      g_last_error = msg[w];
+      return rc[w];
+    }
+  return LT_OK;
+}
+
+static int ensure_ring(Workspace &W) {
+  RET(W.ring.ensure(kRingSlot * kRingSlots));
+  for (int k = 0; k < kRingSlots; ++k)
+    if (!W.ring_ev[k]) CK(cudaEventCreateWithFlags(&W.ring_ev[k], cudaEventDisableTiming));
+  return LT_OK;
+}
+
+// A resident scene buffer: a cached block of a destroyed scene when one fits
+// (ordered after that scene's last use on `st`), else a new allocation.
+static int take_cached(Workspace &W, DevBuf &b, size_t want, cudaStream_t st) {
+  if (b.bytes >= want) return LT_OK;
+  {
+    std::lock_guard<std::mutex> lk(W.cache_mu);
+    int best = -1;
+    for (int i = 0; i < (int)W.cache.size(); ++i) {
+      const size_t sz = W.cache[i].bytes;
+      if (sz >= want && sz <= want + want / 2 + (size_t(16) << 20) &&
+          (best < 0 || sz < W.cache[best].bytes))
+        best = i;
+    }
+    if (best >= 0) {
+      b.release();
+      Workspace::Cached c = W.cache[best];
+      W.cache.erase(W.cache.begin() + best);
+      CK(cudaStreamWaitEvent(st, c.ev, 0));
+      cudaEventDestroy(c.ev);
+      b.p = c.p;
+      b.bytes = c.bytes;
+      return LT_OK;
+    }
+  }
+  return b.ensure(want);
+}
+
+// Park a destroyed scene's stream-ordered buffer for reuse (after its last
+// use on `st`); the oldest blocks are freed beyond kCacheBytes.
+static void park_cached(Workspace &W, DevBuf &b, cudaStream_t st) {
+  if (!b.p) return;
+  if (!b.stream_ordered) {
+    b.release();
+    return;
+  }
+  cudaEvent_t ev = nullptr;
+  if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventRecord(ev, st) != cudaSuccess) {
+    if (ev) cudaEventDestroy(ev);
+    b.release();
+    return;
+  }
+  std::lock_guard<std::mutex> lk(W.cache_mu);
+  W.cache.push_back(Workspace::Cached{b.p, b.bytes, ev});
+  b.p = nullptr;
+  b.bytes = 0;
+  size_t total = 0;
+  for (const auto &c : W.cache) total += c.bytes;
+  while (total > kCacheBytes && !W.cache.empty()) {
+    Workspace::Cached c = W.cache.front();
+    W.cache.erase(W.cache.begin());
+    cudaStreamWaitEvent(st, c.ev, 0);
+    cudaEventDestroy(c.ev);
+    cudaFreeAsync(c.p, st);
+    total -= c.bytes;
+  }
+}
 
 static Workspace *workspace_for(int device) {
   static std::mutex g_mu;
@@ -514,6 +687,10 @@ static void destroy_scene(lt_scene *s) {
     if (s->ws->last_use) cudaStreamWaitEvent(s->stream, s->ws->last_use, 0);
   }
   pt.mark("destroy: order after last pass");
+  if (s->stream && s->ws) {
+    park_cached(*s->ws, s->geo, s->stream);
+    park_cached(*s->ws, s->nodes2, s->stream);
+  }
   for (DevBuf *b : {&s->geo, &s->nodes2, &s->shade, &s->mats, &s->env, &s->ray_ctr,
                     &s->pix_list, &s->s_a, &s->s_b, &s->s_c, &s->s_d, &s->s_e, &s->s_f})
     b->release();
@@ -707,8 +884,12 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
   s->n_tris = n;
   pt.mark("stream + attributes");
 
-  // --- every upload that depends only on the description, enqueued first
-  // (pinned sources: asynchronous DMA)
+  // --- uploads.  Small scenes: every array through one pinned staging
+  // buffer and ONE copy.  Otherwise the arrays land in the workspace's
+  // device scratch (serialized by create_mu): page-locked sources by direct
+  // DMA, pageable ones through the pinned ring (staged_h2d); the BVH arrays
+  // first, then the triangle arrays on a host thread + the side stream
+  // while the device lays the tree out.
   TmpBuf t_v[6], t_mat, t_order, t_end, t_bmin, t_bmax, t_left, t_right, t_first, t_count,
       t_perm, t_new, t_wch, t_wof, t_env;
   const double *src[6] = {d->v0, d->v1, d->v2, d->n0, d->n1, d->n2};
@@ -721,63 +902,109 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
   bool root_leaf;
   int32_t root_first;
   double root_lo[3], root_hi[3];
-  cudaEvent_t tri_done = nullptr;
-  // small scenes (<= 4 MB of arrays): every array through the workspace's
-  // pinned staging buffer and ONE copy -- ~15 separate small (pageable)
-  // copies cost more than a tiny scene's whole layout
   const size_t kSmallUpload = size_t(4) << 20;
   TmpBuf t_all;
-  bool small_upload = false;
-  {
-    struct Item {
-      TmpBuf *dst;
-      const void *src;
-      size_t bytes;
-    };
-    std::vector<Item> items;
-    for (int k = 0; k < 6; ++k) items.push_back({&t_v[k], src[k], 24 * (size_t)n});
-    items.push_back({&t_mat, d->material_index, 4 * (size_t)n});
-    if (!build_here) {
-      items.push_back({&t_order, d->triangle_order, 4 * (size_t)n});
-      items.push_back({&t_bmin, d->bounds_min, 24 * (size_t)nn});
-      items.push_back({&t_bmax, d->bounds_max, 24 * (size_t)nn});
-      items.push_back({&t_left, d->left_child, 4 * (size_t)nn});
-      items.push_back({&t_right, d->right_child, 4 * (size_t)nn});
-      items.push_back({&t_first, d->first_triangle, 4 * (size_t)nn});
-      items.push_back({&t_count, d->triangle_count, 4 * (size_t)nn});
-    }
-    std::vector<size_t> off(items.size());
-    size_t total = 0;
-    for (size_t i = 0; i < items.size(); ++i) {
-      off[i] = total;
-      total += (items[i].bytes + 255) / 256 * 256;
-    }
-    small_upload = total <= kSmallUpload;
-    if (small_upload) {
-      RET(t_all.alloc(total, st));
-      Workspace &W = *s->ws;
-      std::lock_guard<std::mutex> lk(W.upload_mu);
-      if (W.stage_ev)
-        CK(cudaEventSynchronize(W.stage_ev));  // the previous small scene's copy
-      else
-        CK(cudaEventCreateWithFlags(&W.stage_ev, cudaEventDisableTiming));
-      RET(W.stage.ensure(kSmallUpload));
-      for (size_t i = 0; i < items.size(); ++i)
-        std::memcpy(static_cast<char *>(W.stage.p) + off[i], items[i].src, items[i].bytes);
-      CK(cudaMemcpyAsync(t_all.p, W.stage.p, total, cudaMemcpyHostToDevice, st));
-      CK(cudaEventRecord(W.stage_ev, st));
-      for (size_t i = 0; i < items.size(); ++i)
-        items[i].dst->set_view(static_cast<char *>(t_all.p) + off[i]);
-    }
+  Workspace &W = *s->ws;
+  std::unique_lock<std::mutex> create_lk(W.create_mu);
+  struct Item {
+    TmpBuf *dst;
+    const void *src;
+    size_t bytes;
+    bool tri;  // a triangle array (uploaded after the BVH arrays)
+  };
+  std::vector<Item> items;
+  for (int k = 0; k < 6; ++k) items.push_back({&t_v[k], src[k], 24 * (size_t)n, true});
+  items.push_back({&t_mat, d->material_index, 4 * (size_t)n, true});
+  if (!build_here) {
+    items.push_back({&t_order, d->triangle_order, 4 * (size_t)n, false});
+    items.push_back({&t_bmin, d->bounds_min, 24 * (size_t)nn, false});
+    items.push_back({&t_bmax, d->bounds_max, 24 * (size_t)nn, false});
+    items.push_back({&t_left, d->left_child, 4 * (size_t)nn, false});
+    items.push_back({&t_right, d->right_child, 4 * (size_t)nn, false});
+    items.push_back({&t_first, d->first_triangle, 4 * (size_t)nn, false});
+    items.push_back({&t_count, d->triangle_count, 4 * (size_t)nn, false});
   }
-  auto upload_triangles = [&](cudaStream_t ts) -> int {
-    if (small_upload) return LT_OK;  // already staged
-    for (int k = 0; k < 6; ++k) RET(upload(t_v[k], src[k], 3 * n, ts));
-    RET(upload(t_mat, d->material_index, n, ts));
+  std::vector<size_t> off(items.size());
+  size_t total = 0;
+  for (size_t i = 0; i < items.size(); ++i) {
+    off[i] = total;
+    total += (items[i].bytes + 255) / 256 * 256;
+  }
+  const bool small_upload = total <= kSmallUpload;
+  char *base = nullptr;
+  if (small_upload) {
+    RET(t_all.alloc(total, st));
+    std::lock_guard<std::mutex> lk(W.upload_mu);
+    if (W.stage_ev)
+      CK(cudaEventSynchronize(W.stage_ev));  // the previous small scene's copy
+    else
+      CK(cudaEventCreateWithFlags(&W.stage_ev, cudaEventDisableTiming));
+    RET(W.stage.ensure(kSmallUpload));
+    for (size_t i = 0; i < items.size(); ++i)
+      std::memcpy(static_cast<char *>(W.stage.p) + off[i], items[i].src, items[i].bytes);
+    CK(cudaMemcpyAsync(t_all.p, W.stage.p, total, cudaMemcpyHostToDevice, st));
+    CK(cudaEventRecord(W.stage_ev, st));
+    base = static_cast<char *>(t_all.p);
+  } else {
+    // the scratch is reused by every creation on the device: order this
+    // one's copies after the previous creation's last read of it (growth is
+    // a plain, rare allocation)
+    if (W.scratch_ev) CK(cudaEventSynchronize(W.scratch_ev));
+    else CK(cudaEventCreateWithFlags(&W.scratch_ev, cudaEventDisableTiming));
+    RET(W.scratch.ensure(total));
+    base = W.scratch.as<char>();
+  }
+  struct ScratchGuard {
+    Workspace &W;
+    cudaStream_t st;
+    bool on;
+    ~ScratchGuard() {
+      if (!on) return;
+      if (W.upload_st) {  // side-stream copies (joined before this runs)
+        cudaEventRecord(W.scratch_ev, W.upload_st);
+        cudaStreamWaitEvent(st, W.scratch_ev, 0);
+      }
+      cudaEventRecord(W.scratch_ev, st);
+    }
+  } scratch_guard{W, st, !small_upload};
+  for (size_t i = 0; i < items.size(); ++i) items[i].dst->set_view(base + off[i]);
+  auto copies = [&](bool tri) {
+    std::vector<CopyItem> c;
+    for (const Item &it : items)
+      if (it.tri == tri) c.push_back(CopyItem{it.dst->p, it.src, it.bytes});
+    return c;
+  };
+  // triangle arrays in flight on a host thread (large host-BVH scenes);
+  // every exit path joins it before its captures go out of scope
+  cudaEvent_t tri_done = nullptr;
+  struct EventGuard {
+    cudaEvent_t &e;
+    ~EventGuard() {
+      if (e) cudaEventDestroy(e);  // released once the recorded work completes
+    }
+  } tri_done_guard{tri_done};
+  int tri_rc = LT_OK;
+  std::string tri_msg;
+  std::thread tri_thread;
+  struct JoinGuard {
+    std::thread &t;
+    ~JoinGuard() {
+      if (t.joinable()) t.join();
+    }
+  } tri_join_guard{tri_thread};
+  auto join_triangles = [&]() -> int {
+    if (tri_thread.joinable()) tri_thread.join();
+    if (tri_rc != LT_OK) {
+      g_last_error = tri_msg;
+      return tri_rc;
+    }
     return LT_OK;
   };
   if (build_here) {
-    RET(upload_triangles(st));  // the device build reads the vertices
+    if (!small_upload) {
+      RET(ensure_ring(W));
+      RET(staged_h2d(W, device, copies(true), st));  // the build reads vertices
+    }
     RET(lt_gpu_tree_build(t_v[0].as<double>(), t_v[1].as<double>(), t_v[2].as<double>(), n, 4,
                           12, st, &tree.t));
     nn = tree.t.n_nodes;
@@ -799,27 +1026,27 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
     pt.mark("device BVH build");
   } else {
     if (!small_upload) {
-      RET(upload(t_order, d->triangle_order, n, st));
-      RET(upload(t_bmin, d->bounds_min, 3 * nn, st));
-      RET(upload(t_bmax, d->bounds_max, 3 * nn, st));
-      RET(upload(t_left, d->left_child, nn, st));
-      RET(upload(t_right, d->right_child, nn, st));
-      RET(upload(t_first, d->first_triangle, nn, st));
-      RET(upload(t_count, d->triangle_count, nn, st));
-      // the triangle arrays follow on the workspace's side stream: the BVH
-      // arrays are enqueued first (the copy engine serves them first) and
-      // their device layout overlaps the larger triangle transfer; the
-      // flatten joins both streams
+      // two concurrent staging jobs on disjoint halves of the ring: the
+      // triangle arrays (the bulk) on the side stream from a host thread,
+      // the BVH arrays on the scene stream from this one (the device
+      // layout needs them first)
       {
-        std::lock_guard<std::mutex> lk(s->ws->upload_mu);
-        if (!s->ws->upload_st)
-          CK(cudaStreamCreateWithFlags(&s->ws->upload_st, cudaStreamNonBlocking));
-        CK(cudaEventCreateWithFlags(&tri_done, cudaEventDisableTiming));
-        CK(cudaEventRecord(tri_done, st));
-        CK(cudaStreamWaitEvent(s->ws->upload_st, tri_done, 0));
-        RET(upload_triangles(s->ws->upload_st));
-        CK(cudaEventRecord(tri_done, s->ws->upload_st));
+        std::lock_guard<std::mutex> lk(W.upload_mu);
+        if (!W.upload_st) CK(cudaStreamCreateWithFlags(&W.upload_st, cudaStreamNonBlocking));
       }
+      RET(ensure_ring(W));
+      CK(cudaEventCreateWithFlags(&tri_done, cudaEventDisableTiming));
+      tri_thread = std::thread([&, tri_items = copies(true)]() {
+        tri_rc = staged_h2d(W, device, tri_items, W.upload_st, 2, kRingWorkers - 2);
+        if (tri_rc == LT_OK) {
+          const cudaError_t e = cudaEventRecord(tri_done, W.upload_st);
+          if (e != cudaSuccess)
+            tri_rc = lt_fail(LT_ERR_CUDA, "cudaEventRecord failed: %s", cudaGetErrorString(e));
+        }
+        if (tri_rc != LT_OK) tri_msg = g_last_error;
+      });
+      RET(staged_h2d(W, device, copies(false), st, 0, 2));
+      pt.mark("BVH arrays staged");
     }
     g_bmin = t_bmin.as<double>();
     g_bmax = t_bmax.as<double>();
@@ -838,11 +1065,9 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
   // index checks on host threads while the DMA runs; nothing on the device
   // has read an index yet (the device build reads only vertices)
   if (int rc = validate_indices(d)) {
-    if (tri_done) {
-      cudaEventSynchronize(tri_done);
-      cudaEventDestroy(tri_done);
-    }
+    join_triangles();
     cudaStreamSynchronize(st);
+    if (W.upload_st) cudaStreamSynchronize(W.upload_st);
     return rc;
   }
   pt.mark("validate indices (overlaps DMA)");
@@ -858,13 +1083,19 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
   // (greedy largest-area expansion, one single-CTA launch; the host-side
   // version took ~4.6 ms of host time at 1 M triangles, the level-by-level
   // launches ~2 ms of per-level synchronizations)
-  RET(device_layout(s, g_bmin, g_bmax, g_left, g_right, g_count, nn, root_leaf, t_perm, t_new,
-                    t_wch, t_wof));
-  pt.mark("device layout");
-  if (tri_done) {
-    CK(cudaStreamWaitEvent(st, tri_done, 0));  // the triangle uploads
-    cudaEventDestroy(tri_done);  // released once the recorded work completes
+  {
+    const int rc = device_layout(s, g_bmin, g_bmax, g_left, g_right, g_count, nn, root_leaf,
+                                 t_perm, t_new, t_wch, t_wof);
+    if (rc != LT_OK) {
+      join_triangles();
+      if (W.upload_st) cudaStreamSynchronize(W.upload_st);
+      return rc;
+    }
   }
+  pt.mark("device layout");
+  RET(join_triangles());
+  if (tri_done) CK(cudaStreamWaitEvent(st, tri_done, 0));  // the triangle uploads
+  pt.mark("triangle arrays staged");
   // --- flatten on the device
   int rc = LT_OK;
   do {
@@ -873,8 +1104,11 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
     // half of one cache line
     s->shade_off = (s->nodes_bytes + 16 * LT_TRI_F4 * (size_t)n + 127) / 128 * 128;
     s->geo_bytes = s->shade_off + 64 * (size_t)n;
-    if ((rc = s->geo.ensure(s->geo_bytes))) break;
-    if ((rc = s->nodes2.ensure((size_t)std::max<int64_t>(1, s->n_internal) * 64))) break;
+    if ((rc = take_cached(W, s->geo, s->geo_bytes, st))) break;
+    pt.mark("geo alloc");
+    if ((rc = take_cached(W, s->nodes2, (size_t)std::max<int64_t>(1, s->n_internal) * 64, st)))
+      break;
+    pt.mark("nodes2 alloc");
     float4 *g_wide = s->geo.as<float4>();
     float4 *g_tris = g_wide + s->nodes_bytes / 16;
     float4 *g_shade = g_wide + s->shade_off / 16;
@@ -904,7 +1138,10 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
     if (d->env_kind == LT_ENV_LATLONG) {
       const int64_t np = (int64_t)d->env_width * d->env_height;
       // float3 texels as given; widened to float4 records on the device
-      if ((rc = upload(t_env, d->env_texels, 3 * (size_t)np, st))) break;
+      const size_t env_bytes = sizeof(float) * 3 * (size_t)np;
+      if ((rc = t_env.alloc(env_bytes, st))) break;
+      if ((rc = ensure_ring(W))) break;
+      if ((rc = staged_h2d(W, device, {CopyItem{t_env.p, d->env_texels, env_bytes}}, st))) break;
       if ((rc = s->env.ensure((size_t)np * 16))) break;
       launch_expand_rgb(t_env.as<float>(), np, s->env.as<float4>(), st);
     }

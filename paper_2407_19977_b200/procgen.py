@@ -1,20 +1,9 @@
-"""Procedural benchmark scenes (BASELINE.json configs).
+"""Procedural test geometry -- the reference's procgen API (procgen.py:21-207):
+an icosphere, a displaced sphere with an exact triangle count, and GLB
+writers (`save_glb` lives with the ingest code, ingest.py).
 
-  * cornell_box      C1/C2: ~36 axis-aligned triangles on a dyadic grid (all
-                     coordinates exact in fp32), diffuse walls, emissive quad;
-                     variant "mixed" adds metal / glossy-dielectric boxes,
-                     variant "extended" adds coat / glass (extensions).
-  * sphere_on_plane  C3: `bumpy_sphere(70_000)` on a 2-triangle metal plane
-                     under the reference's benchmark gradient sky.
-  * pushbutton       C4/C5: a CAD-style pushbutton assembly of ~1.06 M
-                     triangles (housing, knurled collar, chrome bezel,
-                     coated cap, glass lens, LED ring, base plate, screws)
-                     with mixed OpenPBR materials.
-  * synthetic_hdr    equirectangular sky + sun radiance map (extension).
-
-Vertices are rounded to float32 (as a GLB stores them, procgen.py:123 of the
-reference) so the float64 oracle and the fp32 kernels see identical
-positions.  Everything is deterministic.
+The benchmark scenes (Cornell box, bunny-scale sphere, CAD pushbutton, HDR
+sky) are workloads, not product API: see /workloads.py at the repo root.
 """
 from __future__ import annotations
 
@@ -22,27 +11,43 @@ import math
 
 import numpy as np
 
-from .geometry import TriangleBuffer
-from .material import OpenPbrParams
-from .scene import CameraConfig, EnvironmentConfig, SceneDescription
-
-BENCH_ENVIRONMENT = dict(zenith=(0.5, 0.6, 0.9), horizon=(0.9, 0.85, 0.8))  # bench.py:33-34
+_PHI = (1.0 + math.sqrt(5.0)) / 2.0
 
 
-# ------------------------------------------------------------------ meshes
+def icosphere(subdivisions: int = 2, radius: float = 1.0) -> tuple[np.ndarray, np.ndarray]:
+    """Subdivided icosahedron on a sphere (procgen.py:21-68): positions (n, 3)
+    float64 and indices (3k,) int64, k = 20 * 4**subdivisions, watertight.
+    Midpoints are created in face order, edge (a, b) once, so the vertex
+    numbering is the reference's."""
+    if subdivisions < 0:
+        raise ValueError("subdivisions must be >= 0")
+    if radius <= 0.0:
+        raise ValueError("radius must be positive")
+    p = _PHI
+    base = np.array([[-1, p, 0], [1, p, 0], [-1, -p, 0], [1, -p, 0], [0, -1, p], [0, 1, p],
+                     [0, -1, -p], [0, 1, -p], [p, 0, -1], [p, 0, 1], [-p, 0, -1], [-p, 0, 1]],
+                    dtype=np.float64)
+    verts = [v / np.linalg.norm(v) for v in base]
+    faces = [(0, 11, 5), (0, 5, 1), (0, 1, 7), (0, 7, 10), (0, 10, 11), (1, 5, 9), (5, 11, 4),
+             (11, 10, 2), (10, 7, 6), (7, 1, 8), (3, 9, 4), (3, 4, 2), (3, 2, 6), (3, 6, 8),
+             (3, 8, 9), (4, 9, 5), (2, 4, 11), (6, 2, 10), (8, 6, 7), (9, 8, 1)]
+    for _ in range(subdivisions):
+        mids: dict[tuple[int, int], int] = {}
 
-def smooth_normals(positions: np.ndarray, indices: np.ndarray) -> np.ndarray:
-    """Area-weighted vertex normals (scene.py:493-507 semantics)."""
-    a, b, c = (positions[indices[k::3]] for k in range(3))
-    face = np.cross(b - a, c - a)
-    acc = np.zeros_like(positions)
-    for k in range(3):
-        np.add.at(acc, indices[k::3], face)
-    length = np.linalg.norm(acc, axis=1, keepdims=True)
-    zero = length[:, 0] == 0.0
-    acc[zero] = (0.0, 0.0, 1.0)
-    length[zero] = 1.0
-    return acc / length
+        def mid(a: int, b: int) -> int:
+            key = (min(a, b), max(a, b))
+            if key not in mids:
+                m = verts[a] + verts[b]
+                verts.append(m / np.linalg.norm(m))
+                mids[key] = len(verts) - 1
+            return mids[key]
+
+        refined = []
+        for a, b, c in faces:
+            ab, bc, ca = mid(a, b), mid(b, c), mid(c, a)
+            refined.extend([(a, ab, ca), (b, bc, ab), (c, ca, bc), (ab, bc, ca)])
+        faces = refined
+    return np.asarray(verts) * radius, np.asarray(faces, dtype=np.int64).ravel()
 
 
 def bumpy_sphere(n_triangles: int, bump_amplitude: float = 0.12,
@@ -71,294 +76,20 @@ def bumpy_sphere(n_triangles: int, bump_amplitude: float = 0.12,
     return pos, faces[:n_triangles].ravel()
 
 
-class MeshBuilder:
-    """Collects indexed parts, emits a TriangleBuffer with per-corner
-    normals (smooth within a part, float32-rounded positions)."""
 
-    def __init__(self):
-        self.parts = []
-
-    def add(self, positions, indices, material: int, normals=None):
-        positions = np.asarray(positions, dtype=np.float32).astype(np.float64)
-        indices = np.asarray(indices, dtype=np.int64).ravel()
-        if normals is None:
-            normals = smooth_normals(positions, indices)
-        self.parts.append((positions, indices, np.asarray(normals, np.float64), int(material)))
-        return self
-
-    def add_flat(self, tris, material: int):
-        """tris: (k, 3, 3) corner positions; flat (face) normals."""
-        tris = np.asarray(tris, dtype=np.float32).astype(np.float64)
-        fn = np.cross(tris[:, 1] - tris[:, 0], tris[:, 2] - tris[:, 0])
-        fn /= np.linalg.norm(fn, axis=1, keepdims=True)
-        pos = tris.reshape(-1, 3)
-        idx = np.arange(pos.shape[0])
-        return self.add(pos, idx, material, normals=np.repeat(fn, 3, axis=0))
-
-    def build(self) -> TriangleBuffer:
-        cols = {k: [] for k in ("v0", "v1", "v2", "n0", "n1", "n2")}
-        mats = []
-        for pos, idx, nrm, mat in self.parts:
-            for k in range(3):
-                cols[f"v{k}"].append(pos[idx[k::3]])
-                cols[f"n{k}"].append(nrm[idx[k::3]])
-            mats.append(np.full(idx.size // 3, mat, np.int32))
-        return TriangleBuffer(*(np.vstack(cols[k]) for k in ("v0", "v1", "v2", "n0", "n1", "n2")),
-                              material_index=np.concatenate(mats))
-
-    @property
-    def n_triangles(self) -> int:
-        return sum(p[1].size // 3 for p in self.parts)
+def icosphere_glb(path, subdivisions: int = 2, radius: float = 1.0,
+                  material_name: str | None = None) -> int:
+    """icosphere -> GLB with smooth normals (procgen.py:193-199); returns the
+    triangle count."""
+    from .ingest import generate_smooth_normals, save_glb
+    positions, indices = icosphere(subdivisions, radius)
+    save_glb(path, positions, indices, generate_smooth_normals(positions, indices), material_name)
+    return indices.size // 3
 
 
-def quad(a, b, c, d):
-    """Two triangles (a, b, c), (a, c, d)."""
-    return [[a, b, c], [a, c, d]]
-
-
-def box_tris(lo, hi):
-    x0, y0, z0 = lo
-    x1, y1, z1 = hi
-    p = [(x0, y0, z0), (x1, y0, z0), (x1, y1, z0), (x0, y1, z0),
-         (x0, y0, z1), (x1, y0, z1), (x1, y1, z1), (x0, y1, z1)]
-    faces = [(0, 3, 2, 1), (4, 5, 6, 7), (0, 1, 5, 4), (3, 7, 6, 2), (0, 4, 7, 3), (1, 2, 6, 5)]
-    out = []
-    for a, b, c, d in faces:   # outward winding
-        out += quad(p[a], p[b], p[c], p[d])
-    return out
-
-
-def revolve(profile_r, profile_y, n_theta: int, radial=None):
-    """Surface of revolution about +y: profile (r_j, y_j), j = 0..m-1,
-    n_theta segments; `radial(theta, j)` optionally multiplies r.  Returns
-    (positions, indices) with a duplicated seam (outward winding for a
-    profile that runs bottom -> top on the outside)."""
-    r = np.asarray(profile_r, np.float64)
-    y = np.asarray(profile_y, np.float64)
-    m = r.size
-    th = np.linspace(0.0, 2.0 * math.pi, n_theta + 1)
-    R = np.broadcast_to(r[None, :], (n_theta + 1, m)).copy()
-    if radial is not None:
-        R = R * radial(th[:, None], np.arange(m)[None, :])
-    pos = np.stack([R * np.cos(th)[:, None], np.broadcast_to(y[None, :], R.shape),
-                    -R * np.sin(th)[:, None]], axis=-1).reshape(-1, 3)
-    i = np.arange(n_theta)[:, None] * m
-    j = np.arange(m - 1)[None, :]
-    a = i + j
-    b = a + m
-    lo = np.stack([a, b, a + 1], -1).reshape(-1, 3)
-    hi = np.stack([a + 1, b, b + 1], -1).reshape(-1, 3)
-    faces = np.empty((2 * lo.shape[0], 3), np.int64)
-    faces[0::2], faces[1::2] = lo, hi
-    return pos, faces.ravel()
-
-
-def torus(R: float, r: float, y0: float, n_theta: int, n_phi: int):
-    ph = np.linspace(0.0, 2.0 * math.pi, n_phi + 1)
-    return revolve(R + r * np.cos(ph), y0 + r * np.sin(ph), n_theta)
-
-
-# ------------------------------------------------------------------ scenes
-
-def cornell_box(width: int = 64, height: int = 64, variant: str = "diffuse") -> SceneDescription:
-    """Cornell-style box on a dyadic grid.  variant: 'diffuse' (C1),
-    'mixed' (metal + glossy dielectric boxes, reference lobes only), or
-    'extended' (coat + glass boxes: extension lobes)."""
-    white = OpenPbrParams(base_color=(0.75, 0.75, 0.75), specular_weight=0.0)
-    red = OpenPbrParams(base_color=(0.75, 0.125, 0.125), specular_weight=0.0)
-    green = OpenPbrParams(base_color=(0.125, 0.75, 0.125), specular_weight=0.0)
-    light = OpenPbrParams(base_color=(0.75, 0.75, 0.75), specular_weight=0.0,
-                          emission_luminance=15.0, emission_color=(1.0, 0.875, 0.75))
-    if variant == "diffuse":
-        tall = short = white
-    elif variant == "mixed":
-        tall = OpenPbrParams(base_color=(0.875, 0.75, 0.5), base_metalness=1.0,
-                             specular_roughness=0.125)
-        short = OpenPbrParams(base_color=(0.25, 0.375, 0.75), specular_roughness=0.25,
-                              specular_ior=1.5)
-    elif variant == "extended":
-        tall = OpenPbrParams(base_color=(0.875, 0.75, 0.5), base_metalness=1.0,
-                             specular_roughness=0.125)
-        short = OpenPbrParams(base_color=(0.75, 0.125, 0.0625), specular_roughness=0.375,
-                              coat_weight=1.0, coat_roughness=0.0625)
-        glass = OpenPbrParams(base_color=(1.0, 1.0, 1.0), specular_roughness=0.0625,
-                              transmission_weight=1.0, transmission_color=(0.875, 0.9375, 1.0))
-    else:
-        raise ValueError(f"unknown cornell variant {variant!r}")
-    mats = [white, red, green, light, tall, short]
-    mb = MeshBuilder()
-    s = 1.0
-    h = 2.0
-    walls = []
-    walls += quad((-s, 0, -s), (s, 0, -s), (s, 0, s), (-s, 0, s))      # floor (y=0, faces +y)
-    walls += quad((-s, h, -s), (-s, h, s), (s, h, s), (s, h, -s))      # ceiling
-    walls += quad((-s, 0, -s), (-s, h, -s), (s, h, -s), (s, 0, -s))    # back
-    mb.add_flat(walls, 0)
-    mb.add_flat(quad((-s, 0, -s), (-s, 0, s), (-s, h, s), (-s, h, -s)), 1)   # left (red)
-    mb.add_flat(quad((s, 0, -s), (s, h, -s), (s, h, s), (s, 0, s)), 2)       # right (green)
-    ly = 1.984375
-    mb.add_flat(quad((-0.25, ly, -0.25), (0.25, ly, -0.25), (0.25, ly, 0.25), (-0.25, ly, 0.25)),
-                3)
-    mb.add_flat(box_tris((-0.625, 0.0, -0.625), (-0.125, 1.25, -0.125)), 4)   # tall box
-    mb.add_flat(box_tris((0.125, 0.0, -0.125), (0.625, 0.625, 0.375)), 5)     # short box
-    if variant == "extended":
-        mats.append(glass)
-        mb.add_flat(box_tris((-0.5, 0.0, 0.25), (-0.125, 0.375, 0.625)), 6)   # glass block
-    cam = CameraConfig(position=(0.0, 1.0, 3.75), look_at=(0.0, 1.0, 0.0),
-                       vertical_fov_deg=40.0, width=width, height=height)
-    return SceneDescription(mb.build(), mats, cam, EnvironmentConfig.uniform((0.0, 0.0, 0.0)))
-
-
-def sphere_on_plane(n_triangles: int = 70_000, width: int = 1920, height: int = 1080,
-                    environment=None) -> SceneDescription:
-    """C3: bumpy_sphere(n) resting above a 2-triangle metal ground plane."""
-    pos, idx = bumpy_sphere(n_triangles)
-    pos = pos + np.array([0.0, 1.125, 0.0])
-    mb = MeshBuilder()
-    mb.add(pos, idx, 0)
-    g = 16.0
-    mb.add_flat(quad((-g, 0, -g), (-g, 0, g), (g, 0, g), (g, 0, -g)), 1)
-    mats = [OpenPbrParams(base_color=(0.8, 0.55, 0.45), specular_roughness=0.4),
-            OpenPbrParams(base_color=(0.9, 0.9, 0.92), base_metalness=1.0,
-                          specular_roughness=0.2)]
-    cam = CameraConfig(position=(0.0, 1.5, 4.75), look_at=(0.0, 1.0, 0.0),
-                       vertical_fov_deg=40.0, width=width, height=height)
-    env = environment or EnvironmentConfig.gradient(**BENCH_ENVIRONMENT)
-    return SceneDescription(mb.build(), mats, cam, env)
-
-
-def pushbutton(width: int = 1920, height: int = 1080, extended: bool = True,
-               environment=None, detail: float = 0.807) -> SceneDescription:
-    """C4: CAD-style pushbutton assembly, ~1.07 M triangles at the default detail.
-    extended=False swaps the coat / glass materials for reference lobes (the
-    parity-pinned variant)."""
-    def n(x):
-        return max(8, int(round(x * detail)))
-
-    mats = [
-        OpenPbrParams(base_color=(0.35, 0.36, 0.38), specular_roughness=0.55),          # 0 ground
-        OpenPbrParams(base_color=(0.91, 0.92, 0.92), base_metalness=1.0,
-                      specular_roughness=0.35),                                          # 1 housing
-        OpenPbrParams(base_color=(0.56, 0.57, 0.58), base_metalness=1.0,
-                      specular_roughness=0.25),                                          # 2 knurl
-        OpenPbrParams(base_color=(0.97, 0.96, 0.91), base_metalness=1.0,
-                      specular_roughness=0.06),                                          # 3 bezel
-        OpenPbrParams(base_color=(0.8, 0.05, 0.04), specular_roughness=0.35,
-                      coat_weight=1.0 if extended else 0.0, coat_roughness=0.05),        # 4 cap
-        OpenPbrParams(base_color=(0.95, 0.97, 1.0), specular_roughness=0.02,
-                      specular_weight=1.0,
-                      transmission_weight=1.0 if extended else 0.0,
-                      transmission_color=(0.9, 0.95, 1.0)),                              # 5 lens
-        OpenPbrParams(base_color=(0.2, 0.9, 0.3), specular_weight=0.0,
-                      emission_luminance=8.0, emission_color=(0.2, 1.0, 0.35)),          # 6 LED
-        OpenPbrParams(base_color=(0.04, 0.04, 0.045), specular_roughness=0.5),           # 7 plate
-        OpenPbrParams(base_color=(0.75, 0.75, 0.77), base_metalness=1.0,
-                      specular_roughness=0.2),                                           # 8 screws
-    ]
-    mb = MeshBuilder()
-    # ground
-    g = 24.0
-    mb.add_flat(quad((-g, 0, -g), (-g, 0, g), (g, 0, g), (g, 0, -g)), 0)
-    # base plate and four screws
-    mb.add_flat(box_tris((-1.6, 0.0, -1.6), (1.6, 0.12, 1.6)), 7)
-    for sx, sz in ((-1.3, -1.3), (1.3, -1.3), (-1.3, 1.3), (1.3, 1.3)):
-        ph = np.linspace(0.0, 0.5 * math.pi, n(24))
-        prof_r = np.concatenate([[0.0], 0.11 * np.cos(ph[::-1])])
-        prof_y = np.concatenate([[0.12], 0.12 + 0.05 * np.sin(ph[::-1])])
-        pos, idx = revolve(prof_r[::-1], prof_y[::-1], n(192))
-        mb.add(pos + np.array([sx, 0.0, sz]), idx, 8)
-    # housing: cylinder with a rounded top edge, y in [0.12, 0.75]
-    t = np.linspace(0.0, 1.0, n(96))
-    edge = np.linspace(0.0, 0.5 * math.pi, n(48))
-    hr = np.concatenate([np.full(t.size, 1.0), 0.92 + 0.08 * np.cos(edge[1:]),
-                         np.linspace(0.92, 0.86, n(8))[1:]])
-    hy = np.concatenate([0.12 + 0.55 * t, 0.67 + 0.08 * np.sin(edge[1:]),
-                         np.full(n(8) - 1, 0.75)])
-    pos, idx = revolve(hr, hy, n(1536))
-    mb.add(pos, idx, 1)
-    # knurled collar: radius modulated by 60 ridges
-    kt = np.linspace(0.0, 1.0, n(40))
-    ridges = 60
-
-    def knurl(theta, j):
-        return 1.0 + 0.018 * np.abs(np.cos(0.5 * ridges * theta))
-
-    pos, idx = revolve(np.full(kt.size, 1.02), 0.2 + 0.3 * kt, n(3072), radial=knurl)
-    mb.add(pos, idx, 2)
-    # chrome bezel: torus
-    pos, idx = torus(0.86, 0.07, 0.76, n(1536), n(96))
-    mb.add(pos, idx, 3)
-    # LED ring
-    pos, idx = torus(0.74, 0.018, 0.77, n(1024), n(24))
-    mb.add(pos, idx, 6)
-    # cap: rippled dome over r in [0, 0.7]
-    ct = np.linspace(0.0, 1.0, n(160))
-    cr = 0.7 * np.sin(0.5 * math.pi * (1.0 - ct))
-    cy = 0.78 + 0.22 * np.sin(0.5 * math.pi * ct)
-
-    def ripple(theta, j):
-        return 1.0 + 0.01 * np.sin(12.0 * theta) * np.sin(math.pi * np.clip(j / (ct.size - 1), 0, 1))
-
-    pos, idx = revolve(cr[::-1], cy[::-1], n(1536), radial=ripple)
-    mb.add(pos, idx, 4)
-    # glass lens over the cap top
-    lt = np.linspace(0.0, 1.0, n(48))
-    lr = 0.3 * np.cos(0.5 * math.pi * lt)
-    ly = 1.015 + 0.06 * np.sin(0.5 * math.pi * lt)
-    pos, idx = revolve(lr, ly, n(768))
-    mb.add(pos, idx, 5)
-    cam = CameraConfig(position=(0.0, 2.6, 3.9), look_at=(0.0, 0.55, 0.0),
-                       vertical_fov_deg=34.0, width=width, height=height)
-    env = environment
-    if env is None:
-        env = EnvironmentConfig.latlong(synthetic_hdr(), 1.0) if extended else \
-            EnvironmentConfig.gradient(**BENCH_ENVIRONMENT)
-    return SceneDescription(mb.build(), mats, cam, env)
-
-
-def synthetic_hdr(width: int = 1024, height: int = 512, sun_dir=(0.45, 0.6, 0.35),
-                  sun_radiance: float = 400.0, sun_angle_deg: float = 2.5) -> np.ndarray:
-    """Equirectangular (height, width, 3) float32 radiance: a vertical sky
-    gradient, a warm horizon band, a dark ground and a small bright sun --
-    the dynamic range of a captured HDR sky (extension; no reference)."""
-    v = (np.arange(height) + 0.5) / height
-    u = (np.arange(width) + 0.5) / width
-    theta = v * math.pi                       # 0 at zenith
-    phi = (u - 0.5) * 2.0 * math.pi
-    st, ct = np.sin(theta)[:, None], np.cos(theta)[:, None]
-    d = np.stack([st * np.sin(phi)[None, :], np.broadcast_to(ct, (height, width)),
-                  -st * np.cos(phi)[None, :]], axis=-1)
-    y = d[..., 1:2]
-    zen = np.array([0.25, 0.45, 1.0])
-    hor = np.array([1.0, 0.85, 0.65])
-    ground = np.array([0.18, 0.16, 0.14])
-    sky = hor + (zen - hor) * np.clip(y, 0.0, 1.0) ** 0.5
-    img = np.where(y >= 0.0, sky, ground * (1.0 + 0.5 * np.clip(-y, 0.0, 1.0)))
-    s = np.asarray(sun_dir, np.float64)
-    s /= np.linalg.norm(s)
-    cosang = np.tensordot(d, s, axes=([2], [0]))
-    core = np.cos(math.radians(sun_angle_deg))
-    halo = np.clip((cosang - 0.9) / 0.1, 0.0, 1.0) ** 8
-    img = img + (cosang >= core)[..., None] * sun_radiance * np.array([1.0, 0.95, 0.85])
-    img = img + halo[..., None] * np.array([2.0, 1.8, 1.4])
-    return np.ascontiguousarray(img, dtype=np.float32)
-
-
-def scene_by_name(name: str, **kw) -> SceneDescription:
-    """Named workloads used by bench.py and the tests."""
-    if name == "cornell_c1":
-        return cornell_box(kw.get("width", 64), kw.get("height", 64), "diffuse")
-    if name == "cornell_c2":
-        return cornell_box(kw.get("width", 512), kw.get("height", 512), "mixed")
-    if name == "cornell_c2x":
-        return cornell_box(kw.get("width", 512), kw.get("height", 512), "extended")
-    if name == "sphere70k":
-        return sphere_on_plane(kw.get("n_triangles", 70_000), kw.get("width", 1920),
-                               kw.get("height", 1080))
-    if name == "pushbutton":
-        return pushbutton(kw.get("width", 1920), kw.get("height", 1080), True,
-                          detail=kw.get("detail", 0.807))
-    if name == "pushbutton_ref":
-        return pushbutton(kw.get("width", 1920), kw.get("height", 1080), False,
-                          detail=kw.get("detail", 0.807))
-    raise ValueError(f"unknown scene {name!r}")
+def bumpy_sphere_glb(path, n_triangles: int, material_name: str | None = None) -> int:
+    """bumpy_sphere -> GLB with smooth normals (procgen.py:202-207)."""
+    from .ingest import generate_smooth_normals, save_glb
+    positions, indices = bumpy_sphere(n_triangles)
+    save_glb(path, positions, indices, generate_smooth_normals(positions, indices), material_name)
+    return indices.size // 3

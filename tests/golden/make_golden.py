@@ -34,7 +34,7 @@ import numpy as np  # noqa: E402
 import luxtrace as lx  # noqa: E402
 from luxtrace.integrator import _camera_pack, _render_pass, _scene_arrays  # noqa: E402
 
-from paper_2407_19977_b200 import procgen  # noqa: E402  (scene geometry only)
+import workloads as procgen  # noqa: E402  (scene geometry only)
 
 
 def mixed_rays(n, seed, spread=1.4, radius=3.0, center=(0.0, 0.0, 0.0)):

@@ -153,7 +153,7 @@ def test_gpu_build_equals_host_build_bench_scenes(scene):
     """The bench workloads (1.06 M and 70 k triangles)."""
     import time
     from paper_2407_19977_b200 import build_bvh
-    from paper_2407_19977_b200.procgen import scene_by_name
+    from workloads import scene_by_name
     tris = scene_by_name(scene, width=64, height=36).triangles
     build_bvh(tris, device=0)   # warm (module load, allocations)
     t0 = time.perf_counter()

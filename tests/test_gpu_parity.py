@@ -16,6 +16,8 @@ from __future__ import annotations
 import numpy as np
 import pytest
 
+import workloads as wl
+
 from conftest import golden_scene
 
 pytestmark = pytest.mark.gpu
@@ -345,7 +347,7 @@ def test_primary_hits_at_scale(scene_name):
     """Primary-hit ids of a full frame vs the float64 oracle traversal on the
     same jittered rays; mismatches are ulp-level edges/ties, counted."""
     from oracle.oracle import OracleScene, primary_rays
-    from paper_2407_19977_b200.procgen import scene_by_name
+    from workloads import scene_by_name
     m = lb()
     sc = scene_by_name(scene_name, width=480, height=270)
     bvh = m.build_bvh(sc.triangles)
@@ -367,7 +369,7 @@ def test_primary_hits_at_scale(scene_name):
 def test_per_sample_parity_at_scale():
     """Matched-stream radiance on the 70k-triangle C3 scene (depth 8)."""
     from oracle.oracle import OracleScene
-    from paper_2407_19977_b200.procgen import scene_by_name
+    from workloads import scene_by_name
     m = lb()
     sc = scene_by_name("sphere70k", width=192, height=108)
     bvh = m.build_bvh(sc.triangles)
@@ -394,7 +396,7 @@ def test_converged_image_within_monte_carlo_ci():
     time."""
     from oracle.oracle import OracleScene
     m = lb()
-    sc = m.cornell_box(48, 48, "mixed")
+    sc = wl.cornell_box(48, 48, "mixed")
     bvh = m.build_bvh(sc.triangles)
     spp = 256
     st = m.RenderSettings(samples_per_pixel=spp, max_depth=8, seed=101)
@@ -420,7 +422,7 @@ def test_extension_lobes_match_oracle_matched_streams():
     and the float64 oracle implement the same estimator."""
     from oracle.oracle import OracleScene
     m = lb()
-    sc = m.cornell_box(48, 48, "extended")
+    sc = wl.cornell_box(48, 48, "extended")
     bvh = m.build_bvh(sc.triangles)
     ds = m.DeviceScene(sc, bvh)
     oc = OracleScene.from_scene(sc, bvh)
@@ -440,7 +442,7 @@ def test_glass_furnace():
     (apart from path-length truncation) loses energy."""
     m = lb()
     pos, idx = m.bumpy_sphere(20_000, bump_amplitude=0.0)
-    from paper_2407_19977_b200.procgen import MeshBuilder
+    from workloads import MeshBuilder
     mb = MeshBuilder().add(pos, idx, 0)
     glass = m.OpenPbrParams(base_color=(1, 1, 1), specular_roughness=0.0,
                             transmission_weight=1.0)
@@ -457,8 +459,8 @@ def test_glass_furnace():
 def test_latlong_environment_matches_oracle():
     from oracle.oracle import OracleScene
     m = lb()
-    sc = m.sphere_on_plane(5_000, 40, 24,
-                           environment=m.EnvironmentConfig.latlong(m.synthetic_hdr(256, 128), 0.5))
+    sc = wl.sphere_on_plane(5_000, 40, 24,
+                            environment=m.EnvironmentConfig.latlong(wl.synthetic_hdr(256, 128), 0.5))
     bvh = m.build_bvh(sc.triangles)
     ds = m.DeviceScene(sc, bvh)
     oc = OracleScene.from_scene(sc, bvh)

@@ -6,6 +6,8 @@ from __future__ import annotations
 import numpy as np
 import pytest
 
+import workloads as wl
+
 from conftest import GOLDEN, golden_scene, gpu_available
 
 import paper_2407_19977_b200 as lb
@@ -51,7 +53,7 @@ def test_camera_and_environment_validation():
         lb.EnvironmentConfig(kind="sky")
     with pytest.raises(lb.SceneError):
         lb.EnvironmentConfig.latlong(np.zeros((4, 8)))
-    env = lb.EnvironmentConfig.latlong(lb.synthetic_hdr(64, 32), 2.0)
+    env = lb.EnvironmentConfig.latlong(wl.synthetic_hdr(64, 32), 2.0)
     assert env.texels.dtype == np.float32 and env.texels.shape == (32, 64, 3)
 
 
@@ -103,16 +105,16 @@ def test_bumpy_sphere_matches_reference_generator():
 
 
 def test_procedural_scenes():
-    c1 = lb.cornell_box(64, 64, "diffuse")
+    c1 = wl.cornell_box(64, 64, "diffuse")
     assert 30 <= len(c1.triangles) <= 40
     # dyadic coordinates: exact in float32
     for k in ("v0", "v1", "v2"):
         a = getattr(c1.triangles, k)
         assert np.array_equal(a.astype(np.float32).astype(np.float64), a)
-    ext = lb.cornell_box(32, 32, "extended")
+    ext = wl.cornell_box(32, 32, "extended")
     assert any(m.transmission_weight > 0 for m in ext.materials)
     assert any(m.coat_weight > 0 for m in ext.materials)
-    pb = lb.pushbutton(64, 36, detail=0.2)
+    pb = wl.pushbutton(64, 36, detail=0.2)
     assert len(pb.triangles) > 10_000
     assert pb.environment.kind == "latlong"
 

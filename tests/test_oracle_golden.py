@@ -137,3 +137,23 @@ def test_oracle_chunking_invariant(oracle_lib):
                        threads=3)
     for x, y in zip(a, b):
         assert np.array_equal(x, y)
+
+
+@pytest.mark.parametrize("name", ["floor", "shell", "glossy", "sphere2k", "dup", "cornell_c1",
+                                  "cornell_c2", "sphere20k"])
+def test_oracle_bvh_build_bit_exact(name, oracle_lib):
+    """oc_build_bvh (the reference arm's tree) == luxtrace.build_bvh's arrays."""
+    g = golden_scene(name)
+    b = oracle_lib.build_bvh(g.triangles)
+    assert np.array_equal(b.bounds_min, g["bvh_bounds_min"])
+    assert np.array_equal(b.bounds_max, g["bvh_bounds_max"])
+    for mine, ref in (("left_child", "bvh_left"), ("right_child", "bvh_right"),
+                      ("first_triangle", "bvh_first"), ("triangle_count", "bvh_count"),
+                      ("triangle_order", "bvh_order")):
+        assert np.array_equal(getattr(b, mine), g[ref]), mine
+
+
+@pytest.mark.parametrize("name", ["floor", "glossy", "cornell_c2"])
+def test_oracle_camera_pack_matches_reference(name, oracle_lib):
+    g = golden_scene(name)
+    assert np.array_equal(oracle_lib.camera_pack(g.camera), g["cam_pack"])

@@ -5,7 +5,7 @@ from pathlib import Path
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2407_19977_b200 import build_bvh  # noqa: E402
-from paper_2407_19977_b200.procgen import scene_by_name  # noqa: E402
+from workloads import scene_by_name  # noqa: E402
 
 for name in sys.argv[1:] or ["pushbutton", "sphere70k"]:
     tris = scene_by_name(name, width=64, height=36).triangles

@@ -5,7 +5,7 @@ import sys, time, numpy as np
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2407_19977_b200 import build_bvh
-from paper_2407_19977_b200.procgen import scene_by_name
+from workloads import scene_by_name
 name = sys.argv[1] if len(sys.argv) > 1 else 'pushbutton'
 sc = scene_by_name(name)
 t0=time.time(); bvh = build_bvh(sc.triangles, device=None); print('build', time.time()-t0)

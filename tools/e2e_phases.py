@@ -1,5 +1,6 @@
-"""Phase timing of end-to-end render_progressive calls (GPU box), inputs in
-pinned host memory as bench.py's e2e leg uses them."""
+"""Phase timing of end-to-end render_progressive calls (GPU box): the scene's
+plain numpy arrays (pageable, as a luxtrace caller holds them), or with
+--pinned page-locked copies."""
 import gc
 import sys
 import time
@@ -11,7 +12,7 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 from paper_2407_19977_b200 import RenderSettings, build_bvh, render_progressive  # noqa: E402
-from paper_2407_19977_b200.procgen import scene_by_name  # noqa: E402
+from workloads import scene_by_name  # noqa: E402
 
 
 def pin(obj, names, keep):
@@ -26,11 +27,12 @@ def pin(obj, names, keep):
 sc = scene_by_name("pushbutton")
 bvh = build_bvh(sc.triangles)
 keep = []
-pin(sc.triangles, ["v0", "v1", "v2", "n0", "n1", "n2", "material_index"], keep)
-pin(bvh, ["bounds_min", "bounds_max", "left_child", "right_child", "first_triangle",
-          "triangle_count", "triangle_order"], keep)
-if sc.environment.texels is not None:
-    pin(sc.environment, ["texels"], keep)
+if "--pinned" in sys.argv:
+    pin(sc.triangles, ["v0", "v1", "v2", "n0", "n1", "n2", "material_index"], keep)
+    pin(bvh, ["bounds_min", "bounds_max", "left_child", "right_child", "first_triangle",
+              "triangle_count", "triangle_order"], keep)
+    if sc.environment.texels is not None:
+        pin(sc.environment, ["texels"], keep)
 st = RenderSettings(samples_per_pixel=256, max_depth=8, rr_start_depth=3, seed=0)
 for it in range(4):
     torch.cuda.synchronize()

@@ -6,7 +6,7 @@ from pathlib import Path
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2407_19977_b200 import RenderSettings, build_bvh, render_progressive  # noqa: E402
-from paper_2407_19977_b200.procgen import scene_by_name  # noqa: E402
+from workloads import scene_by_name  # noqa: E402
 
 scene = scene_by_name("pushbutton")
 st = RenderSettings(samples_per_pixel=256, max_depth=8, rr_start_depth=3, seed=0)

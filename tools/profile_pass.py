@@ -24,7 +24,7 @@ def main():
     from paper_2407_19977_b200 import RenderSettings, build_bvh
     from paper_2407_19977_b200.device import DeviceScene
     from paper_2407_19977_b200.integrator import Accumulator, render_pass_device
-    from paper_2407_19977_b200.procgen import scene_by_name
+    from workloads import scene_by_name
     scene = scene_by_name(a.workload, width=1920, height=1080)
     bvh = build_bvh(scene.triangles)
     ds = DeviceScene(scene, bvh)

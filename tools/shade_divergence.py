@@ -10,7 +10,7 @@ from paper_2407_19977_b200 import RenderSettings, build_bvh  # noqa: E402
 from paper_2407_19977_b200._lib import LT_FLAG_COUNT  # noqa: E402
 from paper_2407_19977_b200.device import DeviceScene  # noqa: E402
 from paper_2407_19977_b200.integrator import Accumulator, render_pass_device  # noqa: E402
-from paper_2407_19977_b200.procgen import scene_by_name  # noqa: E402
+from workloads import scene_by_name  # noqa: E402
 
 for name in sys.argv[1:] or ["pushbutton", "cornell_c2x", "sphere70k"]:
     scene = scene_by_name(name, width=1920, height=1080) if name in ("pushbutton", "sphere70k") \

@@ -12,7 +12,7 @@ import torch  # noqa: E402
 from paper_2407_19977_b200 import RenderSettings, build_bvh  # noqa: E402
 from paper_2407_19977_b200.device import DeviceScene  # noqa: E402
 from paper_2407_19977_b200.integrator import Accumulator, render_pass_device  # noqa: E402
-from paper_2407_19977_b200.procgen import scene_by_name  # noqa: E402
+from workloads import scene_by_name  # noqa: E402
 
 scene = scene_by_name("pushbutton")
 bvh = build_bvh(scene.triangles)

@@ -5,7 +5,7 @@ from pathlib import Path
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2407_19977_b200 import RenderSettings, build_bvh, render_progressive  # noqa: E402
-from paper_2407_19977_b200.procgen import scene_by_name  # noqa: E402
+from workloads import scene_by_name  # noqa: E402
 
 scene = scene_by_name("cornell_c1")
 bvh = build_bvh(scene.triangles)
