@@ -108,3 +108,40 @@ def oracle_lib():
     from oracle import oracle
     oracle.build()
     return oracle
+
+
+# ------------------------------------------------------------------ parity record
+
+PARITY_LOG = ROOT / "gpurun_out" / "parity_r02.jsonl"
+
+
+def record_parity(test: str, **fields) -> None:
+    """Append one parity measurement (agreement fractions, id-mismatch
+    counts) to gpurun_out/parity_r02.jsonl; tools/parity_report.py folds the
+    lines into the committed profiles/parity_r02.json."""
+    import json
+    import time
+    PARITY_LOG.parent.mkdir(exist_ok=True)
+    with open(PARITY_LOG, "a") as f:
+        f.write(json.dumps({"test": test, "time": time.strftime("%Y-%m-%dT%H:%M:%S"),
+                            **fields}, default=float) + "\n")
+
+
+def agreement_tiers(got, ref, rels=(1e-5, 1e-4, 1e-3, 1e-2)) -> dict:
+    """Fraction of (pixel, sample) rows whose three channels satisfy
+    |got - ref| <= rel * max(1, |ref|), per tolerance; rows where both are
+    non-finite count as agreeing, exactly one non-finite as disagreeing."""
+    got = np.asarray(got).reshape(-1, 3)
+    ref = np.asarray(ref).reshape(-1, 3)
+    fin_g = np.isfinite(got).all(axis=1)
+    fin_r = np.isfinite(ref).all(axis=1)
+    both_nan = ~fin_g & ~fin_r
+    err = np.abs(np.nan_to_num(got) - np.nan_to_num(ref)) / np.maximum(1.0, np.abs(
+        np.nan_to_num(ref)))
+    worst = err.max(axis=1)
+    out = {"rows": int(got.shape[0]), "nonfinite_mismatch": int(np.sum(fin_g != fin_r))}
+    for r in rels:
+        ok = (fin_g & fin_r & (worst <= r)) | both_nan
+        out[f"frac_le_{r:g}"] = float(ok.mean())
+        out[f"count_gt_{r:g}"] = int((~ok).sum())
+    return out

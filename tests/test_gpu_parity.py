@@ -18,7 +18,7 @@ import pytest
 
 import workloads as wl
 
-from conftest import golden_scene
+from conftest import agreement_tiers, golden_scene, record_parity
 
 pytestmark = pytest.mark.gpu
 
@@ -62,6 +62,8 @@ def test_intersect_batch_matches_reference(name):
     idx, t = lb().intersect_scene_batch(g.triangles, g.bvh, g["rays_o"], g["rays_d"], scene=ds)
     ref_i, ref_t = g["isect_idx"], g["isect_t"]
     mism = int(np.sum(idx != ref_i))
+    record_parity("fixture_ids", scene=name, rays=len(idx), id_mismatches=mism,
+                  ppm=1e6 * mism / len(idx))
     assert mism <= 2, f"{mism} id mismatches of {len(idx)}"
     same = (idx == ref_i) & (ref_i >= 0)
     assert np.all(np.abs(t[same] - ref_t[same]) <= 2e-5 * np.maximum(1.0, ref_t[same]))
@@ -139,11 +141,15 @@ def test_roulette_unbiased_and_dyadic():
 def test_per_sample_radiance_matched_streams(name):
     g = golden_scene(name)
     ds = device_scene(g)
-    fracs = []
+    fracs, gots = [], []
     for s, ref in enumerate(g["per_sample"]):
         got = gpu_sample_values(ds, g.camera, g.settings, s)
+        gots.append(got)
         fracs.append(close_fraction(got, ref.reshape(-1, 3)))
     frac = float(np.mean(fracs))
+    record_parity("fixture_per_sample", scene=name,
+                  **agreement_tiers(np.concatenate(gots), np.concatenate(
+                      [r.reshape(-1, 3) for r in g["per_sample"]])))
     print(f"{name}: per-sample agreement {frac:.5f}")
     assert frac >= 0.99
 
@@ -359,6 +365,8 @@ def test_primary_hits_at_scale(scene_name):
     ref_i, ref_t = oc.intersect_batch(o, d)
     idx, t = m.intersect_scene_batch(sc.triangles, bvh, o, d, scene=ds)
     mism = int(np.sum(idx != ref_i))
+    record_parity("scale_primary_ids", scene=scene_name, rays=pix.size, id_mismatches=mism,
+                  ppm=1e6 * mism / pix.size)
     print(f"{scene_name}: {mism} primary-hit id mismatches of {pix.size} "
           f"({1e6 * mism / pix.size:.1f} ppm)")
     assert mism <= max(2, int(50e-6 * pix.size))
@@ -378,12 +386,16 @@ def test_per_sample_parity_at_scale():
     st = m.RenderSettings(samples_per_pixel=1, max_depth=8, seed=9)
     cam = m.camera_pack(sc.camera)
     pix = np.arange(192 * 108)
-    fr = []
+    fr, gots, refs = [], [], []
     for s in range(2):
         ref, _ = oc.sample_values(pix, s, cam, 192, 108, st.seed, st.max_depth,
                                   st.rr_start_depth, st.t_min)
         got = gpu_sample_values(ds, sc.camera, st, s)
         fr.append(close_fraction(got, ref))
+        gots.append(got)
+        refs.append(ref)
+    record_parity("scale_per_sample", scene="sphere70k",
+                  **agreement_tiers(np.concatenate(gots), np.concatenate(refs)))
     print(f"sphere70k per-sample agreement {np.mean(fr):.5f}")
     assert np.mean(fr) >= 0.99
 

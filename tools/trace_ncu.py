@@ -36,7 +36,8 @@ PCTS = {
     "dram_throughput_pct": "dram__throughput.avg.pct_of_peak_sustained_elapsed",
     "simt_threads": "smsp__thread_inst_executed_per_inst_executed.ratio",
 }
-UNITS = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
+UNITS = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "ns": 1e-9,
+         "us": 1e-6, "ms": 1e-3,
          "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1.0}
 
 
@@ -80,7 +81,7 @@ def summarize(a):
         "rays": rays, "launches": len(launches),
         "ncu_serialized_ms": dur * 1e3,
         "source_sha": trace_source_sha(),
-        "source": f"{a.csv}: ncu of the {len(launches)} k_trace launches of one whole-frame "
+        "source": f"profiles/r02_trace_ncu_{a.workload}.csv: ncu of the {len(launches)} k_trace launches of one whole-frame "
                   f"batch ({rays} rays, LT_LANES=1, tools/trace_ncu.py)",
     }
     for k, m in PCTS.items():
