@@ -215,6 +215,14 @@ int lt_tonemap_u8(const float *linear, int64_t n_pixels, uint8_t *out, void *str
  * draws; front (n,) geometric-side flag (transmission only). ---- */
 int lt_bsdf_eval_batch(const double *params, const double *wo, const double *wi,
                        const double *normal, int64_t n, double *f, double *pdf);
+/* The same with the effective BSDF of the extension estimator for coat /
+ * transmission materials (the value and density sample_bsdf realizes; see
+ * csrc/lt_material.cuh eval_material): front (n,) geometric side (NULL =
+ * outside), for the dielectric interface's eta.  lt_bsdf_eval_batch = this
+ * with front NULL.  Extension: no reference (parity unpinned). */
+int lt_bsdf_eval_ext_batch(const double *params, const double *wo, const double *wi,
+                           const double *normal, const int32_t *front, int64_t n, double *f,
+                           double *pdf);
 int lt_bsdf_sample_batch(const double *params, const double *wo, const double *normal,
                          const double *u, const int32_t *front, int64_t n, int32_t *ok,
                          double *wi, double *weight);

@@ -640,7 +640,9 @@ static int oc_sample_glass(const double wo[3], const double n[3], const oc_mat *
   return 1;
 }
 
-/* Extension: clear-coat GGX lobe on top of the base.  PARITY UNPINNED. */
+/* Extension: clear-coat GGX lobe on top of the base, picked with probability
+ * cw F(no); the base's light crosses the coat twice, (1 - cw F(no)) (1 - cw
+ * F(|ni|)) -- the estimator of csrc/lt_material.cuh.  PARITY UNPINNED. */
 static int oc_sample_coat(const double wo[3], const double n[3], const oc_mat *mt,
                           double p_coat, double u1, double u2, double wi[3], double wgt[3],
                           double *pdf_out, int *spike) {
@@ -671,19 +673,19 @@ static int oc_sample_coat(const double wo[3], const double n[3], const oc_mat *m
 static int oc_sample_material(const double wo[3], const double n[3], const oc_mat *mt,
                               int front, double u_lobe, double u1, double u2, double wi[3],
                               double wgt[3], double *pdf, int *spike) {
-  double under = 1.0;
+  double under = 1.0, f0c = 0.0;
   if (mt->cw > 0.0) {
     double no = dot3(n, wo);
     if (no <= 0.0) return 0;
-    double f0c = oc_f0_from_ior(mt->cior);
-    double fc = f0c + (1.0 - f0c) * oc_pow5(1.0 - no);
+    f0c = oc_f0_from_ior(mt->cior);
+    double fo = f0c + (1.0 - f0c) * oc_pow5(1.0 - no);
+    double fc = fo;
     if (fc < 0.05) fc = 0.05;
     else if (fc > 0.95) fc = 0.95;
     double p_coat = mt->cw * fc;
     if (u_lobe < p_coat) return oc_sample_coat(wo, n, mt, p_coat, u1, u2, wi, wgt, pdf, spike);
     u_lobe = (u_lobe - p_coat) / (1.0 - p_coat);
-    double fbar = f0c + (1.0 - f0c) / 21.0;
-    under = (1.0 - mt->cw * fbar) / (1.0 - p_coat);
+    under = (1.0 - mt->cw * fo) / (1.0 - p_coat);
   }
   int ok;
   if (mt->tw > 0.0 && mt->m < 1.0) {
@@ -709,7 +711,10 @@ static int oc_sample_material(const double wo[3], const double n[3], const oc_ma
   } else {
     ok = oc_sample_reference(wo, n, mt, 1.0, u_lobe, u1, u2, wi, wgt, pdf, spike);
   }
-  if (ok && under != 1.0) {
+  if (ok && mt->cw > 0.0) {
+    /* the light that reaches the base crosses the coat twice */
+    double fi = f0c + (1.0 - f0c) * oc_pow5(1.0 - fabs(dot3(n, wi)));
+    under = under * (1.0 - mt->cw * fi);
     for (int k = 0; k < 3; ++k) {
       double tint = 1.0 + (mt->cc[k] - 1.0) * mt->cw;
       wgt[k] = wgt[k] * under * tint;

@@ -128,6 +128,7 @@ SIGNATURES = {
                                   C.c_void_p, C.c_void_p]),
     "lt_read_bandwidth": (C.c_int, [C.c_int32, C.c_int64, C.c_int32, C.POINTER(C.c_double)]),
     "lt_bsdf_eval_batch": (C.c_int, [_dp, _dp, _dp, _dp, C.c_int64, _dp, _dp]),
+    "lt_bsdf_eval_ext_batch": (C.c_int, [_dp, _dp, _dp, _dp, _ip, C.c_int64, _dp, _dp]),
     "lt_bsdf_sample_batch": (C.c_int, [_dp, _dp, _dp, _dp, _ip, C.c_int64, _ip, _dp, _dp]),
     "lt_occluded_batch_host": (C.c_int, [C.c_void_p, _dp, _dp, C.c_int64, C.c_double,
                                          C.c_double, _ip]),

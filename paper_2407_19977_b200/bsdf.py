@@ -37,18 +37,23 @@ def _v3(a, n):
     return np.ascontiguousarray(np.broadcast_to(np.asarray(a, dtype=np.float64), (n, 3)))
 
 
-def eval_pdf_batch(params, wo, wi, normal):
+def eval_pdf_batch(params, wo, wi, normal, front=None):
     """(f (n,3), pdf (n,)) for n cases; `params` are OpenPbrParams-like
-    objects or (n,21) rows."""
+    objects or (n,21) rows.  For coat / transmission materials: the
+    effective BSDF and density the extension sampler realizes (`front`: the
+    geometric side, for the interface's eta; default outside)."""
     p = params if isinstance(params, np.ndarray) else material_rows(params)
     n = p.shape[0]
     wo, wi, nr = _v3(wo, n), _v3(wi, n), _v3(normal, n)
+    fr = None if front is None else np.ascontiguousarray(
+        np.broadcast_to(np.asarray(front, dtype=np.int32), (n,)))
     f = np.zeros((n, 3))
     pdf = np.zeros(n)
     P = _lib.ptr
-    _lib.check(_lib.lib().lt_bsdf_eval_batch(P(p, C.c_double), P(wo, C.c_double),
-                                             P(wi, C.c_double), P(nr, C.c_double), n,
-                                             P(f, C.c_double), P(pdf, C.c_double)))
+    _lib.check(_lib.lib().lt_bsdf_eval_ext_batch(
+        P(p, C.c_double), P(wo, C.c_double), P(wi, C.c_double), P(nr, C.c_double),
+        P(fr, C.c_int32) if fr is not None else None, n, P(f, C.c_double),
+        P(pdf, C.c_double)))
     return f, pdf
 
 
@@ -58,7 +63,8 @@ def sample_batch(params, wo, normal, draws, front=None):
     n = p.shape[0]
     wo, nr = _v3(wo, n), _v3(normal, n)
     u = np.ascontiguousarray(np.asarray(draws, dtype=np.float64).reshape(n, 3))
-    fr = None if front is None else np.ascontiguousarray(front, dtype=np.int32).reshape(n)
+    fr = None if front is None else np.ascontiguousarray(
+        np.broadcast_to(np.asarray(front, dtype=np.int32), (n,)))
     ok = np.zeros(n, np.int32)
     wi = np.zeros((n, 3))
     w = np.zeros((n, 3))

@@ -648,7 +648,6 @@ static void build_material(const lt_scene_desc *d, int i, GpuMaterial &g) {
     g.calpha = (float)ca;
     g.ca2 = (float)(ca * ca);
     g.f0c = (float)f0c;
-    g.cfbar = (float)(f0c + (1.0 - f0c) / 21.0);
   }
   for (int k = 0; k < 3; ++k) {
     g.cc[k] = d->coat_color ? (float)d->coat_color[3 * i + k] : 1.f;
@@ -1791,14 +1790,15 @@ static void materials_from_params(const double *p, int64_t n, std::vector<GpuMat
   for (int64_t i = 0; i < n; ++i) build_material(&d, (int)i, out[i]);
 }
 
-extern "C" int lt_bsdf_eval_batch(const double *params, const double *wo, const double *wi,
-                                  const double *normal, int64_t n, double *f, double *pdf) {
+extern "C" int lt_bsdf_eval_ext_batch(const double *params, const double *wo, const double *wi,
+                                      const double *normal, const int32_t *front, int64_t n,
+                                      double *f, double *pdf) {
   if (n < 0 || (n > 0 && (!params || !wo || !wi || !normal || !f || !pdf)))
     return lt_fail(LT_ERR_INVALID, "invalid bsdf arguments");
   if (n == 0) return LT_OK;
   std::vector<GpuMaterial> mats;
   materials_from_params(params, n, mats);
-  DevBuf dm, da;
+  DevBuf dm, da, dfr;
   RET(dm.ensure(sizeof(GpuMaterial) * n));
   RET(da.ensure(sizeof(double) * 13 * n));
   double *dwo = da.as<double>(), *dwi = dwo + 3 * n, *dn = dwi + 3 * n, *df = dn + 3 * n,
@@ -1807,11 +1807,21 @@ extern "C" int lt_bsdf_eval_batch(const double *params, const double *wo, const 
   CK(cudaMemcpy(dwo, wo, 24 * n, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(dwi, wi, 24 * n, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(dn, normal, 24 * n, cudaMemcpyHostToDevice));
-  launch_bsdf_eval(dm.as<GpuMaterial>(), dwo, dwi, dn, n, df, dp, 0);
+  if (front) {
+    RET(dfr.ensure(sizeof(int32_t) * n));
+    CK(cudaMemcpy(dfr.p, front, 4 * n, cudaMemcpyHostToDevice));
+  }
+  launch_bsdf_eval(dm.as<GpuMaterial>(), dwo, dwi, dn, front ? dfr.as<int32_t>() : nullptr, n,
+                   df, dp, 0);
   CK(cudaGetLastError());
   CK(cudaMemcpy(f, df, 24 * n, cudaMemcpyDeviceToHost));
   CK(cudaMemcpy(pdf, dp, 8 * n, cudaMemcpyDeviceToHost));
   return LT_OK;
+}
+
+extern "C" int lt_bsdf_eval_batch(const double *params, const double *wo, const double *wi,
+                                  const double *normal, int64_t n, double *f, double *pdf) {
+  return lt_bsdf_eval_ext_batch(params, wo, wi, normal, nullptr, n, f, pdf);
 }
 
 extern "C" int lt_bsdf_sample_batch(const double *params, const double *wo, const double *normal,

@@ -85,7 +85,7 @@ struct __align__(16) GpuMaterial {
   float m, sw, alpha, f0d;    // metalness, specular_weight, alpha_of(rough), f0_from_ior
   float sc[3], diff;          // specular_color, bw/pi (1 - avg Fresnel)
   float el, ec[3];            // emission luminance / color
-  float cw, calpha, f0c, cfbar;  // coat extension
+  float cw, calpha, f0c, rsv;    // coat extension (rsv: unused)
   float cc[3], tw;            // coat color, transmission weight
   float tc[3], ior;           // transmission color, specular ior
   uint32_t flags;

@@ -903,17 +903,19 @@ __device__ __forceinline__ f3 load3(const double *a, int64_t i) {
 // eval_bsdf / pdf_bsdf (material.py:389-407) with the shade kernel's code
 __global__ void k_bsdf_eval(const GpuMaterial *__restrict__ mats, const double *__restrict__ wo,
                             const double *__restrict__ wi, const double *__restrict__ nrm,
-                            int64_t n, double *__restrict__ f, double *__restrict__ pdf) {
+                            const int32_t *__restrict__ front, int64_t n, double *__restrict__ f,
+                            double *__restrict__ pdf) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   const GpuMaterial mt = mats[i];
-  const float opaque = (mt.flags & MAT_GLASS) ? 1.f - mt.tw : 1.f;
-  const f3 a = load3(wo, i), b = load3(wi, i), c = load3(nrm, i);
-  const f3 v = eval_core(a, b, c, mt, opaque);
+  f3 v;
+  float p;
+  eval_material(load3(wo, i), load3(wi, i), load3(nrm, i), mt, front ? front[i] != 0 : true, v,
+                p);
   f[3 * i] = v.x;
   f[3 * i + 1] = v.y;
   f[3 * i + 2] = v.z;
-  pdf[i] = pdf_core(a, b, c, mt, opaque);
+  pdf[i] = p;
 }
 
 // sample_bsdf (material.py:410-426): the draws are rounded toward zero to
@@ -949,8 +951,10 @@ __global__ void k_occluded(SceneView sc, const float4 *__restrict__ q_o,
 }
 
 void launch_bsdf_eval(const GpuMaterial *mats, const double *wo, const double *wi,
-                      const double *nrm, int64_t n, double *f, double *pdf, cudaStream_t st) {
-  if (n > 0) k_bsdf_eval<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(mats, wo, wi, nrm, n, f, pdf);
+                      const double *nrm, const int32_t *front, int64_t n, double *f, double *pdf,
+                      cudaStream_t st) {
+  if (n > 0)
+    k_bsdf_eval<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(mats, wo, wi, nrm, front, n, f, pdf);
 }
 
 void launch_bsdf_sample(const GpuMaterial *mats, const double *wo, const double *nrm,

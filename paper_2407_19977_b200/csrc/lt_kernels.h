@@ -145,7 +145,8 @@ void launch_material_sort(const SceneView &sc, const float4 *hits, const int32_t
 void launch_accum_finish(const float *sum, const uint32_t *valid, const uint32_t *invalid,
                          int64_t n_pix, double *mean, int64_t *inv, cudaStream_t st);
 void launch_bsdf_eval(const GpuMaterial *mats, const double *wo, const double *wi,
-                      const double *nrm, int64_t n, double *f, double *pdf, cudaStream_t st);
+                      const double *nrm, const int32_t *front, int64_t n, double *f, double *pdf,
+                      cudaStream_t st);
 void launch_bsdf_sample(const GpuMaterial *mats, const double *wo, const double *nrm,
                         const double *u, const int32_t *front, int64_t n, int32_t *ok, double *wi,
                         double *wgt, cudaStream_t st);

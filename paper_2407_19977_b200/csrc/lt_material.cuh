@@ -266,7 +266,11 @@ __device__ __forceinline__ bool sample_coat(f3 wo, f3 n, const GpuMaterial &mt, 
 
 // _sample_core with the extension chain on the same lobe draw:
 // coat -> [metal | glass | reference dielectric]; reduces exactly to the
-// reference for materials without coat/transmission
+// reference for materials without coat/transmission.  The coat is a GGX
+// interface of Schlick reflectance F (f0 from coat_ior) picked with
+// probability cw F(no); the light that reaches the base crosses it twice
+// and keeps (1 - cw F(no)) (1 - cw F(|ni|)) -- reciprocal, and energy
+// conserving up to the coat's own masking (white furnace <= 1).
 __device__ __forceinline__ bool sample_material(f3 wo, f3 n, const GpuMaterial &mt, bool front,
                                                 float u_lobe, float u1, float u2, f3 &wi,
                                                 f3 &wgt) {
@@ -277,12 +281,11 @@ __device__ __forceinline__ bool sample_material(f3 wo, f3 n, const GpuMaterial &
   if (mt.flags & MAT_COAT) {
     float no = dot(n, wo);
     if (no <= 0.f) return false;
-    float fc = mt.f0c + (1.f - mt.f0c) * pow5f(1.f - no);
-    fc = fminf(fmaxf(fc, 0.05f), 0.95f);
-    float p_coat = mt.cw * fc;
+    const float fo = mt.f0c + (1.f - mt.f0c) * pow5f(1.f - no);
+    float p_coat = mt.cw * fminf(fmaxf(fo, 0.05f), 0.95f);
     if (u_lobe < p_coat) return sample_coat(wo, n, mt, p_coat, u1, F, wi, wgt);
     u_lobe = (u_lobe - p_coat) / (1.f - p_coat);
-    under = (1.f - mt.cw * mt.cfbar) / (1.f - p_coat);
+    under = (1.f - mt.cw * fo) / (1.f - p_coat);
   }
   bool ok;
   if (mt.flags & MAT_GLASS) {
@@ -298,9 +301,130 @@ __device__ __forceinline__ bool sample_material(f3 wo, f3 n, const GpuMaterial &
     ok = sample_reference(wo, n, mt, 1.f, u_lobe, u1, F, wi, wgt);
   }
   if (ok && (mt.flags & MAT_COAT)) {
+    // light crosses the coat twice: (1 - cw F(no)) (1 - cw F(|ni|))
+    const float fi = mt.f0c + (1.f - mt.f0c) * pow5f(1.f - fabsf(dot(n, wi)));
+    under *= 1.f - mt.cw * fi;
     wgt.x *= under * (1.f + (mt.cc[0] - 1.f) * mt.cw);
     wgt.y *= under * (1.f + (mt.cc[1] - 1.f) * mt.cw);
     wgt.z *= under * (1.f + (mt.cc[2] - 1.f) * mt.cw);
   }
   return ok;
+}
+
+// ---- the effective BSDF of the extension estimator (no reference; checked
+// by furnace, reciprocity and chi-square tests, tests/test_gpu_functions.py)
+//
+// sample_material draws one lobe per scatter; the value and density that
+// sampler realizes are:
+//   f   = f_coat + (1 - cw F(no)) (1 - cw F(|ni|)) * tint_c * f_under
+//   pdf = p_coat * pdf_coat + (1 - p_coat) * pdf_under
+//   f_under   = f_ref(opaque = 1 - tw) + (1 - m) * tw * f_glass
+//   pdf_under = pdf_ref(opaque)        + (1 - m) * tw * pdf_glass
+// with the rough-dielectric interface of Walter et al. 2007 for the glass
+// lobe (h ~ D(h) n.h, reflection with probability F):
+//   reflection   f = F D G / (4 no |ni|),            pdf = F D nh / (4 wo.h)
+//   transmission f = (1-F) D G (wo.h)|wi.h| / (no |ni| (eta wo.h + wi.h)^2) * tint_t,
+//                pdf = (1-F) D nh |wi.h| / (eta wo.h + wi.h)^2
+// (eta = eta_wo / eta_wi); every sample weight equals f |ni| / (lobe pdf).
+
+__device__ __forceinline__ void eval_glass(f3 wo, f3 wi, f3 n, const GpuMaterial &mt, bool front,
+                                           f3 &f, float &pdf) {
+  f = f3{0.f, 0.f, 0.f};
+  pdf = 0.f;
+  const float no = dot(n, wo), ni = dot(n, wi);
+  if (no <= 0.f || ni == 0.f) return;
+  const float eta = front ? 1.f / mt.ior : mt.ior;
+  const bool reflect = ni > 0.f;
+  float hx, hy, hz;
+  if (reflect) {
+    hx = wo.x + wi.x;
+    hy = wo.y + wi.y;
+    hz = wo.z + wi.z;
+  } else {  // wi = -eta wo + k h  =>  h ~ wi + eta wo
+    hx = wi.x + eta * wo.x;
+    hy = wi.y + eta * wo.y;
+    hz = wi.z + eta * wo.z;
+  }
+  const float hl = sqrtf(hx * hx + hy * hy + hz * hz);
+  if (!(hl > 0.f)) return;
+  float s = 1.f / hl;
+  if (n.x * hx + n.y * hy + n.z * hz < 0.f) s = -s;
+  const f3 h{hx * s, hy * s, hz * s};
+  const float c = dot(wo, h), ih = dot(wi, h), nh = dot(n, h);
+  if (c <= 0.f || nh <= 0.f) return;
+  const float sin2t = eta * eta * (1.f - c * c);
+  float F = 1.f;
+  if (sin2t < 1.f) {
+    const float cos_t = sqrtf(1.f - sin2t);
+    const float rs = (eta * c - cos_t) / (eta * c + cos_t);
+    const float rp = (c - eta * cos_t) / (c + eta * cos_t);
+    F = 0.5f * (rs * rs + rp * rp);
+  }
+  const float D = ggx_ndf(nh, mt.a2);
+  const float G = smith_g2(no, fabsf(ni), mt.a2);
+  if (reflect) {
+    const float v = F * D * G / (4.f * no * ni);
+    f = f3{v, v, v};
+    pdf = F * D * nh / (4.f * c);
+  } else {
+    if (ih >= 0.f || F >= 1.f) return;  // not reachable by refraction
+    const float den = eta * c + ih;
+    const float q = (1.f - F) * D / (den * den);
+    const float v = q * G * c * fabsf(ih) / (no * fabsf(ni));
+    f = f3{v * mt.tc[0], v * mt.tc[1], v * mt.tc[2]};
+    pdf = q * nh * fabsf(ih);
+  }
+}
+
+__device__ __forceinline__ void eval_material(f3 wo, f3 wi, f3 n, const GpuMaterial &mt,
+                                              bool front, f3 &f, float &pdf) {
+  if (!(mt.flags & (MAT_COAT | MAT_GLASS))) {
+    f = eval_core(wo, wi, n, mt, 1.f);
+    pdf = pdf_core(wo, wi, n, mt, 1.f);
+    return;
+  }
+  const float opaque = (mt.flags & MAT_GLASS) ? 1.f - mt.tw : 1.f;
+  f3 fu = eval_core(wo, wi, n, mt, opaque);
+  float pu = pdf_core(wo, wi, n, mt, opaque);
+  if (mt.flags & MAT_GLASS) {
+    f3 fg;
+    float pg;
+    eval_glass(wo, wi, n, mt, front, fg, pg);
+    const float sg = (1.f - mt.m) * mt.tw;
+    fu = f3{fu.x + sg * fg.x, fu.y + sg * fg.y, fu.z + sg * fg.z};
+    pu += sg * pg;
+  }
+  if (!(mt.flags & MAT_COAT)) {
+    f = fu;
+    pdf = pu;
+    return;
+  }
+  f = f3{0.f, 0.f, 0.f};
+  pdf = 0.f;
+  const float no = dot(n, wo), ni = dot(n, wi);
+  if (no <= 0.f) return;
+  const float fo = mt.f0c + (1.f - mt.f0c) * pow5f(1.f - no);
+  const float p_coat = mt.cw * fminf(fmaxf(fo, 0.05f), 0.95f);
+  float fc = 0.f, pc = 0.f;
+  if (ni > 0.f) {
+    float hx = wo.x + wi.x, hy = wo.y + wi.y, hz = wo.z + wi.z;
+    const float hl = sqrtf(hx * hx + hy * hy + hz * hz);
+    if (hl > 0.f) {
+      const float r = 1.f / hl;
+      const f3 h{hx * r, hy * r, hz * r};
+      const float oh = dot(wo, h), nh = dot(n, h);
+      if (oh > 0.f && nh > 0.f) {
+        const float D = ggx_ndf(nh, mt.ca2);
+        fc = mt.cw * (mt.f0c + (1.f - mt.f0c) * pow5f(1.f - oh)) * D *
+             smith_g2(no, ni, mt.ca2) / (4.f * no * ni);
+        pc = D * nh / (4.f * oh);
+      }
+    }
+  }
+  const float under = (1.f - mt.cw * fo) *
+                      (1.f - mt.cw * (mt.f0c + (1.f - mt.f0c) * pow5f(1.f - fabsf(ni))));
+  f = f3{fc + under * (1.f + (mt.cc[0] - 1.f) * mt.cw) * fu.x,
+         fc + under * (1.f + (mt.cc[1] - 1.f) * mt.cw) * fu.y,
+         fc + under * (1.f + (mt.cc[2] - 1.f) * mt.cw) * fu.z};
+  pdf = p_coat * pc + (1.f - p_coat) * pu;
 }

@@ -96,24 +96,67 @@ def test_headline_per_sample_parity(name):
     assert all_rows["nonfinite_mismatch"] == 0
 
 
+def edge_margin(tris, k, o, d):
+    """float64 plane hit of ray (o, d) with triangle k: (t, signed distance
+    of the hit point to the triangle's boundary in world units; >= 0 inside)."""
+    a, b, c = tris.v0[k], tris.v1[k], tris.v2[k]
+    n = np.cross(b - a, c - a)
+    n /= np.linalg.norm(n)
+    t = np.dot(a - o, n) / np.dot(d, n)
+    p = o + t * d
+    margin = np.inf
+    for u, v, w in ((a, b, c), (b, c, a), (c, a, b)):
+        e = np.cross(n, v - u)
+        e /= np.linalg.norm(e)
+        if np.dot(w - u, e) < 0:
+            e = -e
+        margin = min(margin, float(np.dot(p - u, e)))
+    return float(t), margin
+
+
+def classify_mismatch(tris, o, d, ours, ref):
+    """A mismatch is ulp-level when, in float64, the two candidates are a
+    near-tie in t or one of them is hit within EPS of its boundary (an
+    edge or vertex shared by neighbours), EPS = 1e-6 * (|o| + t): ~10
+    float32 ulps of the hit coordinates."""
+    t_o, m_o = edge_margin(tris, ours, o, d)
+    t_r, m_r = edge_margin(tris, ref, o, d)
+    eps = 1e-6 * (np.abs(o).max() + max(abs(t_o), abs(t_r)))
+    return {"tie": abs(t_o - t_r) <= eps, "edge": min(abs(m_o), abs(m_r)) <= eps,
+            "dt": abs(t_o - t_r), "margin": min(abs(m_o), abs(m_r)), "eps": eps}
+
+
 def test_headline_primary_hit_ids():
     """Full-frame primary-hit ids on the 1.06 M-triangle scene vs the
-    float64 oracle traversal of the same jittered rays."""
+    float64 oracle traversal of the same jittered rays; every mismatch is
+    classified in float64 as an edge or tie case."""
     import paper_2407_19977_b200 as m
     from oracle.oracle import primary_rays
     sc, bvh, ds, oc, cam = headline("pushbutton_ref")
-    total, mism_total = 0, 0
+    total, mism_total, unexplained = 0, 0, []
     for s in range(2):
         o, d = primary_rays(np.arange(W * H), s, cam, W, H, 0)
         ref_i, ref_t = oc.intersect_batch(o, d)
         idx, t = m.intersect_scene_batch(sc.triangles, bvh, o, d, scene=ds)
-        mism = int(np.sum(idx != ref_i))
+        bad = np.nonzero(idx != ref_i)[0]
+        flips = int(np.sum((idx >= 0) != (ref_i >= 0)))
+        kinds = [classify_mismatch(sc.triangles, o[r], d[r], idx[r], ref_i[r])
+                 for r in bad if idx[r] >= 0 and ref_i[r] >= 0]
+        edge = sum(k["edge"] for k in kinds)
+        tie = sum(k["tie"] and not k["edge"] for k in kinds)
+        unexplained += [k for k in kinds if not (k["edge"] or k["tie"])]
         same = (idx == ref_i) & (ref_i >= 0)
         rel_t = float(np.max(np.abs(t[same] - ref_t[same]) / np.maximum(1.0, ref_t[same])))
         total += idx.size
-        mism_total += mism
+        mism_total += bad.size
         record_parity("headline_primary_ids", scene="pushbutton_ref", sample=s, rays=idx.size,
-                      id_mismatches=mism, ppm=1e6 * mism / idx.size, max_rel_t=rel_t,
-                      hit_miss_flips=int(np.sum((idx >= 0) != (ref_i >= 0))))
+                      id_mismatches=int(bad.size), ppm=1e6 * bad.size / idx.size,
+                      max_rel_t=rel_t, hit_miss_flips=flips, edge_cases=int(edge),
+                      tie_cases=int(tie),
+                      max_margin_over_eps=max((k["margin"] / k["eps"] for k in kinds),
+                                              default=0.0))
         assert rel_t <= 2e-5
-    assert mism_total <= max(2, int(10e-6 * total))
+        assert flips == 0
+    print(f"{mism_total} id mismatches in {total} rays; unexplained {unexplained[:5]}")
+    assert mism_total <= int(50e-6 * total)
+    assert not unexplained
