@@ -168,6 +168,17 @@ int lt_intersect_batch(lt_scene *scene, const float *origins, const float *dirs,
  * float64 t (the fp32 result widened). */
 int lt_intersect_batch_host(lt_scene *scene, const double *origins, const double *dirs,
                             int64_t n, double t_min, double t_max, int64_t *idx, double *t);
+/* The same with the barycentrics of each hit: uv (n,2) float64 (0 on a miss);
+ * the scalar intersect_scene (bvh.py:632-641) builds its Hit from them. */
+int lt_intersect_hits_host(lt_scene *scene, const double *origins, const double *dirs,
+                           int64_t n, double t_min, double t_max, int64_t *idx, double *t,
+                           double *uv);
+/* Exhaustive closest hit: brute_force_intersect_batch (bvh.py:694-701,
+ * _brute_force_batch bvh.py:586-610), every triangle against every ray with
+ * the traversal's fp32 arithmetic and tie rule, so it equals
+ * lt_intersect_batch_host exactly (test_bvh.py:91-100). */
+int lt_brute_force_batch_host(lt_scene *scene, const double *origins, const double *dirs,
+                              int64_t n, double t_min, double t_max, int64_t *idx, double *t);
 /* Work counters: traversal_counts_batch (bvh.py:680-691), host buffers.
  * nodes = child-box tests + 1 (root), tests = triangle tests. */
 int lt_traversal_counts_host(lt_scene *scene, const double *origins, const double *dirs,
@@ -232,6 +243,44 @@ int lt_bsdf_sample_batch(const double *params, const double *wo, const double *n
  * within [t_min, t_max]. ---- */
 int lt_occluded_batch_host(lt_scene *scene, const double *origins, const double *dirs,
                            int64_t n, double t_min, double t_max, int32_t *occluded);
+
+/* ---- the reference's scalar query API in float64 on the device
+ * (csrc/lt_query64.cu, the reference's operation order, no FMA contraction).
+ * Host buffers; (n,3) arrays row-major. ---- */
+/* ray_triangle_intersect (geometry.py:255-278): per case a ray (origin,
+ * dir, t_min, t_max) and a triangle (v0..v2, n0..n2); ok, tuv (n,3) =
+ * (t, u, v), the hit frame of _hit_frame (geometry.py:210-241). */
+int lt_ray_triangle_batch(const double *origins, const double *dirs, const double *t_min,
+                          const double *t_max, const double *v0, const double *v1,
+                          const double *v2, const double *n0, const double *n1, const double *n2,
+                          int64_t n, int32_t *ok, double *tuv, double *geo_normal,
+                          double *shading_normal, int32_t *front);
+/* _hit_frame (geometry.py:210-241) at given barycentrics uv (n,2). */
+int lt_hit_frame_batch(const double *dirs, const double *v0, const double *v1, const double *v2,
+                       const double *n0, const double *n1, const double *n2, const double *uv,
+                       int64_t n, double *geo_normal, double *shading_normal, int32_t *front);
+/* ray_aabb_intersect (geometry.py:281-295): _inv_component + the
+ * compare/select _slab_intersect; t_enter_exit (n,2). */
+int lt_ray_aabb_batch(const double *origins, const double *dirs, const double *t_min,
+                      const double *t_max, const double *box_min, const double *box_max,
+                      int64_t n, int32_t *ok, double *t_enter_exit);
+/* eval_bsdf / pdf_bsdf / sample_bsdf (material.py:389-426) on the reference
+ * materials: params (n,11) = [bw, bc.rgb, m, sw, sc.rgb, roughness, ior]. */
+int lt_bsdf64_eval_batch(const double *params, const double *wo, const double *wi,
+                         const double *normal, int64_t n, double *f, double *pdf);
+int lt_bsdf64_sample_batch(const double *params, const double *wo, const double *normal,
+                           const double *u, int64_t n, int32_t *ok, double *wi, double *weight,
+                           double *pdf, int32_t *spike);
+/* microfacet helpers (material.py:107-126, 264-290, 371-386): op 0
+ * ggx_ndf(a = n.h, b = alpha) -> out (n,); 1 smith_g2(a = n.o, b = n.i,
+ * c = alpha); 2 cosine_sample_hemisphere(normal, a = u1, b = u2) -> out
+ * (n,3); 3 ggx_sample_half_vector(normal, c = alpha, a = u1, b = u2). */
+int lt_microfacet_batch(int32_t op, const double *a, const double *b, const double *c,
+                        const double *normal, int64_t n, double *out);
+/* display transform (tonemap.py:18-61): op 0 pbr_neutral_tonemap (n rgb
+ * triples -> out (n,3)), 1 linear_to_srgb, 2 srgb_to_linear (n values ->
+ * out), 3 quantize_to_u8 (n values -> out_u8). */
+int lt_display_batch(int32_t op, const double *in, int64_t n, double *out, uint8_t *out_u8);
 
 /* ---- measurement helper (not on the render path): streaming-read
  * bandwidth of a `bytes` device buffer, `iters` passes, CUDA events.  A

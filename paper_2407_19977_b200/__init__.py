@@ -6,13 +6,20 @@ Host code is Python; the hot path is hand-written sm_100a CUDA behind the
 C-ABI in include/luxb200.h (built in-tree by `build.py`).  There is no CPU
 fallback: compute entry points raise when the library or a GPU is missing.
 """
-from .geometry import (DEFAULT_T_MIN, Ray, Triangle, TriangleBuffer, normalize, vec3)
+from .geometry import (DEFAULT_T_MIN, Aabb, Hit, Ray, Triangle, TriangleBuffer, aabb_surface_area,
+                       aabb_union, normalize, ray_aabb_intersect, ray_triangle_intersect,
+                       triangle_bounds, vec3)
 from .material import (OpenPbrParams, emitted_radiance, pack_material_table, pack_materials)
 from .scene import (CameraConfig, EnvironmentConfig, SceneDescription, SceneError, camera_pack)
 from .rng import PcgState, next_unit_real, pcg_next_u32, pcg_seed, seed_stream
-from .bvh import (STACK_SIZE, BuildStats, Bvh, build_bvh, intersect_any, intersect_any_batch,
-                  intersect_scene, intersect_scene_batch, traversal_counts_batch)
-from .bsdf import BsdfSample, eval_bsdf, pdf_bsdf, sample_bsdf
+from .bvh import (STACK_SIZE, BuildStats, Bvh, brute_force_intersect_batch, build_bvh,
+                  intersect_any, intersect_any_batch, intersect_scene, intersect_scene_batch,
+                  intersect_scene_counted, traversal_counts_batch, validate_bvh)
+from .bsdf import (BsdfSample, cosine_sample_hemisphere, eval_bsdf, fresnel_schlick, ggx_ndf,
+                   ggx_sample_half_vector, pdf_bsdf, sample_bsdf, smith_g2)
+from .tonemap import (linear_to_srgb, pbr_neutral_tonemap, quantize_to_u8, srgb_to_linear,
+                      tonemap_to_u8, write_linear_dump, write_png)
+from ._parallel import set_worker_count, thread_cap
 from .device import DeviceScene
 from .integrator import (RenderResult, RenderSettings, environment_radiance,
                          generate_camera_ray, render_image, render_pass, render_progressive,
@@ -24,13 +31,19 @@ from .ingest import (MaterialMap, RenderConfig, flatten_scene, generate_smooth_n
 __version__ = "0.1.0"
 
 __all__ = [
-    "DEFAULT_T_MIN", "Ray", "Triangle", "TriangleBuffer", "normalize", "vec3",
+    "DEFAULT_T_MIN", "Aabb", "Hit", "Ray", "Triangle", "TriangleBuffer", "aabb_surface_area",
+    "aabb_union", "normalize", "ray_aabb_intersect", "ray_triangle_intersect",
+    "triangle_bounds", "vec3",
     "OpenPbrParams", "emitted_radiance", "pack_material_table", "pack_materials",
     "CameraConfig", "EnvironmentConfig", "SceneDescription", "SceneError", "camera_pack",
     "PcgState", "next_unit_real", "pcg_next_u32", "pcg_seed", "seed_stream",
-    "STACK_SIZE", "BuildStats", "Bvh", "build_bvh", "intersect_any", "intersect_any_batch",
-    "intersect_scene", "intersect_scene_batch", "traversal_counts_batch", "DeviceScene",
-    "BsdfSample", "eval_bsdf", "pdf_bsdf", "sample_bsdf",
+    "STACK_SIZE", "BuildStats", "Bvh", "brute_force_intersect_batch", "build_bvh",
+    "intersect_any", "intersect_any_batch", "intersect_scene", "intersect_scene_batch",
+    "intersect_scene_counted", "traversal_counts_batch", "validate_bvh", "DeviceScene",
+    "BsdfSample", "cosine_sample_hemisphere", "eval_bsdf", "fresnel_schlick", "ggx_ndf",
+    "ggx_sample_half_vector", "pdf_bsdf", "sample_bsdf", "smith_g2",
+    "linear_to_srgb", "pbr_neutral_tonemap", "quantize_to_u8", "srgb_to_linear",
+    "tonemap_to_u8", "write_linear_dump", "write_png", "set_worker_count", "thread_cap",
     "RenderResult", "RenderSettings", "environment_radiance", "generate_camera_ray",
     "render_image", "render_pass", "render_progressive", "trace_radiance",
     "trace_radiance_batch",

@@ -115,6 +115,20 @@ SIGNATURES = {
                                      C.c_float, C.c_void_p, C.c_void_p, C.c_void_p]),
     "lt_intersect_batch_host": (C.c_int, [C.c_void_p, _dp, _dp, C.c_int64, C.c_double,
                                           C.c_double, _lp, _dp]),
+    "lt_intersect_hits_host": (C.c_int, [C.c_void_p, _dp, _dp, C.c_int64, C.c_double,
+                                         C.c_double, _lp, _dp, _dp]),
+    "lt_brute_force_batch_host": (C.c_int, [C.c_void_p, _dp, _dp, C.c_int64, C.c_double,
+                                            C.c_double, _lp, _dp]),
+    "lt_ray_triangle_batch": (C.c_int, [_dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp,
+                                        C.c_int64, _ip, _dp, _dp, _dp, _ip]),
+    "lt_hit_frame_batch": (C.c_int, [_dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp, C.c_int64, _dp,
+                                     _dp, _ip]),
+    "lt_ray_aabb_batch": (C.c_int, [_dp, _dp, _dp, _dp, _dp, _dp, C.c_int64, _ip, _dp]),
+    "lt_bsdf64_eval_batch": (C.c_int, [_dp, _dp, _dp, _dp, C.c_int64, _dp, _dp]),
+    "lt_bsdf64_sample_batch": (C.c_int, [_dp, _dp, _dp, _dp, C.c_int64, _ip, _dp, _dp, _dp,
+                                         _ip]),
+    "lt_microfacet_batch": (C.c_int, [C.c_int32, _dp, _dp, _dp, _dp, C.c_int64, _dp]),
+    "lt_display_batch": (C.c_int, [C.c_int32, _dp, C.c_int64, _dp, _u8p]),
     "lt_traversal_counts_host": (C.c_int, [C.c_void_p, _dp, _dp, C.c_int64, C.c_double,
                                            C.c_double, _lp, _lp]),
     "lt_render_pass": (C.c_int, [C.c_void_p, C.POINTER(RenderParams), C.c_void_p, C.c_void_p,

@@ -1639,7 +1639,7 @@ extern "C" int lt_intersect_batch(lt_scene *s, const float *origins, const float
   launch_pack_rays_f32(origins, dirs, n, t_min, t_max, s->s_d.as<float4>(), s->s_e.as<float4>(),
                        st);
   RET(intersect_common(s, n, st, false, nullptr, nullptr));
-  launch_unpack_hits(s->view, s->s_f.as<float4>(), n, idx, t, nullptr, nullptr, st);
+  launch_unpack_hits(s->view, s->s_f.as<float4>(), n, idx, t, nullptr, nullptr, nullptr, st);
   CK(cudaGetLastError());
   return LT_OK;
 }
@@ -1658,24 +1658,53 @@ static int upload_rays_f64(lt_scene *s, const double *o, const double *d, int64_
   return LT_OK;
 }
 
-extern "C" int lt_intersect_batch_host(lt_scene *s, const double *origins, const double *dirs,
-                                       int64_t n, double t_min, double t_max, int64_t *idx,
-                                       double *t) {
+// Closest hits of host rays (fp32 traversal, or the exhaustive kernel) as
+// the reference's dtypes: idx int64 / t float64, optionally (u, v).
+static int hits_host(lt_scene *s, const double *origins, const double *dirs, int64_t n,
+                     double t_min, double t_max, bool brute, int64_t *idx, double *t,
+                     double *uv) {
   if (!s || n < 0) return lt_fail(LT_ERR_INVALID, "invalid arguments");
   if (n == 0) return LT_OK;
   if (!origins || !dirs || !idx || !t) return lt_fail(LT_ERR_INVALID, "null ray buffer");
   DeviceGuard g(s->device);
   cudaStream_t st = s->stream;
   RET(upload_rays_f64(s, origins, dirs, n, t_min, t_max, st));
-  RET(intersect_common(s, n, st, false, nullptr, nullptr));
-  RET(s->s_a.ensure(16 * n));
+  if (brute) {
+    RET(s->s_f.ensure(std::max<int64_t>(16, 16 * n)));
+    launch_brute_force(s->view, s->n_tris, s->s_d.as<float4>(), s->s_e.as<float4>(), n,
+                       s->s_f.as<float4>(), st);
+    CK(cudaGetLastError());
+  } else {
+    RET(intersect_common(s, n, st, false, nullptr, nullptr));
+  }
+  RET(s->s_a.ensure(32 * n));
   int64_t *d_idx = s->s_a.as<int64_t>();
   double *d_t = reinterpret_cast<double *>(d_idx + n);
-  launch_unpack_hits(s->view, s->s_f.as<float4>(), n, nullptr, nullptr, d_idx, d_t, st);
+  double *d_uv = uv ? d_t + n : nullptr;
+  launch_unpack_hits(s->view, s->s_f.as<float4>(), n, nullptr, nullptr, d_idx, d_t, d_uv, st);
   CK(cudaMemcpyAsync(idx, d_idx, 8 * n, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(t, d_t, 8 * n, cudaMemcpyDeviceToHost, st));
+  if (uv) CK(cudaMemcpyAsync(uv, d_uv, 16 * n, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   return LT_OK;
+}
+
+extern "C" int lt_intersect_batch_host(lt_scene *s, const double *origins, const double *dirs,
+                                       int64_t n, double t_min, double t_max, int64_t *idx,
+                                       double *t) {
+  return hits_host(s, origins, dirs, n, t_min, t_max, false, idx, t, nullptr);
+}
+
+extern "C" int lt_intersect_hits_host(lt_scene *s, const double *origins, const double *dirs,
+                                      int64_t n, double t_min, double t_max, int64_t *idx,
+                                      double *t, double *uv) {
+  return hits_host(s, origins, dirs, n, t_min, t_max, false, idx, t, uv);
+}
+
+extern "C" int lt_brute_force_batch_host(lt_scene *s, const double *origins, const double *dirs,
+                                         int64_t n, double t_min, double t_max, int64_t *idx,
+                                         double *t) {
+  return hits_host(s, origins, dirs, n, t_min, t_max, true, idx, t, nullptr);
 }
 
 extern "C" int lt_traversal_counts_host(lt_scene *s, const double *origins, const double *dirs,

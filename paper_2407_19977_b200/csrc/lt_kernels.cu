@@ -854,7 +854,8 @@ __global__ void k_pack_rays_f64(const double *__restrict__ o, const double *__re
 
 __global__ void k_unpack_hits(SceneView sc, const float4 *__restrict__ hits, int64_t n,
                               int32_t *__restrict__ idx32, float *__restrict__ t32,
-                              int64_t *__restrict__ idx64, double *__restrict__ t64) {
+                              int64_t *__restrict__ idx64, double *__restrict__ t64,
+                              double *__restrict__ uv64) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   const float4 h = hits[i];
@@ -865,6 +866,49 @@ __global__ void k_unpack_hits(SceneView sc, const float4 *__restrict__ hits, int
   if (t32) t32[i] = t;
   if (idx64) idx64[i] = orig;
   if (t64) t64[i] = (double)t;
+  if (uv64) {
+    uv64[2 * i] = k >= 0 ? (double)h.y : 0.0;
+    uv64[2 * i + 1] = k >= 0 ? (double)h.z : 0.0;
+  }
+}
+
+// Exhaustive closest hit (brute_force_intersect_batch, bvh.py:586-610,
+// 694-701) with the traversal's own fp32 Moller-Trumbore and (t, original
+// index) tie rule: one ray per thread, the leaf-ordered triangles streamed
+// through shared memory a block-sized tile at a time.  Its result equals the
+// BVH traversal's exactly (the closest hit is a lexicographic minimum and
+// the traversal's boxes are conservative) -- the GPU twin of the
+// reference's test_bvh.py:91-100 check.
+__global__ void __launch_bounds__(128)
+    k_brute_force(SceneView sc, int64_t n_tris, const float4 *__restrict__ q_o,
+                  const float4 *__restrict__ q_d, int64_t n, float4 *__restrict__ hits) {
+  __shared__ float4 tile[3 * 128];
+  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const bool live = q < n;
+  const float4 ro = live ? q_o[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+  const float4 rd = live ? q_d[q] : make_float4(0.f, 0.f, 1.f, 0.f);
+  const f3 o = mk(ro.x, ro.y, ro.z), d = mk(rd.x, rd.y, rd.z);
+  HitRec best{ro.w, 0.f, 0.f, -1};
+  int32_t best_orig = 0x7fffffff;
+  for (int64_t base = 0; base < n_tris; base += 128) {
+    const int64_t k = base + threadIdx.x;
+    __syncthreads();
+    if (k < n_tris)
+      for (int c = 0; c < 3; ++c) tile[3 * threadIdx.x + c] = __ldg(&sc.tris[LT_TRI_F4 * k + c]);
+    __syncthreads();
+    const int cnt = n_tris - base < 128 ? (int)(n_tris - base) : 128;
+    if (live)
+      for (int j = 0; j < cnt; ++j)
+        mt_test(o, d, rd.w, tile[3 * j], tile[3 * j + 1], tile[3 * j + 2], (int32_t)(base + j),
+                best, best_orig);
+  }
+  if (live) hits[q] = make_float4(best.t, best.u, best.v, __int_as_float(best.k));
+}
+
+void launch_brute_force(const SceneView &sc, int64_t n_tris, const float4 *q_o,
+                        const float4 *q_d, int64_t n, float4 *hits, cudaStream_t st) {
+  if (n > 0)
+    k_brute_force<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(sc, n_tris, q_o, q_d, n, hits);
 }
 
 // ------------------------------------------------------------------ display
@@ -1132,9 +1176,10 @@ void launch_pack_rays_f64(const double *o, const double *d, int64_t n, float t_m
 }
 
 void launch_unpack_hits(const SceneView &sc, const float4 *hits, int64_t n, int32_t *idx32,
-                        float *t32, int64_t *idx64, double *t64, cudaStream_t st) {
+                        float *t32, int64_t *idx64, double *t64, double *uv64, cudaStream_t st) {
   if (n <= 0) return;
-  k_unpack_hits<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(sc, hits, n, idx32, t32, idx64, t64);
+  k_unpack_hits<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(sc, hits, n, idx32, t32, idx64, t64,
+                                                             uv64);
 }
 
 // Shading class of queue entry q (k_shade's divergence classes).

@@ -132,7 +132,7 @@ void launch_pack_rays_f32(const float *o, const float *d, int64_t n, float t_min
 void launch_pack_rays_f64(const double *o, const double *d, int64_t n, float t_min, float t_max,
                           float4 *q_o, float4 *q_d, cudaStream_t st);
 void launch_unpack_hits(const SceneView &sc, const float4 *hits, int64_t n, int32_t *idx32,
-                        float *t32, int64_t *idx64, double *t64, cudaStream_t st);
+                        float *t32, int64_t *idx64, double *t64, double *uv64, cudaStream_t st);
 void launch_tonemap_u8(const float *lin, int64_t n_pixels, uint8_t *out, cudaStream_t st);
 // material-class grouping of a hit queue (LT_FLAG_SORT_MATERIALS): per
 // entry class (miss, final segment, diffuse-only, reference GGX, coat,
@@ -154,5 +154,29 @@ void launch_occluded(const SceneView &sc, const float4 *q_o, const float4 *q_d, 
                      int32_t *out, cudaStream_t st);
 void launch_read_probe(const float4 *src, int64_t n4, int passes, float *sink, int grid,
                        cudaStream_t st);
+// exhaustive closest hit over the leaf-ordered triangles (the traversal's
+// fp32 Moller-Trumbore and tie rule, no BVH): hits as k_trace_rays writes them
+void launch_brute_force(const SceneView &sc, int64_t n_tris, const float4 *q_o,
+                        const float4 *q_d, int64_t n, float4 *hits, cudaStream_t st);
+
+// ---- float64 query kernels (lt_query64.cu, the reference's arithmetic)
+void launch_ray_triangle64(const double *o, const double *d, const double *tmin,
+                           const double *tmax, const double *v0, const double *v1,
+                           const double *v2, const double *n0, const double *n1,
+                           const double *n2, int64_t n, int32_t *ok, double *tuv, double *g,
+                           double *s, int32_t *front, cudaStream_t st);
+void launch_hit_frame64(const double *d, const double *v0, const double *v1, const double *v2,
+                        const double *n0, const double *n1, const double *n2, const double *uv,
+                        int64_t n, double *g, double *s, int32_t *front, cudaStream_t st);
+void launch_ray_aabb64(const double *o, const double *d, const double *tmin, const double *tmax,
+                       const double *lo, const double *hi, int64_t n, int32_t *ok, double *tnf,
+                       cudaStream_t st);
+void launch_bsdf64(int mode, const double *params, const double *wo, const double *wi,
+                   const double *nrm, const double *u, int64_t n, int32_t *ok, double *out3a,
+                   double *out3b, double *out1, int32_t *flag, cudaStream_t st);
+void launch_microfacet64(int op, const double *a, const double *b, const double *c,
+                         const double *nrm, int64_t n, double *out, cudaStream_t st);
+void launch_display64(int op, const double *in, int64_t n, double *out, uint8_t *out8,
+                      cudaStream_t st);
 
 }  // namespace lt

@@ -1,9 +1,10 @@
-"""Host-side geometry types of the drop-in API.
+"""Geometry types and single-object queries of the drop-in API.
 
-Mirrors luxtrace.geometry's public names (geometry.py:22-131) so callers can
-pass either these objects or the reference's own (duck-typed: only the
-attributes are read).  No arithmetic of the hot path lives here; it runs in
-the CUDA kernels behind the C-ABI.
+Mirrors luxtrace.geometry's public names (geometry.py:22-131, 255-315) so
+callers can pass either these objects or the reference's own (duck-typed:
+only the attributes are read).  The ray / triangle and ray / box queries
+run the float64 device kernels of csrc/lt_query64.cu (the reference's
+arithmetic); the AABB helpers are the reference's own numpy expressions.
 """
 from __future__ import annotations
 
@@ -59,6 +60,30 @@ class Triangle:
     material_index: int = 0
 
 
+@dataclass
+class Aabb:
+    min: np.ndarray
+    max: np.ndarray
+
+    @classmethod
+    def empty(cls) -> "Aabb":
+        return cls(vec3(math.inf, math.inf, math.inf), vec3(-math.inf, -math.inf, -math.inf))
+
+    def is_empty(self) -> bool:
+        return bool(np.any(self.min > self.max))
+
+
+@dataclass
+class Hit:
+    t: float
+    triangle_index: int
+    barycentric_u: float
+    barycentric_v: float
+    geometric_normal: np.ndarray
+    shading_normal: np.ndarray
+    is_front_face: bool
+
+
 _CORNERS = ("v0", "v1", "v2", "n0", "n1", "n2")
 
 
@@ -102,3 +127,51 @@ class TriangleBuffer:
         tris = list(triangles)
         cols = {k: np.array([getattr(t, k) for t in tris], dtype=np.float64) for k in _CORNERS}
         return cls(**cols, material_index=np.array([t.material_index for t in tris], np.int32))
+
+
+# ------------------------------------------------------------------ queries
+
+def ray_triangle_intersect(ray: Ray, tri: Triangle, triangle_index: int = 0) -> Hit | None:
+    """Nearest double-sided hit of one ray with one triangle (geometry.py:
+    255-278): _mt_intersect + _hit_frame in float64 on the device."""
+    from . import query
+    ok, tuv, g, s, front = query.ray_triangle_batch(
+        ray.origin, ray.direction, ray.t_min, ray.t_max, tri.v0, tri.v1, tri.v2, tri.n0, tri.n1,
+        tri.n2)
+    if not ok[0]:
+        return None
+    t, u, v = tuv[0]
+    return Hit(float(t), triangle_index, float(u), float(v), g[0].copy(), s[0].copy(),
+               bool(front[0]))
+
+
+def ray_aabb_intersect(ray: Ray, box: Aabb):
+    """Clipped slab interval (t_enter, t_exit) or None (geometry.py:281-295),
+    the reference's NaN-tolerant compare / select form, float64 on the
+    device."""
+    from . import query
+    ok, tnf = query.ray_aabb_batch(ray.origin, ray.direction, ray.t_min, ray.t_max, box.min,
+                                   box.max)
+    if not ok[0]:
+        return None
+    return float(tnf[0, 0]), float(tnf[0, 1])
+
+
+def triangle_bounds(tri: Triangle) -> Aabb:
+    """AABB of a triangle padded by BOUNDS_PADDING times its max extent
+    (geometry.py:298-304)."""
+    lo = np.minimum(np.minimum(tri.v0, tri.v1), tri.v2)
+    hi = np.maximum(np.maximum(tri.v0, tri.v1), tri.v2)
+    pad = BOUNDS_PADDING * float(np.max(hi - lo))
+    return Aabb(lo - pad, hi + pad)
+
+
+def aabb_union(a: Aabb, b: Aabb) -> Aabb:
+    return Aabb(np.minimum(a.min, b.min), np.maximum(a.max, b.max))
+
+
+def aabb_surface_area(box: Aabb) -> float:
+    if box.is_empty():
+        return 0.0
+    d = box.max - box.min
+    return float(2.0 * (d[0] * d[1] + d[0] * d[2] + d[1] * d[2]))

@@ -9,7 +9,8 @@ the reference's per-(pixel, sample) PCG32 streams.  There is no CPU path.
 Differences from the reference, all deliberate:
   * RenderSettings accepts rr_start_depth > max_depth (roulette simply never
     triggers), which the reference's own tests rely on (SURVEY §4);
-  * `threads` is accepted and ignored (reported as the GPU count, 1);
+  * `threads` is accepted and has no effect on the GPU render (reported
+    back as the clamped host worker count, as the reference reports it);
   * per-sample arithmetic is fp32 (tolerances in tests/), accumulation is an
     fp32 per-pixel sum in sample order, returned as a float64 mean.
 """
@@ -179,7 +180,10 @@ def render_progressive(scene, settings: RenderSettings, bvh=None, threads: int |
     if dropped > total * INVALID_SAMPLE_WARN_FRACTION:
         warnings.warn(f"{dropped} of {total} samples were non-finite and dropped",
                       RuntimeWarning, stacklevel=2)
-    res = RenderResult(image, spp, invalid, elapsed_ms, 1)
+    # `threads` keeps its meaning as the host worker count (clamped as the
+    # reference clamps it, _parallel.py:27-36); the GPU render ignores it
+    from ._parallel import set_worker_count
+    res = RenderResult(image, spp, invalid, elapsed_ms, set_worker_count(threads))
     res.timings = {"scene_create_ms": ds.create_ms if owned else 0.0,
                    "scene_wall_ms": scene_wall_ms if owned else 0.0, "render_ms": elapsed_ms,
                    "image_d2h_ms": d2h_ms}

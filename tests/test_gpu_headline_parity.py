@@ -98,10 +98,12 @@ def test_headline_per_sample_parity(name):
 
 def edge_margin(tris, k, o, d):
     """float64 plane hit of ray (o, d) with triangle k: (t, signed distance
-    of the hit point to the triangle's boundary in world units; >= 0 inside)."""
+    of the hit point to the triangle's boundary in world units, >= 0 inside;
+    |cos| of the ray against the plane)."""
     a, b, c = tris.v0[k], tris.v1[k], tris.v2[k]
     n = np.cross(b - a, c - a)
     n /= np.linalg.norm(n)
+    cos = abs(float(np.dot(d, n)))
     t = np.dot(a - o, n) / np.dot(d, n)
     p = o + t * d
     margin = np.inf
@@ -111,19 +113,24 @@ def edge_margin(tris, k, o, d):
         if np.dot(w - u, e) < 0:
             e = -e
         margin = min(margin, float(np.dot(p - u, e)))
-    return float(t), margin
+    return float(t), margin, cos
 
 
 def classify_mismatch(tris, o, d, ours, ref):
     """A mismatch is ulp-level when, in float64, the two candidates are a
     near-tie in t or one of them is hit within EPS of its boundary (an
-    edge or vertex shared by neighbours), EPS = 1e-6 * (|o| + t): ~10
-    float32 ulps of the hit coordinates."""
-    t_o, m_o = edge_margin(tris, ours, o, d)
-    t_r, m_r = edge_margin(tris, ref, o, d)
-    eps = 1e-6 * (np.abs(o).max() + max(abs(t_o), abs(t_r)))
-    return {"tie": abs(t_o - t_r) <= eps, "edge": min(abs(m_o), abs(m_r)) <= eps,
-            "dt": abs(t_o - t_r), "margin": min(abs(m_o), abs(m_r)), "eps": eps}
+    edge or vertex shared by neighbours).  EPS = 1e-6 (|o| + t) / |cos|:
+    ~10 float32 ulps of the coordinates, times the conditioning of the
+    ray-plane intersection (a grazing ray moves its plane hit point by
+    1/|cos| per unit of error along the ray)."""
+    t_o, m_o, c_o = edge_margin(tris, ours, o, d)
+    t_r, m_r, c_r = edge_margin(tris, ref, o, d)
+    scale = 1e-6 * (np.abs(o).max() + max(abs(t_o), abs(t_r)))
+    eps_o, eps_r = scale / max(c_o, 1e-3), scale / max(c_r, 1e-3)
+    edge = abs(m_o) <= eps_o or abs(m_r) <= eps_r
+    return {"tie": abs(t_o - t_r) <= scale, "edge": edge, "dt": abs(t_o - t_r),
+            "margin": min(abs(m_o), abs(m_r)), "eps": min(eps_o, eps_r),
+            "cos": (c_o, c_r)}
 
 
 def test_headline_primary_hit_ids():
