@@ -574,11 +574,13 @@ static int validate_indices(const lt_scene_desc *d) {
   };
   const int64_t bt = first_bad(n, tri_bad);
   if (bt >= 0) {
-    const int32_t m = d->material_index[bt], o = d->triangle_order[bt];
+    const int32_t m = d->material_index[bt];
     if (m < 0 || m >= d->n_materials)
       return lt_fail(LT_ERR_INVALID, "triangle %lld: material index %d out of range [0, %d)",
                      (long long)bt, m, d->n_materials);
-    return lt_fail(LT_ERR_INVALID, "triangle_order[%lld] = %d out of range", (long long)bt, o);
+    // (only reachable with a host BVH: build_here has no triangle_order)
+    return lt_fail(LT_ERR_INVALID, "triangle_order[%lld] = %d out of range", (long long)bt,
+                   d->triangle_order[bt]);
   }
   const int64_t bn = build_here ? -1 : first_bad(nn, node_bad);
   if (bn >= 0) {
@@ -826,16 +828,23 @@ static int device_layout(lt_scene *s, const double *bmin, const double *bmax,
   RET(t_wch.alloc((size_t)std::max<int64_t>(n_internal, 1) * 16, st));
   RET(t_wof.alloc((size_t)std::max<int64_t>(nn, 1) * 4, st));
   if (root_leaf || n_internal == 0) return LT_OK;
-  // breadth-first 4-wide collapse in one single-CTA launch
+  // breadth-first 4-wide collapse in one single-CTA launch; it also reports
+  // the deepest traversal stack the tree can need
   TmpBuf fifo, nw;
-  RET(fifo.alloc((size_t)n_internal * 4, st));
-  RET(nw.alloc(4, st));
+  RET(fifo.alloc((size_t)n_internal * 12, st));
+  RET(nw.alloc(16, st));
+  int32_t res[3] = {n_internal, 0, 0};
+  CK(cudaMemcpyAsync(nw.p, res, 4, cudaMemcpyHostToDevice, st));
   launch_collapse_all(bmin, bmax, left, right, count, fifo.as<int32_t>(), t_wch.as<int32_t>(),
                       t_wof.as<int32_t>(), nw.as<int32_t>(), st);
-  int32_t n_wide = 0;
-  CK(cudaMemcpyAsync(&n_wide, nw.p, 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(res, nw.p, 12, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
-  s->n_wide = n_wide;
+  s->n_wide = res[0];
+  if (res[1] >= LT_STACK || res[2] >= LT_STACK)
+    return lt_fail(LT_ERR_UNSUPPORTED,
+                   "BVH too deep for the traversal stack: the 4-wide tree can hold %d pending "
+                   "entries and the binary tree is %d levels deep (limit %d)",
+                   res[1], res[2], LT_STACK);
   return LT_OK;
 }
 
@@ -1400,6 +1409,12 @@ static int pixel_set(lt_scene *s, const lt_render_params *p, const int32_t **lis
       const int64_t ty = tile / ntx, tx = tile - ty * ntx;
       tile_start[(size_t)(tile / n_ranks)] = (int32_t)total;
       total += (std::min(W, (tx + 1) * T) - tx * T) * (std::min(H, (ty + 1) * T) - ty * T);
+    }
+    // earlier passes (any stream) may still read the current list: the scene
+    // stream waits for the device's last pass before replacing it
+    {
+      std::lock_guard<std::mutex> lk(s->ws->mu);
+      if (s->ws->last_use) CK(cudaStreamWaitEvent(s->stream, s->ws->last_use, 0));
     }
     RET(s->pix_list.ensure(std::max<size_t>(16, (size_t)total * 4)));
     TmpBuf t_start;

@@ -35,7 +35,12 @@
 #define LT_INV_PI_F 0.318309886183790671538f
 #define LT_DET_EPS_F 1e-9f      // geometry.py:17
 #define LT_RR_MIN_F 0.05f       // integrator.py:34
-#define LT_STACK 64             // bvh.py:27
+// traversal stack entries: a 4-wide visit leaves up to 3 siblings pending
+// per level, so a tree the reference builds (depth cap 60, bvh.py:26) needs
+// up to 3 * 60 + 1; scene creation rejects trees that could need more
+// (k_collapse_all measures it).  Entries past the shared-memory part live in
+// local memory, touched only by the deepest rays.
+#define LT_STACK 192
 #define LT_LINK_EXIT ((int32_t)0x80000000)
 // Wide-node record, in float4 units.  Default: [lo_x, hi_x, lo_y, hi_y,
 // lo_z, hi_z, links, pad] (128 B).  LT_NODE_DUP: every axis stored as

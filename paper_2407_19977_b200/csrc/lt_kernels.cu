@@ -661,10 +661,12 @@ __device__ __forceinline__ int collapse_node(const double *__restrict__ bmin,
                                              const int32_t *__restrict__ left,
                                              const int32_t *__restrict__ right,
                                              const int32_t *__restrict__ count, int32_t r,
-                                             int32_t (&ch)[4]) {
+                                             int32_t (&ch)[4], int (&dep)[4]) {
   ch[0] = left[r];
   ch[1] = right[r];
   ch[2] = ch[3] = -1;
+  dep[0] = dep[1] = 1;  // binary levels below r
+  dep[2] = dep[3] = 0;
   int nc = 2;
   while (nc < 4) {
     int pick = -1;
@@ -679,9 +681,14 @@ __device__ __forceinline__ int collapse_node(const double *__restrict__ bmin,
       }
     if (pick < 0) break;
     const int32_t x = ch[pick];
-    for (int k = nc; k > pick + 1; --k) ch[k] = ch[k - 1];
+    const int dx = dep[pick] + 1;
+    for (int k = nc; k > pick + 1; --k) {
+      ch[k] = ch[k - 1];
+      dep[k] = dep[k - 1];
+    }
     ch[pick] = left[x];
     ch[pick + 1] = right[x];
+    dep[pick] = dep[pick + 1] = dx;
     ++nc;
   }
   int internal = 0;
@@ -692,32 +699,57 @@ __device__ __forceinline__ int collapse_node(const double *__restrict__ bmin,
 // The whole collapse in one CTA: a FIFO of binary roots processed 1024 at a
 // time (wide node id = FIFO position, i.e. breadth-first, the numbering of
 // the level-by-level launches) -- one launch instead of ~4 per level plus a
-// host synchronization per level.
+// host synchronization per level.  Alongside each FIFO entry: its binary
+// depth and the traversal-stack entries pending when a ray reaches it (its
+// ancestors' hit siblings, at most nchildren - 1 per wide level); out[1] =
+// the deepest traversal stack the wide tree can need, out[2] = the binary
+// tree's depth (the counter query's stack), both checked against LT_STACK.
 __global__ void __launch_bounds__(1024)
     k_collapse_all(const double *__restrict__ bmin, const double *__restrict__ bmax,
                    const int32_t *__restrict__ left, const int32_t *__restrict__ right,
                    const int32_t *__restrict__ count, int32_t *__restrict__ fifo,
                    int32_t *__restrict__ wide_children, int32_t *__restrict__ wide_of,
-                   int32_t *__restrict__ n_wide) {
+                   int32_t *__restrict__ out) {
   __shared__ int s_warp[32];
   __shared__ int s_tail;
+  __shared__ int s_stack, s_depth;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // fifo layout: [node ids | binary depth | pending stack entries], capacity
+  // = internal node count, passed as out[0] on entry
+  const int cap = out[0];
+  int32_t *f_dep = fifo + cap, *f_pend = fifo + 2 * (int64_t)cap;
+  __syncthreads();
   if (tid == 0) {
     fifo[0] = 0;  // the root (binary node 0)
+    f_dep[0] = 0;
+    f_pend[0] = 0;
     s_tail = 1;
+    s_stack = 0;
+    s_depth = 0;
   }
   __syncthreads();
   int head = 0;
+  int my_stack = 0, my_depth = 0;
   while (head < s_tail) {
     const int tail = s_tail;
     const int i = head + tid;
     int32_t ch[4] = {-1, -1, -1, -1};
-    int kids = 0;
+    int dep[4] = {0, 0, 0, 0};
+    int kids = 0, depth = 0, pend = 0, nch = 0;
     if (i < tail) {
       const int32_t r = fifo[i];
+      depth = f_dep[i];
+      pend = f_pend[i];
       wide_of[r] = i;
-      kids = collapse_node(bmin, bmax, left, right, count, r, ch);
-      for (int k = 0; k < 4; ++k) wide_children[4 * (int64_t)i + k] = ch[k];
+      kids = collapse_node(bmin, bmax, left, right, count, r, ch, dep);
+      for (int k = 0; k < 4; ++k) {
+        wide_children[4 * (int64_t)i + k] = ch[k];
+        if (ch[k] >= 0) {
+          ++nch;
+          my_depth = max(my_depth, depth + dep[k]);
+        }
+      }
+      my_stack = max(my_stack, pend + nch - 1);
     }
     // block exclusive scan of the internal-children counts
     int x = kids;
@@ -739,14 +771,26 @@ __global__ void __launch_bounds__(1024)
     const int excl = x - kids + (warp ? s_warp[warp - 1] : 0);
     int j = tail + excl;
     for (int k = 0; k < 4; ++k)
-      if (ch[k] >= 0 && count[ch[k]] == 0) fifo[j++] = ch[k];
+      if (ch[k] >= 0 && count[ch[k]] == 0) {
+        fifo[j] = ch[k];
+        f_dep[j] = depth + dep[k];
+        f_pend[j] = pend + nch - 1;
+        ++j;
+      }
     const int total = s_warp[(blockDim.x >> 5) - 1];
     __syncthreads();
     if (tid == 0) s_tail = tail + total;
     head = min(head + (int)blockDim.x, tail);
     __syncthreads();
   }
-  if (tid == 0) *n_wide = s_tail;
+  atomicMax(&s_stack, my_stack);
+  atomicMax(&s_depth, my_depth);
+  __syncthreads();
+  if (tid == 0) {
+    out[0] = s_tail;
+    out[1] = s_stack;
+    out[2] = s_depth;
+  }
 }
 
 

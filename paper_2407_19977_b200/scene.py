@@ -65,8 +65,8 @@ class EnvironmentConfig:
 
     def __post_init__(self) -> None:
         if self.kind not in ("uniform", "gradient", "latlong"):
-            raise SceneError(f"environment type must be 'uniform', 'gradient' or 'latlong', "
-                             f"got {self.kind!r}")
+            raise SceneError(f"environment type must be 'uniform' or 'gradient' (or the "
+                             f"'latlong' extension), got {self.kind!r}")
         for name in ("radiance", "zenith", "horizon"):
             v = np.asarray(getattr(self, name), dtype=np.float64)
             if v.shape != (3,) or np.any(v < 0.0) or not np.all(np.isfinite(v)):

@@ -537,9 +537,79 @@ def test_scene_index_errors_are_reported():
     bad.triangle_order[7] = -2
     with pytest.raises(ValueError, match=r"triangle_order\[7\] = -2"):
         m.DeviceScene(g.scene, bad)
+    # material index out of range with no host BVH (the device builds the
+    # tree; there is no triangle_order to report)
+    tb = g.triangles
+    mi = tb.material_index.copy()
+    mi[11] = 99
+    bad_tris = m.TriangleBuffer(tb.v0, tb.v1, tb.v2, tb.n0, tb.n1, tb.n2, mi)
+    bad_scene = m.SceneDescription(bad_tris, g.materials, g.camera, g.environment, 0)
+    with pytest.raises(ValueError, match="triangle 11: material index 99 out of range"):
+        m.DeviceScene(bad_scene)
+    with pytest.raises(ValueError, match="triangle 11: material index 99"):
+        m.render_progressive(bad_scene, m.RenderSettings(samples_per_pixel=1))
     st = m.RenderSettings(samples_per_pixel=2, max_depth=3, seed=1)
     img = m.render_progressive(device_scene(g), st).image
     assert np.isfinite(img).all()
+
+
+def chain_bvh(n: int):
+    """A caller-supplied, maximally unbalanced tree over n triangles stacked
+    along z: internal node 2k has leaf 2k+1 (triangle k) and internal node
+    2k+2 as children; the last internal node holds two leaves.  Binary depth
+    n - 1; the 4-wide collapse leaves 3 siblings pending per wide level."""
+    m = lb()
+    z = np.arange(n, dtype=np.float64)
+    v0 = np.stack([np.zeros(n), np.zeros(n), z], 1)
+    v1 = np.stack([np.ones(n), np.zeros(n), z], 1)
+    v2 = np.stack([np.zeros(n), np.ones(n), z], 1)
+    nz = np.tile([0.0, 0.0, 1.0], (n, 1))
+    tris = m.TriangleBuffer(v0, v1, v2, nz, nz, nz)
+    nn = 2 * n - 1
+    left = np.full(nn, -1, np.int32)
+    right = np.full(nn, -1, np.int32)
+    first = np.zeros(nn, np.int32)
+    count = np.zeros(nn, np.int32)
+    bmin = np.zeros((nn, 3))
+    bmax = np.zeros((nn, 3))
+    for k in range(n - 1):
+        i = 2 * k
+        left[i], right[i] = i + 1, i + 2
+        first[i + 1], count[i + 1] = k, 1
+        bmin[i] = (0.0, 0.0, k)
+        bmax[i] = (1.0, 1.0, n - 1)
+        bmin[i + 1] = (0.0, 0.0, k)
+        bmax[i + 1] = (1.0, 1.0, k)
+    first[nn - 1], count[nn - 1] = n - 1, 1
+    bmin[nn - 1] = (0.0, 0.0, n - 1)
+    bmax[nn - 1] = (1.0, 1.0, n - 1)
+    bvh = m.Bvh(bmin, bmax, left, right, first, count, np.arange(n, dtype=np.int32),
+                m.BuildStats(nn, n, n - 1, 0.0))
+    assert m.validate_bvh(bvh, tris) == []
+    return tris, bvh
+
+
+def test_deep_trees_traverse_or_are_rejected():
+    """Stack safety: a depth-60 chain (the reference's depth
+    cap) traverses with exact results -- rays down the chain pass every
+    level -- and a chain too deep for the traversal stack is rejected at
+    scene creation instead of overflowing it."""
+    m = lb()
+    tris, bvh = chain_bvh(61)
+    rng = np.random.default_rng(5)
+    o = np.stack([rng.uniform(0.05, 0.3, 256), rng.uniform(0.05, 0.3, 256),
+                  np.full(256, 70.0)], 1)
+    d = np.tile([0.0, 0.0, -1.0], (256, 1))
+    d[128:] = rng.normal(size=(128, 3))
+    d[128:] /= np.linalg.norm(d[128:], axis=1, keepdims=True)
+    o[128:] = rng.uniform(0.0, 1.0, (128, 3)) * [1, 1, 60]
+    idx, t = m.intersect_scene_batch(tris, bvh, o, d)
+    bi, bt = m.brute_force_intersect_batch(tris, o, d)
+    assert np.array_equal(idx, bi) and np.array_equal(t, bt)
+    assert np.all(idx[:128] == 60)
+    deep_tris, deep = chain_bvh(260)
+    with pytest.raises(RuntimeError, match="too deep for the traversal stack"):
+        m.DeviceScene.from_geometry(deep_tris, deep)
 
 
 @pytest.mark.parametrize("name", ["cornell_c1", "sphere20k", "floor"])
