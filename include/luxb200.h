@@ -21,7 +21,7 @@
 extern "C" {
 #endif
 
-#define LT_ABI_VERSION 1
+#define LT_ABI_VERSION 2
 
 /* status codes */
 #define LT_OK 0
@@ -43,7 +43,6 @@ extern "C" {
                                        coat, glass, coat + glass) and the shade kernel
                                        reads it through that permutation; results are
                                        unchanged (off by default) */
-#define LT_FLAG_NO_SMEM_TOP 2u      /* reserved (top-node staging was removed); no effect */
 #define LT_FLAG_PROFILE 4u          /* time every trace launch with CUDA events */
 #define LT_FLAG_COUNT 8u            /* count slab / triangle tests in the trace kernel */
 
@@ -85,7 +84,7 @@ typedef struct lt_scene_desc {
 
 typedef struct lt_scene_info {
   int32_t device;
-  int64_t n_triangles, n_nodes, n_internal, n_smem_nodes;  /* n_smem_nodes: always 0 */
+  int64_t n_triangles, n_nodes, n_internal;
   int64_t device_bytes;         /* resident scene bytes in HBM */
   int32_t sm_count;
   int64_t n_wide;               /* 4-wide nodes of the render layout */

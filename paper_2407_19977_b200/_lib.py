@@ -26,7 +26,6 @@ LT_ENV_GRADIENT = 1
 LT_ENV_LATLONG = 2
 
 LT_FLAG_SORT_MATERIALS = 1
-LT_FLAG_NO_SMEM_TOP = 2
 LT_FLAG_PROFILE = 4
 LT_FLAG_COUNT = 8
 
@@ -67,7 +66,7 @@ class SceneInfo(C.Structure):
     _fields_ = [
         ("device", C.c_int32),
         ("n_triangles", C.c_int64), ("n_nodes", C.c_int64), ("n_internal", C.c_int64),
-        ("n_smem_nodes", C.c_int64), ("device_bytes", C.c_int64),
+        ("device_bytes", C.c_int64),
         ("sm_count", C.c_int32),
         ("n_wide", C.c_int64), ("l2_persist_bytes", C.c_int64), ("l2_window_bytes", C.c_int64),
         ("default_batch_paths", C.c_int64),
@@ -176,7 +175,7 @@ def lib():
         fn = getattr(handle, name)
         fn.restype = res
         fn.argtypes = args
-    if handle.lt_abi_version() != 1:
+    if handle.lt_abi_version() != 2:
         raise NativeLibraryMissing("libluxb200.so ABI version mismatch")
     _lib = handle
     return _lib

@@ -442,7 +442,6 @@ struct lt_scene {
   // launch configuration
   int trace_grid[2] = {0, 0};  // [no smem, smem]
   int shade_grid = 0;
-  int smem_nodes = 0;
   int64_t default_batch = int64_t(1) << 22;
   int n_lanes = kLanes;
   bool octant_sort = false;
@@ -721,7 +720,6 @@ struct LaunchCache {
 };
 
 static int configure_launches(lt_scene *s) {
-  s->smem_nodes = 0;  // (top-level shared-memory staging measured slower; removed)
   static std::mutex mu;
   static std::map<int, LaunchCache> cache;
   LaunchCache lc;
@@ -1189,7 +1187,6 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
   pt.mark("free temporaries + view");
   RET(configure_launches(s));
   pt.mark("configure launches");
-  v.n_top = s->smem_nodes;
   // continuation rays appended grouped by direction octant (+3 % on C4,
   // profiles/r01_octant_sweep.jsonl); LT_OCTANT_SORT=0 disables
   const char *os_env = std::getenv("LT_OCTANT_SORT");
@@ -1238,7 +1235,6 @@ extern "C" int lt_scene_info_get(const lt_scene *s, lt_scene_info *info) {
   info->n_triangles = s->n_tris;
   info->n_nodes = s->n_nodes;
   info->n_internal = s->n_internal;
-  info->n_smem_nodes = s->smem_nodes;
   info->device_bytes = s->device_bytes;
   info->sm_count = s->sm_count;
   info->n_wide = s->n_wide;

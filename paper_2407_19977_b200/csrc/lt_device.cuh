@@ -4,7 +4,7 @@
 //   wnodes : LT_NODE_F4 x float4 per node of the host BVH collapsed to
 //            4-wide (each wide node absorbs the largest-area internal
 //            children of its binary node until it has 4 children); default
-//            (LT_NODE_DUP, 224 B): per axis a = x, y, z the float4s
+//            (224 B): per axis a = x, y, z the float4s
 //            [4a .. 4a+3] = lo[4], hi[4], hi[4], lo[4] (the (near, far) pair
 //            for a positive / negative inverse direction), f4[12] = 4 child
 //            links (>= 0 wide node, < 0 leaf = ~first, INT_MIN empty slot),
@@ -42,37 +42,15 @@
 // local memory, touched only by the deepest rays.
 #define LT_STACK 192
 #define LT_LINK_EXIT ((int32_t)0x80000000)
-// Wide-node record, in float4 units.  Default: [lo_x, hi_x, lo_y, hi_y,
-// lo_z, hi_z, links, pad] (128 B).  LT_NODE_DUP: every axis stored as
+// Wide-node record, in float4 units (224 B): every axis stored as
 // [lo, hi, hi, lo] so the ray's direction octant selects a 32 B-aligned
-// (near, far) pair that one 256-bit load fetches (224 B; the default:
-// +4.5 % on C4, profiles/r01_trace_variants.txt; -DLT_NODE_COMPACT selects
-// the 128 B record).
+// (near, far) pair that one 256-bit load fetches (+4.5 % on C4 over the
+// 128 B [lo, hi] record, profiles/r01_trace_variants.txt); f4[12] = links.
 // Leaf-ordered triangle record in float4 units: (v0, orig), (e1, leaf-end),
-// (e2, 0) = 48 B; LT_TRI_W256 pads it to 64 B so (v0, e1) is one 256-bit load.
-#ifdef LT_TRI_W256
-#define LT_TRI_F4 4
-#else
+// (e2, 0) = 48 B.
 #define LT_TRI_F4 3
-#endif
-#if !defined(LT_NODE_COMPACT) && !defined(LT_NODE_DUP)
-#define LT_NODE_DUP 1
-#endif
-#ifdef LT_NODE_DUP
 #define LT_NODE_F4 14
 #define LT_NODE_LINKS 12
-#ifndef LT_W256
-#define LT_W256 1
-#endif
-#else
-#define LT_NODE_F4 8
-#define LT_NODE_LINKS 6
-#endif
-// Slab arithmetic: packed fp32 pairs (FADD2 / FMUL2, two children per
-// issue slot; +3.5 % on C4) unless -DLT_SCALAR_SLAB.
-#if !defined(LT_SCALAR_SLAB) && !defined(LT_PACKED_SLAB)
-#define LT_PACKED_SLAB 1
-#endif
 // robustness: child exit distances are widened by 1 + 2*gamma(3) so fp32
 // rounding in the slab test never culls a box the float64 reference keeps
 #define LT_SLAB_WIDEN 1.0000004f
@@ -107,7 +85,6 @@ struct SceneView {
   const GpuMaterial *__restrict__ mats;
   const float4 *__restrict__ env_map;  // (h, w) RGB + pad
   int32_t root_link;
-  int32_t n_top;        // internal nodes [0, n_top) are BFS-ordered top levels
   int32_t refill_min;   // idle lanes that trigger a warp refill in k_trace
   int32_t leaf_min;     // lanes at a leaf that trigger the warp's leaf tests
   float root_lo[3], root_hi[3];

@@ -81,19 +81,14 @@ __global__ void k_flatten_wide(const double *__restrict__ bmin, const double *__
   for (int a = 0; a < 3; ++a) {
     const float4 l4 = make_float4(lo[a][0], lo[a][1], lo[a][2], lo[a][3]);
     const float4 h4 = make_float4(hi[a][0], hi[a][1], hi[a][2], hi[a][3]);
-#ifdef LT_NODE_DUP
     o[4 * a] = l4;      // (near, far) for a positive inverse direction
     o[4 * a + 1] = h4;
     o[4 * a + 2] = h4;  // (near, far) for a negative one
     o[4 * a + 3] = l4;
-#else
-    o[2 * a] = l4;
-    o[2 * a + 1] = h4;
-#endif
   }
   o[LT_NODE_LINKS] = make_float4(__int_as_float(link[0]), __int_as_float(link[1]),
                                  __int_as_float(link[2]), __int_as_float(link[3]));
-  if (LT_NODE_LINKS + 1 < LT_NODE_F4) o[LT_NODE_LINKS + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
+  o[LT_NODE_LINKS + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
 }
 
 // End-of-leaf flags of the leaf-ordered triangle stream.
@@ -123,7 +118,6 @@ __global__ void k_flatten_tris(const double *__restrict__ v0, const double *__re
   tr[1] = make_float4((float)(b[0] - a[0]), (float)(b[1] - a[1]), (float)(b[2] - a[2]),
                                 __int_as_float(leaf_end[k] ? 1 : 0));
   tr[2] = make_float4((float)(c[0] - a[0]), (float)(c[1] - a[1]), (float)(c[2] - a[2]), 0.f);
-  if (LT_TRI_F4 > 3) tr[3] = make_float4(0.f, 0.f, 0.f, 0.f);
   // geometric normal as _hit_frame computes it (geometry.py:217-224), float64
   const double e1x = b[0] - a[0], e1y = b[1] - a[1], e1z = b[2] - a[2];
   const double e2x = c[0] - a[0], e2y = c[1] - a[1], e2z = c[2] - a[2];
@@ -331,7 +325,7 @@ __global__ void __launch_bounds__(kTraceThreads, LT_TRACE_MIN_BLOCKS)
     // hit children go on the stack farthest first
 #pragma unroll 1
     for (int step = 0; step < LT_NODE_STEPS && q >= 0 && node >= 0; ++step) {
-      const Hits4 h = LT_VISIT4(sc.wnodes + LT_NODE_F4 * (int64_t)node, rs, t_min, best.t);
+      const Hits4 h = visit4o(sc.wnodes + LT_NODE_F4 * (int64_t)node, rs, t_min, best.t);
       if (COUNT) nn += 4;
       if (sp <= kShortStack - 3) {
         // common case: all three fit in shared memory (predicated stores)
@@ -400,27 +394,11 @@ __global__ void __launch_bounds__(kTraceThreads)
 
 // ------------------------------------------------------------------ shade
 
-// Direction bin of a continuation ray for the block-level grouping:
-// LT_DIR_BINS = 8: octant; 24: octant x dominant axis; 64: 4 levels per
-// component (x-major).
-#ifndef LT_DIR_BINS
+// Direction octant of a continuation ray (the block-level grouping of the
+// append; 24 / 64 finer bins measured +-0 / -1 %, profiles/r01_v12 sweeps).
 #define LT_DIR_BINS 8
-#endif
 __device__ __forceinline__ int dir_bin(const float4 &d) {
-#if LT_DIR_BINS == 64
-  const int qx = min(3, (int)((d.x + 1.f) * 2.f)), qy = min(3, (int)((d.y + 1.f) * 2.f));
-  const int qz = min(3, (int)((d.z + 1.f) * 2.f));
-  return (max(qx, 0) << 4) | (max(qy, 0) << 2) | max(qz, 0);
-#else
-  const int oct = (d.x < 0.f ? 1 : 0) | (d.y < 0.f ? 2 : 0) | (d.z < 0.f ? 4 : 0);
-#if LT_DIR_BINS == 24
-  const float ax = fabsf(d.x), ay = fabsf(d.y), az = fabsf(d.z);
-  const int dom = (ax >= ay && ax >= az) ? 0 : (ay >= az ? 1 : 2);
-  return oct * 3 + dom;
-#else
-  return oct;
-#endif
-#endif
+  return (d.x < 0.f ? 1 : 0) | (d.y < 0.f ? 2 : 0) | (d.z < 0.f ? 4 : 0);
 }
 
 // One bounce of _trace (integrator.py:160-226) for every queued path:

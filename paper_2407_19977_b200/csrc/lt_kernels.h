@@ -29,12 +29,6 @@ constexpr int kShadeThreads = LT_SHADE_THREADS;
 #ifndef LT_SHADE_MIN_BLOCKS
 #define LT_SHADE_MIN_BLOCKS 8
 #endif
-// near/far plane arrays picked by the ray's direction signs (no per-axis
-// min/max in the slab test; profiles/r01_trace_variants.jsonl); build with
-// -DLT_MINMAX_SLAB for the symmetric min/max form
-#if !defined(LT_MINMAX_SLAB) && !defined(LT_OCTANT_SLAB)
-#define LT_OCTANT_SLAB 1
-#endif
 constexpr int kShortStack = LT_SHORT_STACK;  // per-lane traversal stack entries in shared memory
 
 struct PathArrays {

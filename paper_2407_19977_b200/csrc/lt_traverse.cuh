@@ -45,11 +45,9 @@ __device__ __forceinline__ float fmax3f(float a, float b, float c) {
 }
 
 // Per-ray constants of the slab test: `inv` is the clamped inverse
-// direction; `nx/ny/nz` index the wide node's near-plane array per axis in
-// float4 units (lo when the clamped inverse is positive, hi when negative).
-// Default record [lo_x, hi_x, lo_y, hi_y, lo_z, hi_z, links, pad]: near at
-// 2a + sign, far = near ^ 1.  LT_NODE_DUP record [lo_x, hi_x, hi_x, lo_x,
-// ..., links]: the (near, far) pair starts at 4a + 2 sign.
+// direction; `nx/ny/nz` index the wide node's (near, far) plane pair per
+// axis in float4 units: the record stores [lo, hi, hi, lo] per axis a, and
+// the pair starts at 4a + 2 sign(inv_a).
 struct RaySlab {
   f3 o, inv;
   int nx, ny, nz;
@@ -61,18 +59,9 @@ __device__ __forceinline__ RaySlab ray_slab(f3 o, f3 d) {
   r.inv = f3{fminf(fmaxf(1.f / d.x, -LT_INV_CLAMP), LT_INV_CLAMP),
              fminf(fmaxf(1.f / d.y, -LT_INV_CLAMP), LT_INV_CLAMP),
              fminf(fmaxf(1.f / d.z, -LT_INV_CLAMP), LT_INV_CLAMP)};
-  const int sx = (int)(__float_as_uint(r.inv.x) >> 31);
-  const int sy = (int)(__float_as_uint(r.inv.y) >> 31);
-  const int sz = (int)(__float_as_uint(r.inv.z) >> 31);
-#ifdef LT_NODE_DUP
-  r.nx = 2 * sx;
-  r.ny = 4 + 2 * sy;
-  r.nz = 8 + 2 * sz;
-#else
-  r.nx = sx;
-  r.ny = 2 + sy;
-  r.nz = 4 + sz;
-#endif
+  r.nx = 2 * (int)(__float_as_uint(r.inv.x) >> 31);
+  r.ny = 4 + 2 * (int)(__float_as_uint(r.inv.y) >> 31);
+  r.nz = 8 + 2 * (int)(__float_as_uint(r.inv.z) >> 31);
   return r;
 }
 
@@ -94,14 +83,9 @@ __device__ __forceinline__ bool slab(const RaySlab &r, float lox, float hix, flo
 // wavefronts against 1 per 16 B access (tools/micro/ldg256.cu: 1.47x the
 // record rate of 16 B loads on random 128 B records).
 __device__ __forceinline__ void ldg_pair(const float4 *__restrict__ p, float4 &a, float4 &b) {
-#ifdef LT_W256
   asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
       : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
       : "l"(p));
-#else
-  a = __ldg(p);
-  b = __ldg(p + 1);
-#endif
 }
 
 // _mt_intersect (geometry.py:138-167) against the leaf-ordered record
@@ -139,16 +123,8 @@ template <bool COUNT>
 __device__ __forceinline__ void leaf_test(const SceneView &sc, uint32_t k, f3 o, f3 d, float t_min,
                                           HitRec &best, int32_t &best_orig, int &tests) {
   while (true) {
-#ifdef LT_TRI_W256
-    float4 t0, t1;
-    asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-        : "=f"(t0.x), "=f"(t0.y), "=f"(t0.z), "=f"(t0.w), "=f"(t1.x), "=f"(t1.y), "=f"(t1.z),
-          "=f"(t1.w)
-        : "l"(sc.tris + LT_TRI_F4 * (size_t)k));
-#else
     const float4 t0 = __ldg(&sc.tris[LT_TRI_F4 * (size_t)k]);
     const float4 t1 = __ldg(&sc.tris[LT_TRI_F4 * (size_t)k + 1]);
-#endif
     const float4 t2 = __ldg(&sc.tris[LT_TRI_F4 * (size_t)k + 2]);
     if (COUNT) ++tests;
     mt_test(o, d, t_min, t0, t1, t2, (int32_t)k, best, best_orig);
@@ -167,55 +143,20 @@ __device__ __forceinline__ void cswap(float &ka, int32_t &la, float &kb, int32_t
   la = tl;
 }
 
-// One BVH4 node visit: test the four child boxes against [t_min, best_t],
-// sort the hits by entry distance (5-comparator network) and return them
-// nearest first in (l0..l3) with +inf keys for misses / empty slots.
+// One BVH4 node visit: the four child boxes against [t_min, best_t], the
+// hits sorted by entry distance (5-comparator network), returned nearest
+// first in (l0..l3) with +inf keys for misses / empty slots.
 struct Hits4 {
   float k0, k1, k2, k3;
   int32_t l0, l1, l2, l3;
 };
 
-__device__ __forceinline__ Hits4 visit4(const float4 *__restrict__ np, const RaySlab &rs, float t_min,
-                                        float t_max) {
-  const float kInf = __int_as_float(0x7f800000);
-  float4 lx, hx, ly, hy, lz, hz;
-  ldg_pair(np + 0, lx, hx);
-  ldg_pair(np + 2, ly, hy);
-  ldg_pair(np + 4, lz, hz);
-  const int4 ln = __ldg(reinterpret_cast<const int4 *>(np + LT_NODE_LINKS));
-  Hits4 h;
-  float t;
-  h.k0 = slab(rs, lx.x, hx.x, ly.x, hy.x, lz.x, hz.x, t_min, t_max, t) && ln.x != LT_LINK_EXIT
-             ? t : kInf;
-  h.k1 = slab(rs, lx.y, hx.y, ly.y, hy.y, lz.y, hz.y, t_min, t_max, t) && ln.y != LT_LINK_EXIT
-             ? t : kInf;
-  h.k2 = slab(rs, lx.z, hx.z, ly.z, hy.z, lz.z, hz.z, t_min, t_max, t) && ln.z != LT_LINK_EXIT
-             ? t : kInf;
-  h.k3 = slab(rs, lx.w, hx.w, ly.w, hy.w, lz.w, hz.w, t_min, t_max, t) && ln.w != LT_LINK_EXIT
-             ? t : kInf;
-  h.l0 = ln.x;
-  h.l1 = ln.y;
-  h.l2 = ln.z;
-  h.l3 = ln.w;
-  cswap(h.k0, h.l0, h.k1, h.l1);
-  cswap(h.k2, h.l2, h.k3, h.l3);
-  cswap(h.k0, h.l0, h.k2, h.l2);
-  cswap(h.k1, h.l1, h.k3, h.l3);
-  cswap(h.k1, h.l1, h.k2, h.l2);
-  return h;
-}
-
-// Octant form of visit4 (LT_OCTANT_SLAB): the ray's direction signs pick the
-// near and far plane arrays, so each child needs no per-axis min/max; for a
-// box with lo <= hi, (lo - o) * inv and (hi - o) * inv are ordered by the
-// sign of inv (rounding is monotonic), so the entry / exit distances equal
-// the min/max form's exactly.  Empty slots hold inverted infinite boxes and
-// miss without a link check.
-__device__ __forceinline__ float near_far(float n, float f, float o, float inv, float &tf) {
-  tf = (f - o) * inv;
-  return (n - o) * inv;
-}
-
+// The ray's direction signs pick the near and far plane arrays, so each
+// child needs no per-axis min/max: for a box with lo <= hi, (lo - o) * inv
+// and (hi - o) * inv are ordered by the sign of inv (rounding is
+// monotonic), so the entry / exit distances equal the min/max form's
+// exactly.  Empty slots hold inverted infinite boxes and miss without a
+// link check.
 // (p0 - o) * inv and (p1 - o) * inv as one FADD2 + one FMUL2.
 __device__ __forceinline__ void plane2(float p0, float p1, float o, float inv, float &t0,
                                        float &t1) {
@@ -245,21 +186,11 @@ __device__ __forceinline__ Hits4 visit4o(const float4 *__restrict__ np, const Ra
                                          float t_min, float t_max) {
   const float kInf = __int_as_float(0x7f800000);
   float4 nx, fx, ny, fy, nz, fz;
-#ifdef LT_NODE_DUP
   ldg_pair(np + rs.nx, nx, fx);
   ldg_pair(np + rs.ny, ny, fy);
   ldg_pair(np + rs.nz, nz, fz);
-#else
-  nx = __ldg(np + rs.nx);
-  fx = __ldg(np + (rs.nx ^ 1));
-  ny = __ldg(np + rs.ny);
-  fy = __ldg(np + (rs.ny ^ 1));
-  nz = __ldg(np + rs.nz);
-  fz = __ldg(np + (rs.nz ^ 1));
-#endif
   const int4 ln = __ldg(reinterpret_cast<const int4 *>(np + LT_NODE_LINKS));
   Hits4 h;
-#ifdef LT_PACKED_SLAB
   // sm_100 packed fp32 (FADD2 / FMUL2, one issue slot per two children;
   // the scalar origin / inverse are broadcast operands): same IEEE roundings
   // as the scalar form.
@@ -291,48 +222,17 @@ __device__ __forceinline__ Hits4 visit4o(const float4 *__restrict__ np, const Ra
   h.k1 = tn1 <= tf1 ? tn1 : kInf;
   h.k2 = tn2 <= tf2 ? tn2 : kInf;
   h.k3 = tn3 <= tf3 ? tn3 : kInf;
-#else
-#define LT_CHILD(K, C)                                                            \
-  {                                                                               \
-    float fx_, fy_, fz_;                                                          \
-    const float ax = near_far(nx.C, fx.C, rs.o.x, rs.inv.x, fx_);                 \
-    const float ay = near_far(ny.C, fy.C, rs.o.y, rs.inv.y, fy_);                 \
-    const float az = near_far(nz.C, fz.C, rs.o.z, rs.inv.z, fz_);                 \
-    const float tn = fmax3f(ax, ay, fmaxf(az, t_min));                            \
-    const float tf = fmin3f(fx_, fy_, fminf(fz_, t_max));                         \
-    h.K = tn <= tf * LT_SLAB_WIDEN ? tn : kInf;                                   \
-  }
-  LT_CHILD(k0, x)
-  LT_CHILD(k1, y)
-  LT_CHILD(k2, z)
-  LT_CHILD(k3, w)
-#undef LT_CHILD
-#endif
   h.l0 = ln.x;
   h.l1 = ln.y;
   h.l2 = ln.z;
   h.l3 = ln.w;
-#ifdef LT_PARTIAL_SORT
-  // nearest first; the other three only partially ordered (one comparator less)
-  cswap(h.k0, h.l0, h.k1, h.l1);
-  cswap(h.k2, h.l2, h.k3, h.l3);
-  cswap(h.k0, h.l0, h.k2, h.l2);
-  cswap(h.k1, h.l1, h.k2, h.l2);
-#else
   cswap(h.k0, h.l0, h.k1, h.l1);
   cswap(h.k2, h.l2, h.k3, h.l3);
   cswap(h.k0, h.l0, h.k2, h.l2);
   cswap(h.k1, h.l1, h.k3, h.l3);
   cswap(h.k1, h.l1, h.k2, h.l2);
-#endif
   return h;
 }
-
-#if defined(LT_OCTANT_SLAB) || defined(LT_NODE_DUP)
-#define LT_VISIT4 visit4o
-#else
-#define LT_VISIT4 visit4
-#endif
 
 // Pop-time cull distance for the current best t: a stacked entry whose entry
 // distance exceeds it cannot hold a closer hit (bvh.py:389), with the same
@@ -356,7 +256,7 @@ __device__ __forceinline__ bool occluded(const SceneView &sc, f3 o, f3 d, float 
   int32_t best_orig = 0x7fffffff;
   while (true) {
     while (node >= 0) {
-      const Hits4 h = LT_VISIT4(sc.wnodes + LT_NODE_F4 * (int64_t)node, rs, t_min, t_max);
+      const Hits4 h = visit4o(sc.wnodes + LT_NODE_F4 * (int64_t)node, rs, t_min, t_max);
       if (h.k3 < kInf) stk[sp++] = h.l3;
       if (h.k2 < kInf) stk[sp++] = h.l2;
       if (h.k1 < kInf) stk[sp++] = h.l1;
@@ -393,7 +293,7 @@ __device__ __forceinline__ HitRec traverse(const SceneView &sc, f3 o, f3 d, floa
     while (true) {
       while (node >= 0) {
         if (WIDE) {
-          const Hits4 h = LT_VISIT4(sc.wnodes + LT_NODE_F4 * (int64_t)node, rs, t_min, best.t);
+          const Hits4 h = visit4o(sc.wnodes + LT_NODE_F4 * (int64_t)node, rs, t_min, best.t);
           if (COUNT) nodes += 4;
           if (h.k3 < kInf) { stk_node[sp] = h.l3; stk_t[sp] = h.k3; ++sp; }
           if (h.k2 < kInf) { stk_node[sp] = h.l2; stk_t[sp] = h.k2; ++sp; }

@@ -30,7 +30,7 @@ def test_library_builds_and_exports_all_symbols():
     missing = [s for s in syms if not hasattr(handle, s)]
     assert missing == []
     assert set(syms) == set(_lib.SIGNATURES)
-    assert _lib.lib().lt_abi_version() == 1
+    assert _lib.lib().lt_abi_version() == 2
 
 
 def test_struct_layouts_match_header(tmp_path):

@@ -261,8 +261,6 @@ def test_chunking_batching_and_sharding_are_bit_identical():
         assert np.array_equal(total.mean().cpu().numpy(), plain)
     again = m.render_progressive(ds, st).image
     assert np.array_equal(plain, again)
-    nosmem = m.render_progressive(ds, st, flags=2).image
-    assert np.array_equal(plain, nosmem)
 
 
 @pytest.mark.parametrize("knobs", [{"LT_LEAF_MIN": "1"}, {"LT_LEAF_MIN": "33"},
