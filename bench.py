@@ -50,6 +50,10 @@ def parse_args():
     p.add_argument("--rr-start", type=int, default=3)
     p.add_argument("--seed", type=int, default=0)
     p.add_argument("--tile", type=int, default=16)
+    p.add_argument("--mode", choices=["tiles", "spp"], default="tiles",
+                   help="multi-GPU split: interleaved tiles or contiguous sample ranges")
+    p.add_argument("--config", choices=["c4", "c5"], default="c4",
+                   help="c5 = BASELINE configs[4]: 3840x2160, 1024 spp, spp split")
     p.add_argument("--flags", type=int, default=0)
     p.add_argument("--bvh-bins", type=int, default=12,
                    help="SAH bins of the scene BVH (12 = the reference's build_bvh)")
@@ -63,7 +67,10 @@ def parse_args():
                    help="skip the reference-lobe variant measurement")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--ref-step-seconds", type=float, default=6.0)
-    return p.parse_args()
+    a = p.parse_args()
+    if a.config == "c5":
+        a.width, a.height, a.spp, a.mode = 3840, 2160, 1024, "spp"
+    return a
 
 
 def workload_config(args, n_tris: int, world: int) -> dict:
@@ -81,7 +88,8 @@ def workload_config(args, n_tris: int, world: int) -> dict:
         "scene": args.workload, "triangles": n_tris, "width": args.width,
         "height": args.height, "spp": args.spp, "max_depth": args.depth,
         "rr_start_depth": args.rr_start, "seed": args.seed,
-        "parallelism": f"tiles{args.tile}x{world}" if world > 1 else "single",
+        "parallelism": ((f"tiles{args.tile}x{world}" if args.mode == "tiles" else f"spp/{world}")
+                        if world > 1 else "single"),
         "l2": "no explicit flush: every step streams ~8 GB of wavefront queues and path "
               "state through L2 (126 MB); the hot part of the traversal set stays L2-resident "
               "through ordinary caching, as in any steady-state render",
@@ -314,7 +322,8 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     from paper_2407_19977_b200 import RenderSettings, build_bvh, render_progressive
     from paper_2407_19977_b200._lib import LT_FLAG_COUNT, LT_FLAG_PROFILE, read_bandwidth
     from paper_2407_19977_b200.device import DeviceScene
-    from paper_2407_19977_b200.distributed import merge_tiles, render_distributed
+    from paper_2407_19977_b200.distributed import (merge_spp_ordered, merge_tiles,
+                                                   render_distributed, spp_range)
     from paper_2407_19977_b200.integrator import Accumulator, render_pass_device
 
     torch.cuda.set_device(local_rank)
@@ -324,7 +333,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
                               rr_start_depth=args.rr_start, seed=args.seed)
     l2_gbs = read_bandwidth(local_rank, 32 << 20, 10)      # 32 MB: L2-resident
     hbm_probe = read_bandwidth(local_rank, 4 << 30, 5)      # 4 GB: HBM
-    shard = (rank, world, args.tile) if world > 1 else None
+    shard = (rank, world, args.tile) if world > 1 and args.mode == "tiles" else None
     stream = torch.cuda.current_stream(dev)
     samples_per_step = args.width * args.height * args.spp
 
@@ -349,9 +358,17 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
             acc_.sum.zero_()
             acc_.valid.zero_()
             acc_.invalid.zero_()
-            render_pass_device(ds_, ds_.camera, settings, acc_, 0, spp or args.spp,
-                               flags=flags | args.flags, shard=shard,
-                               max_batch_paths=args.batch_paths, stream=stream)
+            n = spp or args.spp
+            if args.mode == "spp":
+                lo, hi = spp_range(n, rank, world)
+                render_pass_device(ds_, ds_.camera, settings, acc_, lo, hi - lo,
+                                   flags=flags | args.flags, max_batch_paths=args.batch_paths,
+                                   stream=stream)
+                if world > 1:
+                    merge_spp_ordered(acc_, dst=0)
+                return
+            render_pass_device(ds_, ds_.camera, settings, acc_, 0, n, flags=flags | args.flags,
+                               shard=shard, max_batch_paths=args.batch_paths, stream=stream)
             if world > 1:
                 merge_tiles(acc_, dst=0)
         return step
@@ -384,7 +401,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         def call():
             if world > 1:
                 return render_distributed(scene_, settings, bvh_, tile_size=args.tile,
-                                          device=local_rank)
+                                          mode=args.mode, device=local_rank)
             return render_progressive(scene_, settings, bvh=bvh_, device=local_rank)
         call()
         torch.cuda.synchronize(dev)

@@ -38,43 +38,83 @@ def spp_range(spp: int, rank: int, world: int) -> tuple[int, int]:
     return lo, hi
 
 
-def merge_tiles(acc, group=None, dst: int | None = 0) -> None:
-    """Sum the zero-padded per-rank accumulators (tile sharding: exact).
-    dst=None all-reduces; otherwise reduces onto rank dst.  Works for NCCL
-    (CUDA tensors) and gloo (CPU tensors)."""
+def _global_rank(group, rank: int) -> int:
     import torch.distributed as dist
-    host_staged = dist.get_backend(group) == "gloo"   # gloo: reduce host copies
-    for t in (acc.sum, acc.valid, acc.invalid):
-        x = t.cpu() if (host_staged and t.is_cuda) else t
-        if dst is None:
-            dist.all_reduce(x, op=dist.ReduceOp.SUM, group=group)
-        else:
-            dist.reduce(x, dst=dst, op=dist.ReduceOp.SUM, group=group)
-        if x is not t:
-            t.copy_(x)
+    return rank if group is None else dist.get_global_rank(group, rank)
 
 
-def merge_spp_ordered(acc, group=None) -> None:
-    """spp splitting: all-gather the partial sums and add them in rank order
-    on every rank (fixed fp32 order => identical result on every run)."""
+def _packed(acc):
+    """One int32 buffer [sum as float32 bits (3n) | valid (n) | invalid (n)]
+    on the accumulator's device, so a merge is one collective."""
+    import torch
+    return torch.cat([acc.sum.view(torch.int32), acc.valid, acc.invalid])
+
+
+def _unpack_into(acc, buf) -> None:
+    import torch
+    n3 = acc.sum.numel()
+    n = acc.valid.numel()
+    acc.sum.copy_(buf[:n3].view(torch.float32))
+    acc.valid.copy_(buf[n3:n3 + n])
+    acc.invalid.copy_(buf[n3 + n:])
+
+
+def merge_tiles(acc, group=None, dst: int | None = 0) -> None:
+    """Merge the per-rank accumulators of a tile-sharded render: every
+    element is non-zero on at most one rank (its pixel's tile owner; x + 0 =
+    x), so an integer SUM of the packed buffers -- float32 bit patterns plus
+    counts -- is exact.  One reduce onto group rank `dst` (its global rank
+    is looked up), or one all-reduce with dst=None.  NCCL reduces CUDA
+    tensors; gloo stages through host memory."""
+    import torch.distributed as dist
+    host_staged = dist.get_backend(group) == "gloo"
+    buf = _packed(acc)
+    x = buf.cpu() if (host_staged and buf.is_cuda) else buf
+    if dst is None:
+        dist.all_reduce(x, op=dist.ReduceOp.SUM, group=group)
+    else:
+        dist.reduce(x, dst=_global_rank(group, dst), op=dist.ReduceOp.SUM, group=group)
+    if dst is None or dist.get_rank(group) == dst:
+        _unpack_into(acc, x.to(acc.sum.device))
+
+
+def merge_spp_ordered(acc, group=None, dst: int | None = 0) -> None:
+    """Merge the partial accumulators of an spp-split render: gather the
+    packed partials onto group rank `dst` and add them there in rank order
+    (a fixed fp32 order => the same result on every run and for any
+    placement of ranks); dst=None broadcasts the sum back to every rank."""
     import torch
     import torch.distributed as dist
     world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
     host_staged = dist.get_backend(group) == "gloo"
-    for t in (acc.sum, acc.valid, acc.invalid):
-        x = t.cpu() if (host_staged and t.is_cuda) else t
-        parts = [torch.empty_like(x) for _ in range(world)]
-        dist.all_gather(parts, x, group=group)
+    root = 0 if dst is None else dst
+    buf = _packed(acc)
+    x = buf.cpu() if (host_staged and buf.is_cuda) else buf
+    parts = [torch.empty_like(x) for _ in range(world)] if rank == root else None
+    dist.gather(x, gather_list=parts, dst=_global_rank(group, root), group=group)
+    n3 = acc.sum.numel()
+    if rank == root:
         total = parts[0].clone()
+        tf = total[:n3].view(torch.float32)
         for p in parts[1:]:
-            total += p
-        t.copy_(total)
+            tf += p[:n3].view(torch.float32)
+            total[n3:] += p[n3:]
+        x = total
+    if dst is None:
+        dist.broadcast(x, src=_global_rank(group, root), group=group)
+    if dst is None or rank == root:
+        _unpack_into(acc, x.to(acc.sum.device))
 
 
 def render_distributed(scene, settings, bvh=None, *, tile_size: int = 16, mode: str = "tiles",
                        device: int | None = None, flags: int = 0, group=None):
-    """render_progressive across all ranks of the default process group.
-    Returns the RenderResult on rank 0 and None elsewhere."""
+    """render_progressive across all ranks of `group` (default: the world):
+    mode "tiles" (interleaved tiles, bit-identical to one GPU) or "spp"
+    (contiguous sample ranges, for small frames / huge spp: C5).  Pass a
+    DeviceScene to keep the scene resident across calls; a scene
+    description is uploaded by every call, as render_progressive does.
+    Returns the RenderResult on group rank 0 and None elsewhere."""
     import time
 
     import torch

@@ -123,3 +123,41 @@ def test_spp_merge_is_deterministic_gloo():
     single = _partial(0, 1, "spp", 4, 32, 24)
     assert np.array_equal(a[1], single.valid.numpy())
     assert np.allclose(a[0], single.sum.numpy(), rtol=1e-6, atol=1e-6)
+
+
+def _subgroup_worker(rank, world, port, out):
+    """World of 3; ranks {1, 2} form a group that renders the frame as a
+    2-way tile split and merges onto the GROUP's rank 0 (= global rank 1)."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2407_19977_b200.distributed import merge_spp_ordered, merge_tiles
+    group = dist.new_group([1, 2])
+    if rank in (1, 2):
+        g_rank = dist.get_rank(group)
+        acc = _partial(g_rank, 2, "tiles", 3, 32, 24)
+        merge_tiles(acc, group, dst=0)
+        if rank == 1:
+            out.put(("tiles", acc.sum.numpy().copy(), acc.valid.numpy().copy()))
+        acc2 = _partial(g_rank, 2, "spp", 3, 32, 24)
+        merge_spp_ordered(acc2, group, dst=None)   # every group rank gets the sum
+        out.put((f"spp{rank}", acc2.sum.numpy().copy(), acc2.valid.numpy().copy()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_merges_on_a_subgroup_gloo():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_subgroup_worker, args=(r, 3, port, q)) for r in range(3)]
+    for p in procs:
+        p.start()
+    got = dict((k, (s, v)) for k, s, v in (q.get(timeout=120) for _ in range(3)))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    single = _partial(0, 1, "tiles", 3, 32, 24)
+    assert np.array_equal(got["tiles"][0], single.sum.numpy())
+    assert np.array_equal(got["tiles"][1], single.valid.numpy())
+    assert np.array_equal(got["spp1"][0], got["spp2"][0])
+    assert np.array_equal(got["spp1"][1], single.valid.numpy())
