@@ -1174,6 +1174,9 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
     v.root_lo[a] = f32_down(root_lo[a]);
     v.root_hi[a] = f32_up(root_hi[a]);
   }
+  v.n_wide = (int32_t)s->n_wide;
+  v.n_tris = (int32_t)n;
+  v.n_mats = d->n_materials;
   v.env_kind = d->env_kind;
   v.env_w = d->env_width;
   v.env_h = d->env_height;
@@ -1324,7 +1327,8 @@ static int run_bounces(lt_scene *s, Lane &lane, int32_t max_depth, int32_t rr_st
       s->stats.kernel_launches += 2;
     }
     ShadeArgs sa{depth, max_depth, rr_start, t_min, 0, s->octant_sort ? 1 : 0, perm,
-                 (flags & LT_FLAG_COUNT) ? s->ray_ctr.as<unsigned long long>() + 3 : nullptr};
+                 (flags & LT_FLAG_COUNT) ? s->ray_ctr.as<unsigned long long>() + 3 : nullptr,
+                 lane.cap};
     CK(launch_shade(sc, sa, pa, shade_grid,
                     s->use_window && s->use_shade_window ? &s->shade_window : nullptr, prim,
                     ws->q_o[cur].as<float4>(), ws->q_d[cur].as<float4>(),

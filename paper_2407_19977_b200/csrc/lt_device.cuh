@@ -31,6 +31,16 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+// -DLT_CHECKS (the checked build, tools/checked_tests.sh): device asserts on
+// every index the hot kernels derive (node / triangle / material ids, stack
+// depth, queue slots, pixels); compiled out otherwise.
+#ifdef LT_CHECKS
+#include <cassert>
+#define LT_ASSERT(c) assert(c)
+#else
+#define LT_ASSERT(c) ((void)0)
+#endif
+
 #define LT_PI_F 3.14159265358979323846f
 #define LT_INV_PI_F 0.318309886183790671538f
 #define LT_DET_EPS_F 1e-9f      // geometry.py:17
@@ -92,6 +102,7 @@ struct SceneView {
   int32_t env_w, env_h;
   float env_scale;
   float env_a[3], env_b[3];
+  int32_t n_wide, n_tris, n_mats;  // bounds for the checked build
 };
 
 // --------------------------------------------------------------- PCG32

@@ -313,6 +313,7 @@ __global__ void __launch_bounds__(kTraceThreads, LT_TRACE_MIN_BLOCKS)
       return LT_LINK_EXIT;
     };
     auto push = [&](int32_t x, float tx) {
+      LT_ASSERT(sp < LT_STACK);
       const uint2 e = make_uint2((uint32_t)x, __float_as_uint(tx));
       if (sp < kShortStack)
         s_stk[sp * kTraceThreads] = e;
@@ -325,6 +326,7 @@ __global__ void __launch_bounds__(kTraceThreads, LT_TRACE_MIN_BLOCKS)
     // hit children go on the stack farthest first
 #pragma unroll 1
     for (int step = 0; step < LT_NODE_STEPS && q >= 0 && node >= 0; ++step) {
+      LT_ASSERT(node < sc.n_wide);
       const Hits4 h = visit4o(sc.wnodes + LT_NODE_F4 * (int64_t)node, rs, t_min, best.t);
       if (COUNT) nn += 4;
       if (sp <= kShortStack - 3) {
@@ -445,6 +447,7 @@ __global__ void __launch_bounds__(kShadeThreads, LT_SHADE_MIN_BLOCKS)
         const float4 ro = __ldcs(&q_o[q]);
         const float4 rd = __ldcs(&q_d[q]);
         p = __float_as_int(ro.w);
+        LT_ASSERT(p >= 0 && p < sa.cap);
         o = mk(ro.x, ro.y, ro.z);
         d = mk(rd.x, rd.y, rd.z);
       }
@@ -470,6 +473,7 @@ __global__ void __launch_bounds__(kShadeThreads, LT_SHADE_MIN_BLOCKS)
       } else {
         // issue every random load of this hit before using any of them: one
         // 64 B shading record (geometric normal + material, vertex normals)
+        LT_ASSERT(k < sc.n_tris);
         const int64_t k4 = 4 * (int64_t)k;
         const bool scatter = sa.depth != sa.max_depth - 1;
         const float4 s0 = __ldg(&sc.shade[k4]);
@@ -481,6 +485,7 @@ __global__ void __launch_bounds__(kShadeThreads, LT_SHADE_MIN_BLOCKS)
           if (!primary) rs = __ldcs(&pa.rng[p]);
         }
         const int32_t mi = __float_as_int(s0.w);
+        LT_ASSERT(mi >= 0 && mi < sc.n_mats);
         const GpuMaterial &mt = sc.mats[mi];
         if (sa.warp_ctr)
           cls = !scatter ? 1
@@ -580,6 +585,7 @@ __global__ void __launch_bounds__(kShadeThreads, LT_SHADE_MIN_BLOCKS)
       __syncthreads();
       if (emit) {
         const int slot = s_base + s_off[bin] + rank;
+        LT_ASSERT(slot < sa.cap);
         __stcs(&n_o[slot], out_o);
         __stcs(&n_d[slot], out_d);
       }
@@ -593,6 +599,7 @@ __global__ void __launch_bounds__(kShadeThreads, LT_SHADE_MIN_BLOCKS)
         slot0 = __shfl_sync(kFull, slot0, leader);
         if (emit) {
           const int slot = slot0 + __popc(mask & ((1u << lane) - 1u));
+          LT_ASSERT(slot < sa.cap);
           __stcs(&n_o[slot], out_o);
           __stcs(&n_d[slot], out_d);
         }

@@ -60,6 +60,7 @@ struct ShadeArgs {
   // LT_FLAG_COUNT: [warps, warps whose active lanes span > 1 material class,
   // sum over warps of the distinct classes] (shading divergence evidence)
   unsigned long long *warp_ctr;
+  int64_t cap;  // path / queue capacity of the lane (checked build)
 };
 
 struct AccumArgs {

@@ -123,6 +123,7 @@ template <bool COUNT>
 __device__ __forceinline__ void leaf_test(const SceneView &sc, uint32_t k, f3 o, f3 d, float t_min,
                                           HitRec &best, int32_t &best_orig, int &tests) {
   while (true) {
+    LT_ASSERT(k < (uint32_t)sc.n_tris);
     const float4 t0 = __ldg(&sc.tris[LT_TRI_F4 * (size_t)k]);
     const float4 t1 = __ldg(&sc.tris[LT_TRI_F4 * (size_t)k + 1]);
     const float4 t2 = __ldg(&sc.tris[LT_TRI_F4 * (size_t)k + 2]);
@@ -256,6 +257,7 @@ __device__ __forceinline__ bool occluded(const SceneView &sc, f3 o, f3 d, float 
   int32_t best_orig = 0x7fffffff;
   while (true) {
     while (node >= 0) {
+      LT_ASSERT(node < sc.n_wide && sp + 3 <= LT_STACK);
       const Hits4 h = visit4o(sc.wnodes + LT_NODE_F4 * (int64_t)node, rs, t_min, t_max);
       if (h.k3 < kInf) stk[sp++] = h.l3;
       if (h.k2 < kInf) stk[sp++] = h.l2;
@@ -293,6 +295,7 @@ __device__ __forceinline__ HitRec traverse(const SceneView &sc, f3 o, f3 d, floa
     while (true) {
       while (node >= 0) {
         if (WIDE) {
+          LT_ASSERT(node < sc.n_wide && sp + 3 <= LT_STACK);
           const Hits4 h = visit4o(sc.wnodes + LT_NODE_F4 * (int64_t)node, rs, t_min, best.t);
           if (COUNT) nodes += 4;
           if (h.k3 < kInf) { stk_node[sp] = h.l3; stk_t[sp] = h.k3; ++sp; }
@@ -300,6 +303,7 @@ __device__ __forceinline__ HitRec traverse(const SceneView &sc, f3 o, f3 d, floa
           if (h.k1 < kInf) { stk_node[sp] = h.l1; stk_t[sp] = h.k1; ++sp; }
           node = h.k0 < kInf ? h.l0 : LT_LINK_EXIT;
         } else {
+          LT_ASSERT(sp + 1 <= LT_STACK);
           const float4 *np = sc.nodes + 4 * (int64_t)node;
           const float4 a = __ldg(np + 0), b = __ldg(np + 1), c = __ldg(np + 2), e = __ldg(np + 3);
           if (COUNT) nodes += 2;
