@@ -59,24 +59,11 @@
 // Leaf-ordered triangle record in float4 units: (v0, orig), (e1, leaf-end),
 // (e2, 0) = 48 B.
 #define LT_TRI_F4 3
-#ifdef LT_QNODE
-// Quantized record (64 B): f4[0] = (origin.xyz, scale.x), f4[1] = (qlo.x,
-// qhi.x, qlo.y, qhi.y), f4[2] = (qlo.z, qhi.z, scale.y, scale.z), f4[3] =
-// links; q* hold one byte per child: plane = origin + q * scale, rounded
-// outward with one quantum of padding (see k_flatten_wide).
-#define LT_NODE_F4 4
-#define LT_NODE_LINKS 3
-#else
 #define LT_NODE_F4 14
 #define LT_NODE_LINKS 12
-#endif
 // robustness: child exit distances are widened by 1 + 2*gamma(3) so fp32
 // rounding in the slab test never culls a box the float64 reference keeps
-#ifdef LT_QNODE
-#define LT_SLAB_WIDEN 1.000001f
-#else
 #define LT_SLAB_WIDEN 1.0000004f
-#endif
 
 enum : uint32_t {
   MAT_DIFFUSE_ONLY = 1u,  // m <= 0 and sw <= 0 (material.py:304-315 fast path)

@@ -78,51 +78,6 @@ __global__ void k_flatten_wide(const double *__restrict__ bmin, const double *__
     link[c] = count[x] > 0 ? ~first[x] : wide_of[x];
   }
   float4 *o = out + LT_NODE_F4 * i;
-#ifdef LT_QNODE
-  // Quantized record: per axis the node box (union of the children's
-  // float64 boxes) on a grid of 2^e steps with at most 250 steps across it;
-  // origin = lo - 1 step rounded down; child planes floor / ceil on that
-  // grid with one more step outward (the decode's rounding allowance), so
-  // every decoded plane lies on or outside the reference's float64 box.
-  // Empty slots: lo byte 255 > hi byte 0, an inverted box.
-  float origin[3], scale[3];
-  uint32_t qlo[3] = {0, 0, 0}, qhi[3] = {0, 0, 0};
-  for (int a = 0; a < 3; ++a) {
-    double nlo = __longlong_as_double(0x7ff0000000000000ll);  // +inf
-    double nhi = -nlo;
-    for (int c = 0; c < 4; ++c) {
-      const int32_t x = children[4 * i + c];
-      if (x < 0) continue;
-      nlo = fmin(nlo, bmin[3 * (int64_t)x + a]);
-      nhi = fmax(nhi, bmax[3 * (int64_t)x + a]);
-    }
-    int e = 0;
-    const double ext = nhi - nlo;
-    if (ext > 0.0) frexp(ext / 250.0, &e);
-    else e = -100;
-    e = max(-100, min(100, e));
-    scale[a] = ldexpf(1.f, e);
-    origin[a] = __double2float_rd(nlo - (double)scale[a]);
-    for (int c = 0; c < 4; ++c) {
-      const int32_t x = children[4 * i + c];
-      uint32_t bl = 255, bh = 0;
-      if (x >= 0) {
-        const double l = floor((bmin[3 * (int64_t)x + a] - (double)origin[a]) / scale[a]) - 1.0;
-        const double h = ceil((bmax[3 * (int64_t)x + a] - (double)origin[a]) / scale[a]) + 1.0;
-        bl = (uint32_t)fmax(0.0, l);
-        bh = (uint32_t)fmin(255.0, h);
-      }
-      qlo[a] |= bl << (8 * c);
-      qhi[a] |= bh << (8 * c);
-    }
-  }
-  (void)lo;
-  (void)hi;
-  o[0] = make_float4(origin[0], origin[1], origin[2], scale[0]);
-  o[1] = make_float4(__uint_as_float(qlo[0]), __uint_as_float(qhi[0]), __uint_as_float(qlo[1]),
-                     __uint_as_float(qhi[1]));
-  o[2] = make_float4(__uint_as_float(qlo[2]), __uint_as_float(qhi[2]), scale[1], scale[2]);
-#else
   for (int a = 0; a < 3; ++a) {
     const float4 l4 = make_float4(lo[a][0], lo[a][1], lo[a][2], lo[a][3]);
     const float4 h4 = make_float4(hi[a][0], hi[a][1], hi[a][2], hi[a][3]);
@@ -132,7 +87,6 @@ __global__ void k_flatten_wide(const double *__restrict__ bmin, const double *__
     o[4 * a + 3] = l4;
   }
   o[LT_NODE_LINKS + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
-#endif
   o[LT_NODE_LINKS] = make_float4(__int_as_float(link[0]), __int_as_float(link[1]),
                                  __int_as_float(link[2]), __int_as_float(link[3]));
 }
@@ -373,7 +327,7 @@ __global__ void __launch_bounds__(kTraceThreads, LT_TRACE_MIN_BLOCKS)
 #pragma unroll 1
     for (int step = 0; step < LT_NODE_STEPS && q >= 0 && node >= 0; ++step) {
       LT_ASSERT(node < sc.n_wide);
-      const Hits4 h = LT_VISIT(sc.wnodes + LT_NODE_F4 * (int64_t)node, rs, t_min, best.t);
+      const Hits4 h = visit4o(sc.wnodes + LT_NODE_F4 * (int64_t)node, rs, t_min, best.t);
       if (COUNT) nn += 4;
       if (sp <= kShortStack - 3) {
         // common case: all three fit in shared memory (predicated stores)

@@ -51,7 +51,6 @@ __device__ __forceinline__ float fmax3f(float a, float b, float c) {
 struct RaySlab {
   f3 o, inv;
   int nx, ny, nz;
-  bool sx, sy, sz;  // negative inverse direction per axis
 };
 
 __device__ __forceinline__ RaySlab ray_slab(f3 o, f3 d) {
@@ -63,9 +62,6 @@ __device__ __forceinline__ RaySlab ray_slab(f3 o, f3 d) {
   r.nx = 2 * (int)(__float_as_uint(r.inv.x) >> 31);
   r.ny = 4 + 2 * (int)(__float_as_uint(r.inv.y) >> 31);
   r.nz = 8 + 2 * (int)(__float_as_uint(r.inv.z) >> 31);
-  r.sx = r.inv.x < 0.f;
-  r.sy = r.inv.y < 0.f;
-  r.sz = r.inv.z < 0.f;
   return r;
 }
 
@@ -239,83 +235,6 @@ __device__ __forceinline__ Hits4 visit4o(const float4 *__restrict__ np, const Ra
   return h;
 }
 
-// Quantized record (LT_QNODE): per axis B = scale * inv and A' = (origin -
-// o) * inv - 2^23 B once per node; a plane byte q becomes the float 2^23 + q
-// with one PRMT (bytes [q, 0, 0, 0x4B]), and its distance is one FMA:
-// (2^23 + q) B + A' = (origin + q scale - o) inv up to the rounding of A'
-// (< one quantum, covered by the record's padding quantum) and relative
-// roundings (covered by LT_SLAB_WIDEN).  The near / far byte words are
-// picked by the ray's direction signs.
-__device__ __forceinline__ float qplane(uint32_t w, uint32_t sel) {
-  return __uint_as_float(__byte_perm(w, 0x4B000000u, sel));
-}
-
-// (f0 * b + a, f1 * b + a) as one FFMA2.
-__device__ __forceinline__ void fma2(float f0, float f1, float b, float a, float &t0, float &t1) {
-  unsigned long long p, r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(p) : "f"(f0), "f"(f1));
-  asm("{\n\t.reg .b64 bb, aa;\n\t"
-      "mov.b64 bb, {%2, %2};\n\t"
-      "mov.b64 aa, {%3, %3};\n\t"
-      "fma.rn.f32x2 %0, %1, bb, aa;\n\t}"
-      : "=l"(r) : "l"(p), "f"(b), "f"(a));
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(t0), "=f"(t1) : "l"(r));
-}
-
-__device__ __forceinline__ void qaxis(uint32_t near_w, uint32_t far_w, float origin, float scale,
-                                      float o, float inv, float (&tn)[4], float (&tf)[4]) {
-  const float B = scale * inv;
-  const float A = fmaf(-8388608.f, B, (origin - o) * inv);
-  fma2(qplane(near_w, 0x7540u), qplane(near_w, 0x7541u), B, A, tn[0], tn[1]);
-  fma2(qplane(near_w, 0x7542u), qplane(near_w, 0x7543u), B, A, tn[2], tn[3]);
-  fma2(qplane(far_w, 0x7540u), qplane(far_w, 0x7541u), B, A, tf[0], tf[1]);
-  fma2(qplane(far_w, 0x7542u), qplane(far_w, 0x7543u), B, A, tf[2], tf[3]);
-}
-
-__device__ __forceinline__ Hits4 visit4q(const float4 *__restrict__ np, const RaySlab &rs,
-                                         float t_min, float t_max) {
-  const float kInf = __int_as_float(0x7f800000);
-  float4 a, b, c, ln4;
-  ldg_pair(np, a, b);
-  ldg_pair(np + 2, c, ln4);
-  const uint32_t lx = __float_as_uint(b.x), hx = __float_as_uint(b.y);
-  const uint32_t ly = __float_as_uint(b.z), hy = __float_as_uint(b.w);
-  const uint32_t lz = __float_as_uint(c.x), hz = __float_as_uint(c.y);
-  float nx[4], fx[4], ny[4], fy[4], nz[4], fz[4];
-  qaxis(rs.sx ? hx : lx, rs.sx ? lx : hx, a.x, a.w, rs.o.x, rs.inv.x, nx, fx);
-  qaxis(rs.sy ? hy : ly, rs.sy ? ly : hy, a.y, c.z, rs.o.y, rs.inv.y, ny, fy);
-  qaxis(rs.sz ? hz : lz, rs.sz ? lz : hz, a.z, c.w, rs.o.z, rs.inv.z, nz, fz);
-  float tn[4], tf[4];
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    tn[k] = fmax3f(nx[k], ny[k], fmaxf(nz[k], t_min));
-    tf[k] = fmin3f(fx[k], fy[k], fminf(fz[k], t_max));
-  }
-  scale2(tf[0], tf[1], LT_SLAB_WIDEN, tf[0], tf[1]);
-  scale2(tf[2], tf[3], LT_SLAB_WIDEN, tf[2], tf[3]);
-  Hits4 h;
-  h.k0 = tn[0] <= tf[0] ? tn[0] : kInf;
-  h.k1 = tn[1] <= tf[1] ? tn[1] : kInf;
-  h.k2 = tn[2] <= tf[2] ? tn[2] : kInf;
-  h.k3 = tn[3] <= tf[3] ? tn[3] : kInf;
-  h.l0 = __float_as_int(ln4.x);
-  h.l1 = __float_as_int(ln4.y);
-  h.l2 = __float_as_int(ln4.z);
-  h.l3 = __float_as_int(ln4.w);
-  cswap(h.k0, h.l0, h.k1, h.l1);
-  cswap(h.k2, h.l2, h.k3, h.l3);
-  cswap(h.k0, h.l0, h.k2, h.l2);
-  cswap(h.k1, h.l1, h.k3, h.l3);
-  cswap(h.k1, h.l1, h.k2, h.l2);
-  return h;
-}
-
-#ifdef LT_QNODE
-#define LT_VISIT visit4q
-#else
-#define LT_VISIT visit4o
-#endif
-
 // Pop-time cull distance for the current best t: a stacked entry whose entry
 // distance exceeds it cannot hold a closer hit (bvh.py:389), with the same
 // error allowance as the slab test.
@@ -339,7 +258,7 @@ __device__ __forceinline__ bool occluded(const SceneView &sc, f3 o, f3 d, float 
   while (true) {
     while (node >= 0) {
       LT_ASSERT(node < sc.n_wide && sp + 3 <= LT_STACK);
-      const Hits4 h = LT_VISIT(sc.wnodes + LT_NODE_F4 * (int64_t)node, rs, t_min, t_max);
+      const Hits4 h = visit4o(sc.wnodes + LT_NODE_F4 * (int64_t)node, rs, t_min, t_max);
       if (h.k3 < kInf) stk[sp++] = h.l3;
       if (h.k2 < kInf) stk[sp++] = h.l2;
       if (h.k1 < kInf) stk[sp++] = h.l1;
@@ -377,7 +296,7 @@ __device__ __forceinline__ HitRec traverse(const SceneView &sc, f3 o, f3 d, floa
       while (node >= 0) {
         if (WIDE) {
           LT_ASSERT(node < sc.n_wide && sp + 3 <= LT_STACK);
-          const Hits4 h = LT_VISIT(sc.wnodes + LT_NODE_F4 * (int64_t)node, rs, t_min, best.t);
+          const Hits4 h = visit4o(sc.wnodes + LT_NODE_F4 * (int64_t)node, rs, t_min, best.t);
           if (COUNT) nodes += 4;
           if (h.k3 < kInf) { stk_node[sp] = h.l3; stk_t[sp] = h.k3; ++sp; }
           if (h.k2 < kInf) { stk_node[sp] = h.l2; stk_t[sp] = h.k2; ++sp; }
