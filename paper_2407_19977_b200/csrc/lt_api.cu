@@ -843,40 +843,6 @@ static int device_layout(lt_scene *s, const double *bmin, const double *bmax,
                    "BVH too deep for the traversal stack: the 4-wide tree can hold %d pending "
                    "entries and the binary tree is %d levels deep (limit %d)",
                    res[1], res[2], LT_STACK);
-  // LT_WIDE_ORDER=dfs (experiment): renumber the wide nodes in depth-first
-  // preorder (a node's first child right after it, every subtree contiguous)
-  // instead of breadth first
-  const char *wo = std::getenv("LT_WIDE_ORDER");
-  if (wo && std::strcmp(wo, "dfs") == 0 && s->n_wide > 1) {
-    const int64_t nw_ = s->n_wide;
-    std::vector<int32_t> ch(4 * nw_), cnt(nn), wof(nn);
-    CK(cudaMemcpyAsync(ch.data(), t_wch.p, 16 * nw_, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(cnt.data(), count, 4 * nn, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(wof.data(), t_wof.p, 4 * nn, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    std::vector<int32_t> newid(nw_, -1), stack{0};
-    int32_t next = 0;
-    while (!stack.empty()) {
-      const int32_t i = stack.back();
-      stack.pop_back();
-      newid[i] = next++;
-      for (int k = 3; k >= 0; --k) {
-        const int32_t x = ch[4 * i + k];
-        if (x >= 0 && cnt[x] == 0) stack.push_back(wof[x]);
-      }
-    }
-    std::vector<int32_t> ch2(4 * nw_), wof2(wof);
-    for (int64_t i = 0; i < nw_; ++i)
-      for (int k = 0; k < 4; ++k) {
-        const int32_t x = ch[4 * i + k];
-        ch2[4 * newid[i] + k] = x;
-        if (x >= 0 && cnt[x] == 0) wof2[x] = newid[wof[x]];
-      }
-    wof2[0] = 0;
-    CK(cudaMemcpyAsync(t_wch.p, ch2.data(), 16 * nw_, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(t_wof.p, wof2.data(), 4 * nn, cudaMemcpyHostToDevice, st));
-    CK(cudaStreamSynchronize(st));
-  }
   return LT_OK;
 }
 
