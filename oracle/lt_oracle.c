@@ -1155,3 +1155,10 @@ done:
   free(sweep_area); free(sweep_count); free(stack);
   return n_nodes;
 }
+
+/* _hit_frame (geometry.py:210-241) for the query-kernel checks */
+void oc_hit_frame_api(const double d[3], const double a[3], const double b[3], const double c[3],
+                      const double n0[3], const double n1[3], const double n2[3], double u,
+                      double v, double g[3], double sh[3], int *front) {
+  oc_hit_frame(d, a, b, c, n0, n1, n2, u, v, g, sh, front);
+}

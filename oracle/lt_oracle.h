@@ -60,6 +60,9 @@ int oc_mt_intersect(const double o[3], const double d[3], const double a[3],
 int oc_slab_intersect(const double o[3], const double inv[3], const double bmin[3],
                       const double bmax[3], double t_min, double t_max,
                       double *t_enter, double *t_exit);
+void oc_hit_frame_api(const double d[3], const double a[3], const double b[3], const double c[3],
+                      const double n0[3], const double n1[3], const double n2[3], double u,
+                      double v, double g[3], double sh[3], int *front);
 int64_t oc_traverse(const oc_scene *s, const double o[3], const double d[3],
                     double t_min, double t_max, double *t, double *u, double *v,
                     int64_t *nodes_visited, int64_t *tri_tests);

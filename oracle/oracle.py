@@ -93,6 +93,13 @@ def lib():
                                        C.c_int]
         h.oc_primary_rays.argtypes = [_lp, C.c_int64, C.c_int64, _dp, C.c_int32, C.c_int32,
                                       C.c_uint64, _dp, _dp]
+        h.oc_mt_intersect.restype = C.c_int
+        h.oc_mt_intersect.argtypes = [_dp, _dp, _dp, _dp, _dp, C.c_double, C.c_double, _dp, _dp,
+                                      _dp]
+        h.oc_slab_intersect.restype = C.c_int
+        h.oc_slab_intersect.argtypes = [_dp, _dp, _dp, _dp, C.c_double, C.c_double, _dp, _dp]
+        h.oc_hit_frame_api.argtypes = [_dp, _dp, _dp, _dp, _dp, _dp, _dp, C.c_double, C.c_double,
+                                       _dp, _dp, C.POINTER(C.c_int)]
         h.oc_build_bvh.restype = C.c_int64
         h.oc_build_bvh.argtypes = [_dp, _dp, _dp, C.c_int64, C.c_int32, C.c_int32, _dp, _dp,
                                    _ip, _ip, _ip, _ip, _ip, _lp, _lp]
@@ -126,6 +133,40 @@ def seed_stream(pixel: int, sample: int, seed: int) -> tuple[int, int]:
     s, i = C.c_uint64(), C.c_uint64()
     lib().oc_seed_stream(pixel, sample, seed & (2**64 - 1), C.byref(s), C.byref(i))
     return s.value, i.value
+
+
+# ------------------------------------------------------------------ geometry
+
+def _v(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def mt_intersect(o, d, a, b, c, t_min, t_max):
+    """_mt_intersect (geometry.py:138-167): (hit, t, u, v)."""
+    t, u, v = C.c_double(), C.c_double(), C.c_double()
+    ok = lib().oc_mt_intersect(*[_p(_v(x), C.c_double) for x in (o, d, a, b, c)], float(t_min),
+                               float(t_max), C.byref(t), C.byref(u), C.byref(v))
+    return bool(ok), t.value, u.value, v.value
+
+
+def slab_intersect(o, d, lo, hi, t_min, t_max):
+    """ray_aabb_intersect's arithmetic (geometry.py:244-248, 170-207):
+    (hit, t_enter, t_exit)."""
+    inv = np.array([np.inf if x == 0.0 else 1.0 / x for x in np.asarray(d, np.float64)])
+    tn, tf = C.c_double(), C.c_double()
+    ok = lib().oc_slab_intersect(_p(_v(o), C.c_double), _p(inv, C.c_double),
+                                 _p(_v(lo), C.c_double), _p(_v(hi), C.c_double), float(t_min),
+                                 float(t_max), C.byref(tn), C.byref(tf))
+    return bool(ok), tn.value, tf.value
+
+
+def hit_frame(d, a, b, c, n0, n1, n2, u, v):
+    """_hit_frame (geometry.py:210-241): (geometric, shading, front)."""
+    g, s = np.zeros(3), np.zeros(3)
+    fr = C.c_int()
+    lib().oc_hit_frame_api(*[_p(_v(x), C.c_double) for x in (d, a, b, c, n0, n1, n2)], float(u),
+                           float(v), _p(g, C.c_double), _p(s, C.c_double), C.byref(fr))
+    return g, s, bool(fr.value)
 
 
 # ------------------------------------------------------------------ camera
