@@ -126,3 +126,72 @@ def test_compute_refuses_without_gpu():
         lb.render_image(g.scene, g.settings)
     with pytest.raises(RuntimeError):
         lb.intersect_scene_batch(g.triangles, g.bvh, g["rays_o"], g["rays_d"])
+
+
+REFERENCE_ALL = [   # luxtrace/__init__.py:40-65
+    "Aabb", "Hit", "Ray", "Triangle", "TriangleBuffer", "aabb_surface_area", "aabb_union",
+    "normalize", "ray_aabb_intersect", "ray_triangle_intersect", "triangle_bounds", "vec3",
+    "PcgState", "next_unit_real", "pcg_next_u32", "pcg_seed", "seed_stream",
+    "BuildStats", "Bvh", "brute_force_intersect_batch", "build_bvh", "intersect_any",
+    "intersect_scene", "intersect_scene_batch", "intersect_scene_counted",
+    "traversal_counts_batch", "validate_bvh",
+    "BsdfSample", "OpenPbrParams", "cosine_sample_hemisphere", "emitted_radiance", "eval_bsdf",
+    "fresnel_schlick", "ggx_ndf", "ggx_sample_half_vector", "pack_materials", "pdf_bsdf",
+    "sample_bsdf", "smith_g2",
+    "CameraConfig", "EnvironmentConfig", "MaterialMap", "RenderConfig", "SceneDescription",
+    "SceneError", "flatten_scene", "generate_smooth_normals", "load_gltf", "load_render_config",
+    "load_scene",
+    "RenderResult", "RenderSettings", "environment_radiance", "generate_camera_ray",
+    "render_image", "render_progressive", "trace_radiance",
+    "linear_to_srgb", "pbr_neutral_tonemap", "quantize_to_u8", "srgb_to_linear",
+    "tonemap_to_u8", "write_linear_dump", "write_png",
+    "bumpy_sphere", "bumpy_sphere_glb", "icosphere", "icosphere_glb", "save_glb",
+    "set_worker_count", "thread_cap",
+]   # (the benchmark harness names are out of scope)
+
+
+def test_reference_api_names_exported():
+    missing = [n for n in REFERENCE_ALL if not hasattr(lb, n)]
+    assert missing == []
+
+
+def test_validate_bvh_flags_faults():
+    """bvh.py:305-352 with the fault injections of test_bvh.py:149-174."""
+    import copy
+    g = golden_scene("sphere2k")
+    assert lb.validate_bvh(g.bvh, g.triangles) == []
+    b = copy.deepcopy(g.bvh)
+    c = (b.bounds_min[0] + b.bounds_max[0]) / 2.0
+    b.bounds_min = b.bounds_min.copy()
+    b.bounds_max = b.bounds_max.copy()
+    b.bounds_min[0], b.bounds_max[0] = c - 1e-4, c + 1e-4
+    assert any("node 0" in m and "exceed" in m for m in lb.validate_bvh(b, g.triangles))
+    b = copy.deepcopy(g.bvh)
+    b.triangle_order = b.triangle_order.copy()
+    b.triangle_order[0] = b.triangle_order[1]
+    assert any("permutation" in m for m in lb.validate_bvh(b, g.triangles))
+    b = copy.deepcopy(g.bvh)
+    victim = int(np.nonzero(b.triangle_count > 0)[0][3])
+    b.first_triangle = b.first_triangle.copy()
+    b.first_triangle[victim] = len(g.triangles)
+    assert any(f"node {victim}" in m and "out of bounds" in m
+               for m in lb.validate_bvh(b, g.triangles))
+
+
+def test_writers_and_geometry_helpers(tmp_path):
+    img = (np.arange(4 * 5 * 3) % 256).astype(np.uint8).reshape(4, 5, 3)
+    lb.write_png(tmp_path / "a.png", img)
+    from PIL import Image
+    assert np.array_equal(np.asarray(Image.open(tmp_path / "a.png")), img)
+    with pytest.raises(ValueError):
+        lb.write_png(tmp_path / "b.png", img.astype(np.float32))
+    lin = np.linspace(0, 2, 4 * 5 * 3).reshape(4, 5, 3)
+    lb.write_linear_dump(tmp_path / "a.raw", lin)
+    assert np.array_equal(np.fromfile(tmp_path / "a.raw", dtype="<f4"),
+                          lin.astype("<f4").ravel())
+    t = lb.Triangle(lb.vec3(0, 0, 0), lb.vec3(1, 0, 0), lb.vec3(0, 2, 0), *[lb.vec3(0, 0, 1)] * 3)
+    box = lb.triangle_bounds(t)
+    assert np.allclose(box.min, -2e-7) and np.allclose(box.max, [1 + 2e-7, 2 + 2e-7, 2e-7])
+    u = lb.aabb_union(box, lb.Aabb(lb.vec3(-1, -1, -1), lb.vec3(0, 0, 0)))
+    assert np.allclose(u.min, -1.0) and lb.aabb_surface_area(lb.Aabb.empty()) == 0.0
+    assert lb.set_worker_count(1) == 1 and lb.thread_cap() >= 1
