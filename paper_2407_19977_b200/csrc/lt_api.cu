@@ -182,7 +182,7 @@ constexpr size_t kCacheBytes = size_t(2) << 30;
 struct Lane {
   int64_t cap = 0;
   int32_t depth_cap = 0;
-  DevBuf q_o[2], q_d[2], hits, T, L, rng, counters;
+  DevBuf q_o[2], q_d[2], hits, S, inc, counters;
   // LT_FLAG_SORT_MATERIALS: per-entry class, the class-grouped slot order,
   // class totals + cursors
   DevBuf cls, perm, cls_ctr;
@@ -1256,9 +1256,7 @@ static int ensure_lane(lt_scene *s, Lane &ln, int64_t cap, int32_t max_depth) {
       RET(ln.q_d[k].ensure(16 * cap));
     }
     RET(ln.hits.ensure(16 * cap));
-    RET(ln.T.ensure(16 * cap));
-    RET(ln.L.ensure(16 * cap));
-    RET(ln.rng.ensure(16 * cap));
+    RET(ln.S.ensure(32 * cap));
     RET(ln.cls.ensure(cap));
     RET(ln.perm.ensure(4 * cap));
     RET(ln.cls_ctr.ensure(sizeof(int32_t) * 2 * kShadeClasses));
@@ -1272,8 +1270,8 @@ static int ensure_lane(lt_scene *s, Lane &ln, int64_t cap, int32_t max_depth) {
   return LT_OK;
 }
 
-static PathArrays path_arrays(Lane &ln) {
-  return PathArrays{ln.T.as<float4>(), ln.L.as<float4>(), ln.rng.as<ulonglong2>()};
+static PathArrays path_arrays(Lane &ln, bool explicit_inc = false) {
+  return PathArrays{ln.S.as<float4>(), explicit_inc ? ln.inc.as<uint64_t>() : nullptr};
 }
 
 static int record_event(lt_scene *s, cudaStream_t st) {
@@ -1292,7 +1290,7 @@ static int record_event(lt_scene *s, cudaStream_t st) {
 // the primary rays and counters[0] their number (explicit rays).
 static int run_bounces(lt_scene *s, Lane &lane, int32_t max_depth, int32_t rr_start, float t_min,
                        uint32_t flags, cudaStream_t st, const RaygenArgs *primary,
-                       int64_t max_rays) {
+                       int64_t max_rays, bool explicit_paths = false) {
   SceneView sc = s->view;
   // a batch never holds more than max_rays rays: small batches (tiny frames)
   // launch only the CTAs that can find work
@@ -1305,10 +1303,9 @@ static int run_bounces(lt_scene *s, Lane &lane, int32_t max_depth, int32_t rr_st
   Lane *ws = &lane;
   int32_t *ctr = ws->counters.as<int32_t>();
   int32_t *fetch = ctr + max_depth + 1;
-  const PathArrays pa = path_arrays(lane);
+  const PathArrays pa = path_arrays(lane, explicit_paths);
   int cur = 0;
   for (int32_t depth = 0; depth < max_depth; ++depth) {
-    const RaygenArgs *prim = depth == 0 ? primary : nullptr;
     if (flags & LT_FLAG_PROFILE) RET(record_event(s, st));
     // (in-kernel ray generation for trace measured slower than reading the
     // 32 B ray record: the float64 camera math serializes the refill path)
@@ -1330,7 +1327,8 @@ static int run_bounces(lt_scene *s, Lane &lane, int32_t max_depth, int32_t rr_st
                  (flags & LT_FLAG_COUNT) ? s->ray_ctr.as<unsigned long long>() + 3 : nullptr,
                  lane.cap};
     CK(launch_shade(sc, sa, pa, shade_grid,
-                    s->use_window && s->use_shade_window ? &s->shade_window : nullptr, prim,
+                    s->use_window && s->use_shade_window ? &s->shade_window : nullptr, primary,
+                    depth == 0,
                     ws->q_o[cur].as<float4>(), ws->q_d[cur].as<float4>(),
                     ws->hits.as<float4>(), ctr + depth, ws->q_o[cur ^ 1].as<float4>(),
                     ws->q_d[cur ^ 1].as<float4>(), ctr + depth + 1, st));
@@ -1522,7 +1520,7 @@ static int render_impl(lt_scene *s, const lt_render_params *p, float *accum, uin
     launch_raygen(ra, path_arrays(ln), ln.q_o[0].as<float4>(), ln.q_d[0].as<float4>(), ctr, ls);
     RET(run_bounces(s, ln, p->max_depth, p->rr_start, t_min, p->flags, ls, &ra, ra.n_paths));
     AccumArgs aa{b.np, b.pc0, b.ns, pix_list};
-    launch_accumulate(aa, ln.L.as<float4>(), accum, valid, invalid, ls);
+    launch_accumulate(aa, ln.S.as<float4>(), accum, valid, invalid, ls);
     s->stats.kernel_launches += 2;
     s->stats.batches += 1;
     s->stats.paths += b.np * b.ns;
@@ -1774,10 +1772,11 @@ extern "C" int lt_trace_paths_host(lt_scene *s, const double *origins, const dou
   CK(cudaMemcpyAsync(d_inc, inc, 8 * n, cudaMemcpyHostToDevice, st));
   CK(cudaMemsetAsync(ln.counters.p, 0, sizeof(int32_t) * (2 * (size_t)max_depth + 2), st));
   CK(cudaMemsetAsync(s->ray_ctr.p, 0, 6 * sizeof(unsigned long long), st));
-  const PathArrays pa = path_arrays(ln);
+  RET(ln.inc.ensure(8 * (size_t)std::max<int64_t>(n, ln.cap)));
+  const PathArrays pa = path_arrays(ln, true);
   launch_raygen_explicit(d_o, d_d, d_state, d_inc, n, (float)t_min, pa, ln.q_o[0].as<float4>(),
                          ln.q_d[0].as<float4>(), ln.counters.as<int32_t>(), st);
-  RET(run_bounces(s, ln, max_depth, rr_start, (float)t_min, 0u, st, nullptr, n));
+  RET(run_bounces(s, ln, max_depth, rr_start, (float)t_min, 0u, st, nullptr, n, true));
   RET(s->s_b.ensure(32 * n));
   double *d_rgb = s->s_b.as<double>();
   uint64_t *d_sout = reinterpret_cast<uint64_t *>(d_rgb + 3 * n);

@@ -174,6 +174,35 @@ __device__ __forceinline__ void primary_rng(const RaygenArgs &ra, int64_t p, uin
   (void)pcg_next(state, inc);
 }
 
+// Pixel of render path p (the batch's sample-major path numbering) and its
+// PCG increment, seed_stream's (mix64(pixel) << 1) | 1 (rng.py:70-78).
+__device__ __forceinline__ uint64_t path_inc(const RaygenArgs &ra, int64_t p) {
+  const int64_t s_local = (int64_t)((uint32_t)p / (uint32_t)ra.n_pix);
+  const int64_t i = p - s_local * ra.n_pix;
+  const int64_t pix = ra.pix_list ? (int64_t)ra.pix_list[ra.pix_offset + i] : ra.pix_offset + i;
+  return (mix64((uint64_t)pix) << 1) | 1ULL;
+}
+
+// The 32 B path record: one 256-bit streaming load / store.
+__device__ __forceinline__ void ld_path(const float4 *__restrict__ S, int64_t p, float4 &T,
+                                        float4 &L, uint64_t &state) {
+  float4 a, b;
+  asm volatile("ld.global.cs.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z),
+                 "=f"(b.w)
+               : "l"(S + 2 * p));
+  T = make_float4(a.x, a.y, a.z, 0.f);
+  L = make_float4(a.w, b.x, b.y, 0.f);
+  state = ((uint64_t)__float_as_uint(b.w) << 32) | __float_as_uint(b.z);
+}
+__device__ __forceinline__ void st_path(float4 *__restrict__ S, int64_t p, const float4 &T,
+                                        const float4 &L, uint64_t state) {
+  asm volatile("st.global.cs.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(S + 2 * p),
+               "f"(T.x), "f"(T.y), "f"(T.z), "f"(L.x), "f"(L.y), "f"(L.z),
+               "f"(__uint_as_float((uint32_t)state)), "f"(__uint_as_float((uint32_t)(state >> 32)))
+               : "memory");
+}
+
 // Primary rays of a render batch: only the 32 B ray record is written; the
 // throughput (1), radiance (0) and PCG state are implied / regenerated by
 // the depth-0 shade launch.
@@ -203,20 +232,21 @@ __global__ void k_raygen_explicit(const double *__restrict__ o, const double *__
   q_o[p] = make_float4((float)o[3 * p], (float)o[3 * p + 1], (float)o[3 * p + 2],
                        __int_as_float((int32_t)p));
   q_d[p] = make_float4((float)d[3 * p], (float)d[3 * p + 1], (float)d[3 * p + 2], t_min);
-  pa.T[p] = make_float4(1.f, 1.f, 1.f, 0.f);
-  pa.L[p] = make_float4(0.f, 0.f, 0.f, 0.f);
-  pa.rng[p] = make_ulonglong2(state[p], inc[p]);
+  st_path(pa.S, p, make_float4(1.f, 1.f, 1.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f), state[p]);
+  pa.inc[p] = inc[p];
 }
 
 __global__ void k_gather_explicit(PathArrays pa, int64_t n, double *__restrict__ rgb,
                                   uint64_t *__restrict__ state_out) {
   const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (p >= n) return;
-  const float4 L = pa.L[p];
+  float4 T, L;
+  uint64_t st;
+  ld_path(pa.S, p, T, L, st);
   rgb[3 * p + 0] = L.x;
   rgb[3 * p + 1] = L.y;
   rgb[3 * p + 2] = L.z;
-  state_out[p] = pa.rng[p].x;
+  state_out[p] = st;
 }
 
 // ------------------------------------------------------------------ trace
@@ -458,17 +488,19 @@ __global__ void __launch_bounds__(kShadeThreads, LT_SHADE_MIN_BLOCKS)
         T = make_float4(1.f, 1.f, 1.f, 0.f);
         L = make_float4(0.f, 0.f, 0.f, 0.f);
       } else {
-        T = __ldcs(&pa.T[p]);
-        L = __ldcs(&pa.L[p]);
+        uint64_t st0;
+        ld_path(pa.S, p, T, L, st0);
+        rs.x = st0;
       }
       bool wrote_l = false;
+      bool scattered = false;
+      uint64_t st_out = rs.x;  // the PCG state after this bounce's draws
       cls = 0;  // miss
       if (k < 0) {
         const f3 e = env_radiance(sc, d);
         L.x += T.x * e.x;
         L.y += T.y * e.y;
         L.z += T.z * e.z;
-        __stcs(&pa.L[p], L);
         wrote_l = true;
       } else {
         // issue every random load of this hit before using any of them: one
@@ -482,7 +514,7 @@ __global__ void __launch_bounds__(kShadeThreads, LT_SHADE_MIN_BLOCKS)
           s1 = __ldg(&sc.shade[k4 + 1]);
           s2 = __ldg(&sc.shade[k4 + 2]);
           s3 = __ldg(&sc.shade[k4 + 3]);
-          if (!primary) rs = __ldcs(&pa.rng[p]);
+          if (!primary) rs.y = pa.inc ? __ldg(&pa.inc[p]) : path_inc(ra, p);
         }
         const int32_t mi = __float_as_int(s0.w);
         LT_ASSERT(mi >= 0 && mi < sc.n_mats);
@@ -498,7 +530,6 @@ __global__ void __launch_bounds__(kShadeThreads, LT_SHADE_MIN_BLOCKS)
           L.x += T.x * mt.el * mt.ec[0];
           L.y += T.y * mt.el * mt.ec[1];
           L.z += T.z * mt.el * mt.ec[2];
-          __stcs(&pa.L[p], L);
           wrote_l = true;
         }
         if (scatter) {
@@ -532,9 +563,11 @@ __global__ void __launch_bounds__(kShadeThreads, LT_SHADE_MIN_BLOCKS)
               Tn.z /= pr;
             }
           }
-          __stcs(&pa.rng[p], make_ulonglong2(state, inc));
+          scattered = true;
+          st_out = state;
           if (alive) {
-            __stcs(&pa.T[p], Tn);
+            st_path(pa.S, p, Tn, L, state);
+            wrote_l = false;  // (the record is current)
             const float t = h.x;
             out_o = make_float4(o.x + t * d.x, o.y + t * d.y, o.z + t * d.z, __int_as_float(p));
             out_d = make_float4(wi.x, wi.y, wi.z, sa.t_min);
@@ -542,9 +575,11 @@ __global__ void __launch_bounds__(kShadeThreads, LT_SHADE_MIN_BLOCKS)
           }
         }
       }
-      // the radiance slot of every path is written by its primary launch
-      // (raygen no longer clears it)
-      if (primary && !wrote_l) __stcs(&pa.L[p], L);
+      // a path that ends here leaves its radiance in the record (the
+      // accumulation reads it); the primary launch writes every path's
+      // record once (raygen does not clear it)
+      // (an explicit path -- pa.inc set -- also reports its final PCG state)
+      if (!emit && (wrote_l || primary || (scattered && pa.inc))) st_path(pa.S, p, T, L, st_out);
     }
     if (sa.warp_ctr) {
       // shading divergence: distinct material classes among a warp's lanes
@@ -834,7 +869,7 @@ void launch_pixel_list(int32_t width, int32_t height, int32_t tile, int32_t rank
 
 // Per-pixel sum of the batch's finite samples in sample order, plus valid /
 // invalid counts (integrator.py:266-272; the mean is sum / valid).
-__global__ void k_accumulate(AccumArgs aa, const float4 *__restrict__ L,
+__global__ void k_accumulate(AccumArgs aa, const float4 *__restrict__ S,
                              float *__restrict__ accum, uint32_t *__restrict__ valid,
                              uint32_t *__restrict__ invalid) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -844,7 +879,9 @@ __global__ void k_accumulate(AccumArgs aa, const float4 *__restrict__ L,
   float r = accum[3 * pix + 0], g = accum[3 * pix + 1], b = accum[3 * pix + 2];
   uint32_t nv = valid[pix], ni = invalid[pix];
   for (int64_t s = 0; s < aa.n_samples; ++s) {
-    const float4 x = L[s * aa.n_pix + i];
+    const int64_t p = s * aa.n_pix + i;
+    const float4 sa = __ldcs(&S[2 * p]), sb = __ldcs(&S[2 * p + 1]);
+    const float3 x = make_float3(sa.w, sb.x, sb.y);
     if (isfinite(x.x) && isfinite(x.y) && isfinite(x.z)) {
       r += x.x;
       g += x.y;
@@ -1164,13 +1201,13 @@ void launch_trace_rays(const SceneView &sc, const float4 *q_o, const float4 *q_d
 }
 
 cudaError_t launch_shade(const SceneView &sc, const ShadeArgs &sa, const PathArrays &pa, int grid,
-                         const cudaAccessPolicyWindow *window, const RaygenArgs *primary,
-                         const float4 *q_o, const float4 *q_d, const float4 *hits,
+                         const cudaAccessPolicyWindow *window, const RaygenArgs *rargs,
+                         bool primary, const float4 *q_o, const float4 *q_d, const float4 *hits,
                          const int32_t *count_in, float4 *n_o, float4 *n_d, int32_t *count_out,
                          cudaStream_t st) {
-  const RaygenArgs ra = primary ? *primary : RaygenArgs{};
+  const RaygenArgs ra = rargs ? *rargs : RaygenArgs{};
   ShadeArgs s2 = sa;
-  s2.primary = primary ? 1 : 0;
+  s2.primary = primary && rargs ? 1 : 0;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kShadeThreads);
@@ -1186,10 +1223,10 @@ cudaError_t launch_shade(const SceneView &sc, const ShadeArgs &sa, const PathArr
                             count_out);
 }
 
-void launch_accumulate(const AccumArgs &aa, const float4 *L, float *accum, uint32_t *valid,
+void launch_accumulate(const AccumArgs &aa, const float4 *S, float *accum, uint32_t *valid,
                        uint32_t *invalid, cudaStream_t st) {
   if (aa.n_pix <= 0) return;
-  k_accumulate<<<(unsigned)((aa.n_pix + 255) / 256), 256, 0, st>>>(aa, L, accum, valid, invalid);
+  k_accumulate<<<(unsigned)((aa.n_pix + 255) / 256), 256, 0, st>>>(aa, S, accum, valid, invalid);
 }
 
 void launch_pack_rays_f32(const float *o, const float *d, int64_t n, float t_min, float t_max,

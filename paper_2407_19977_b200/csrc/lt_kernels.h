@@ -31,10 +31,13 @@ constexpr int kShadeThreads = LT_SHADE_THREADS;
 #endif
 constexpr int kShortStack = LT_SHORT_STACK;  // per-lane traversal stack entries in shared memory
 
+// Per-path state, 32 B: S[2p] = (throughput.rgb, radiance.r), S[2p + 1] =
+// (radiance.gb, PCG state low / high words).  The PCG increment of a
+// rendered path is recomputed from its pixel (seed_stream's mix64), so it
+// is stored only for explicit paths (trace_radiance): inc (NULL in renders).
 struct PathArrays {
-  float4 *T;           // throughput rgb
-  float4 *L;           // radiance rgb
-  ulonglong2 *rng;     // PCG (state, inc)
+  float4 *S;
+  uint64_t *inc;
 };
 
 struct RaygenArgs {
@@ -99,8 +102,11 @@ cudaError_t launch_trace(const SceneView &sc, bool count_work, int grid,
                          unsigned long long *ray_ctr, cudaStream_t st);
 void launch_trace_rays(const SceneView &sc, const float4 *q_o, const float4 *q_d, int64_t n,
                        float4 *hits, int32_t *nodes, int32_t *tests, cudaStream_t st);
+// `ra`: the batch's RaygenArgs (render paths: pixel of a path id, the
+// depth-0 launch regenerates the primary state) or NULL for explicit paths;
+// `primary`: the depth-0 launch of a render batch.
 cudaError_t launch_shade(const SceneView &sc, const ShadeArgs &sa, const PathArrays &pa, int grid,
-                         const cudaAccessPolicyWindow *window, const RaygenArgs *primary,
+                         const cudaAccessPolicyWindow *window, const RaygenArgs *ra, bool primary,
                          const float4 *q_o, const float4 *q_d, const float4 *hits,
                          const int32_t *count_in, float4 *n_o, float4 *n_d, int32_t *count_out,
                          cudaStream_t st);
@@ -120,7 +126,7 @@ void launch_collapse_all(const double *bmin, const double *bmax, const int32_t *
                          const int32_t *right, const int32_t *count, int32_t *fifo,
                          int32_t *wide_children, int32_t *wide_of, int32_t *n_wide,
                          cudaStream_t st);
-void launch_accumulate(const AccumArgs &aa, const float4 *L, float *accum, uint32_t *valid,
+void launch_accumulate(const AccumArgs &aa, const float4 *S, float *accum, uint32_t *valid,
                        uint32_t *invalid, cudaStream_t st);
 void launch_pack_rays_f32(const float *o, const float *d, int64_t n, float t_min, float t_max,
                           float4 *q_o, float4 *q_d, cudaStream_t st);
