@@ -1309,10 +1309,16 @@ static int run_bounces(lt_scene *s, Lane &lane, int32_t max_depth, int32_t rr_st
     if (flags & LT_FLAG_PROFILE) RET(record_event(s, st));
     // (in-kernel ray generation for trace measured slower than reading the
     // 32 B ray record: the float64 camera math serializes the refill path)
+    // a render batch's primary rays carry no origin record (the camera)
+    const bool prim_rays = depth == 0 && primary;
+    const float4 cam_o = primary ? make_float4((float)primary->cam[0], (float)primary->cam[1],
+                                               (float)primary->cam[2], 0.f)
+                                 : make_float4(0.f, 0.f, 0.f, 0.f);
     CK(launch_trace(sc, (flags & LT_FLAG_COUNT) != 0, trace_grid,
-                    s->use_window ? &s->window : nullptr, ws->q_o[cur].as<float4>(),
-                    ws->q_d[cur].as<float4>(), ctr + depth, fetch + depth,
-                    ws->hits.as<float4>(), s->ray_ctr.as<unsigned long long>(), st));
+                    s->use_window ? &s->window : nullptr,
+                    prim_rays ? nullptr : ws->q_o[cur].as<float4>(), ws->q_d[cur].as<float4>(),
+                    ctr + depth, fetch + depth, ws->hits.as<float4>(),
+                    s->ray_ctr.as<unsigned long long>(), cam_o, st));
     if (flags & LT_FLAG_PROFILE) RET(record_event(s, st));
     const int32_t *perm = nullptr;
     if (flags & LT_FLAG_SORT_MATERIALS) {

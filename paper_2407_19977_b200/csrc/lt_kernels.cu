@@ -203,9 +203,10 @@ __device__ __forceinline__ void st_path(float4 *__restrict__ S, int64_t p, const
                : "memory");
 }
 
-// Primary rays of a render batch: only the 32 B ray record is written; the
-// throughput (1), radiance (0) and PCG state are implied / regenerated by
-// the depth-0 shade launch.
+// Primary rays of a render batch: only the 16 B direction record is written
+// (the origin is the camera, the path id the queue slot); the throughput
+// (1), radiance (0) and PCG state are implied / regenerated by the depth-0
+// shade launch.
 __global__ void k_raygen(RaygenArgs ra, PathArrays pa, float4 *__restrict__ q_o,
                          float4 *__restrict__ q_d, int32_t *__restrict__ count0) {
   const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -214,7 +215,7 @@ __global__ void k_raygen(RaygenArgs ra, PathArrays pa, float4 *__restrict__ q_o,
   f3 o, d;
   uint64_t state, inc;
   primary_ray(ra, p, o, d, state, inc);
-  __stcs(&q_o[p], make_float4(o.x, o.y, o.z, __int_as_float((int32_t)p)));
+  (void)q_o;  // a primary ray's origin is the camera and its path id its slot
   __stcs(&q_d[p], make_float4(d.x, d.y, d.z, ra.t_min));
 }
 
@@ -273,7 +274,7 @@ template <bool COUNT>
 __global__ void __launch_bounds__(kTraceThreads, LT_TRACE_MIN_BLOCKS)
     k_trace(SceneView sc, const float4 *__restrict__ q_o, const float4 *__restrict__ q_d,
             const int32_t *__restrict__ count, int32_t *__restrict__ fetch,
-            float4 *__restrict__ hits, unsigned long long *__restrict__ ray_ctr) {
+            float4 *__restrict__ hits, unsigned long long *__restrict__ ray_ctr, float4 cam_o) {
   extern __shared__ float4 s_mem[];
   const int tid = threadIdx.x;
   const int lane = tid & 31;
@@ -310,7 +311,8 @@ __global__ void __launch_bounds__(kTraceThreads, LT_TRACE_MIN_BLOCKS)
         const int r = base + __popc(idle & lanes_below);
         if (r < n) {
           q = r;
-          const float4 ro = __ldcs(&q_o[r]);
+          // (primary rays, q_o NULL: the origin is the camera)
+          const float4 ro = q_o ? __ldcs(&q_o[r]) : cam_o;
           const float4 rd = __ldcs(&q_d[r]);
           t_min = rd.w;
           rs = ray_slab(mk(ro.x, ro.y, ro.z), mk(rd.x, rd.y, rd.z));
@@ -474,7 +476,9 @@ __global__ void __launch_bounds__(kShadeThreads, LT_SHADE_MIN_BLOCKS)
         // the ray record (regenerating the float64 camera ray here instead
         // measured slower: +17 % instructions on an issue-bound launch,
         // profiles/r01_v13_ncu_shade.txt)
-        const float4 ro = __ldcs(&q_o[q]);
+        const float4 ro = primary ? make_float4((float)ra.cam[0], (float)ra.cam[1],
+                                                (float)ra.cam[2], __int_as_float(q))
+                                  : __ldcs(&q_o[q]);
         const float4 rd = __ldcs(&q_d[q]);
         p = __float_as_int(ro.w);
         LT_ASSERT(p >= 0 && p < sa.cap);
@@ -1172,7 +1176,7 @@ size_t trace_smem_bytes() { return (size_t)kShortStack * kTraceThreads * 8; }
 cudaError_t launch_trace(const SceneView &sc, bool count_work, int grid,
                          const cudaAccessPolicyWindow *window, const float4 *q_o,
                          const float4 *q_d, const int32_t *count, int32_t *fetch, float4 *hits,
-                         unsigned long long *ray_ctr, cudaStream_t st) {
+                         unsigned long long *ray_ctr, float4 cam_o, cudaStream_t st) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kTraceThreads);
@@ -1186,8 +1190,10 @@ cudaError_t launch_trace(const SceneView &sc, bool count_work, int grid,
     cfg.numAttrs = 1;
   }
   if (count_work)
-    return cudaLaunchKernelEx(&cfg, k_trace<true>, sc, q_o, q_d, count, fetch, hits, ray_ctr);
-  return cudaLaunchKernelEx(&cfg, k_trace<false>, sc, q_o, q_d, count, fetch, hits, ray_ctr);
+    return cudaLaunchKernelEx(&cfg, k_trace<true>, sc, q_o, q_d, count, fetch, hits, ray_ctr,
+                              cam_o);
+  return cudaLaunchKernelEx(&cfg, k_trace<false>, sc, q_o, q_d, count, fetch, hits, ray_ctr,
+                            cam_o);
 }
 
 void launch_trace_rays(const SceneView &sc, const float4 *q_o, const float4 *q_d, int64_t n,

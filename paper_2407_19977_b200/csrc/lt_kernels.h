@@ -96,10 +96,11 @@ void launch_raygen_explicit(const double *o, const double *d, const uint64_t *st
 void launch_gather_explicit(const PathArrays &pa, int64_t n, double *rgb, uint64_t *state_out,
                             cudaStream_t st);
 size_t trace_smem_bytes();
+// q_o NULL: primary rays (origin cam_o.xyz, path id = queue slot)
 cudaError_t launch_trace(const SceneView &sc, bool count_work, int grid,
                          const cudaAccessPolicyWindow *window, const float4 *q_o,
                          const float4 *q_d, const int32_t *count, int32_t *fetch, float4 *hits,
-                         unsigned long long *ray_ctr, cudaStream_t st);
+                         unsigned long long *ray_ctr, float4 cam_o, cudaStream_t st);
 void launch_trace_rays(const SceneView &sc, const float4 *q_o, const float4 *q_d, int64_t n,
                        float4 *hits, int32_t *nodes, int32_t *tests, cudaStream_t st);
 // `ra`: the batch's RaygenArgs (render paths: pixel of a path id, the
