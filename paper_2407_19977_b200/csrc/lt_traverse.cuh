@@ -183,15 +183,18 @@ __device__ __forceinline__ void scale2(float a, float b, float sc, float &ra, fl
   asm("mov.b64 {%0, %1}, %2;" : "=f"(ra), "=f"(rb) : "l"(r));
 }
 
-__device__ __forceinline__ Hits4 visit4o(const float4 *__restrict__ np, const RaySlab &rs,
-                                         float t_min, float t_max) {
+// The four child boxes of a wide node against [t_min, t_max] for one ray:
+// entry distances in node (slot) order, +inf for misses / empty slots, and
+// the node's links.
+__device__ __forceinline__ void visit4_keys(const float4 *__restrict__ np, const RaySlab &rs,
+                                            float t_min, float t_max, float (&key)[4],
+                                            int4 &ln) {
   const float kInf = __int_as_float(0x7f800000);
   float4 nx, fx, ny, fy, nz, fz;
   ldg_pair(np + rs.nx, nx, fx);
   ldg_pair(np + rs.ny, ny, fy);
   ldg_pair(np + rs.nz, nz, fz);
-  const int4 ln = __ldg(reinterpret_cast<const int4 *>(np + LT_NODE_LINKS));
-  Hits4 h;
+  ln = __ldg(reinterpret_cast<const int4 *>(np + LT_NODE_LINKS));
   // sm_100 packed fp32 (FADD2 / FMUL2, one issue slot per two children;
   // the scalar origin / inverse are broadcast operands): same IEEE roundings
   // as the scalar form.
@@ -219,10 +222,22 @@ __device__ __forceinline__ Hits4 visit4o(const float4 *__restrict__ np, const Ra
          LT_SLAB_WIDEN, tf0, tf1);
   scale2(fmin3f(b2x, b2y, fminf(b2z, t_max)), fmin3f(b3x, b3y, fminf(b3z, t_max)),
          LT_SLAB_WIDEN, tf2, tf3);
-  h.k0 = tn0 <= tf0 ? tn0 : kInf;
-  h.k1 = tn1 <= tf1 ? tn1 : kInf;
-  h.k2 = tn2 <= tf2 ? tn2 : kInf;
-  h.k3 = tn3 <= tf3 ? tn3 : kInf;
+  key[0] = tn0 <= tf0 ? tn0 : kInf;
+  key[1] = tn1 <= tf1 ? tn1 : kInf;
+  key[2] = tn2 <= tf2 ? tn2 : kInf;
+  key[3] = tn3 <= tf3 ? tn3 : kInf;
+}
+
+__device__ __forceinline__ Hits4 visit4o(const float4 *__restrict__ np, const RaySlab &rs,
+                                         float t_min, float t_max) {
+  float key[4];
+  int4 ln;
+  visit4_keys(np, rs, t_min, t_max, key, ln);
+  Hits4 h;
+  h.k0 = key[0];
+  h.k1 = key[1];
+  h.k2 = key[2];
+  h.k3 = key[3];
   h.l0 = ln.x;
   h.l1 = ln.y;
   h.l2 = ln.z;
