@@ -34,7 +34,7 @@ CU_SOURCES = ["lt_kernels.cu", "lt_api.cu", "lt_bvh_gpu.cu", "lt_query64.cu"]
 CU_EXTRA = {"lt_bvh_gpu.cu": ["-fmad=false"], "lt_query64.cu": ["-fmad=false"]}
 CPP_SOURCES = ["lt_bvh_build.cpp"]
 HEADERS = ["lt_device.cuh", "lt_material.cuh", "lt_traverse.cuh", "lt_kernels.h",
-           "lt_internal.h"]
+           "lt_internal.h", "lt_staged.h"]
 
 
 def _run(cmd: list[str], log) -> None:

@@ -20,6 +20,7 @@
 
 #include "lt_internal.h"
 #include "lt_kernels.h"
+#include "lt_staged.h"
 
 using namespace lt;
 
@@ -1847,25 +1848,17 @@ extern "C" int lt_bsdf_eval_ext_batch(const double *params, const double *wo, co
   if (n == 0) return LT_OK;
   std::vector<GpuMaterial> mats;
   materials_from_params(params, n, mats);
-  DevBuf dm, da, dfr;
-  RET(dm.ensure(sizeof(GpuMaterial) * n));
-  RET(da.ensure(sizeof(double) * 13 * n));
-  double *dwo = da.as<double>(), *dwi = dwo + 3 * n, *dn = dwi + 3 * n, *df = dn + 3 * n,
-         *dp = df + 3 * n;
-  CK(cudaMemcpy(dm.p, mats.data(), sizeof(GpuMaterial) * n, cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(dwo, wo, 24 * n, cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(dwi, wi, 24 * n, cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(dn, normal, 24 * n, cudaMemcpyHostToDevice));
-  if (front) {
-    RET(dfr.ensure(sizeof(int32_t) * n));
-    CK(cudaMemcpy(dfr.p, front, 4 * n, cudaMemcpyHostToDevice));
-  }
-  launch_bsdf_eval(dm.as<GpuMaterial>(), dwo, dwi, dn, front ? dfr.as<int32_t>() : nullptr, n,
-                   df, dp, 0);
-  CK(cudaGetLastError());
-  CK(cudaMemcpy(f, df, 24 * n, cudaMemcpyDeviceToHost));
-  CK(cudaMemcpy(pdf, dp, 8 * n, cudaMemcpyDeviceToHost));
-  return LT_OK;
+  lt_staged::Staged q;
+  const size_t v3 = 24 * (size_t)n;
+  const int im = q.add(mats.data(), nullptr, sizeof(GpuMaterial) * n);
+  const int io = q.add(wo, nullptr, v3), ii = q.add(wi, nullptr, v3), in = q.add(normal, nullptr, v3);
+  const int ifr = front ? q.add(front, nullptr, 4 * (size_t)n) : -1;
+  const int iff = q.add(nullptr, f, v3), ip = q.add(nullptr, pdf, 8 * (size_t)n);
+  RET(q.begin());
+  launch_bsdf_eval(q.dev<GpuMaterial>(im), q.dev<double>(io), q.dev<double>(ii),
+                   q.dev<double>(in), ifr >= 0 ? q.dev<int32_t>(ifr) : nullptr, n,
+                   q.dev<double>(iff), q.dev<double>(ip), q.stream());
+  return q.finish();
 }
 
 extern "C" int lt_bsdf_eval_batch(const double *params, const double *wo, const double *wi,
@@ -1881,24 +1874,18 @@ extern "C" int lt_bsdf_sample_batch(const double *params, const double *wo, cons
   if (n == 0) return LT_OK;
   std::vector<GpuMaterial> mats;
   materials_from_params(params, n, mats);
-  DevBuf dm, da, di;
-  RET(dm.ensure(sizeof(GpuMaterial) * n));
-  RET(da.ensure(sizeof(double) * 15 * n));
-  RET(di.ensure(sizeof(int32_t) * 2 * n));
-  double *dwo = da.as<double>(), *dn = dwo + 3 * n, *du = dn + 3 * n, *dwi = du + 3 * n,
-         *dw = dwi + 3 * n;
-  int32_t *dok = di.as<int32_t>(), *dfr = dok + n;
-  CK(cudaMemcpy(dm.p, mats.data(), sizeof(GpuMaterial) * n, cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(dwo, wo, 24 * n, cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(dn, normal, 24 * n, cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(du, u, 24 * n, cudaMemcpyHostToDevice));
-  if (front) CK(cudaMemcpy(dfr, front, 4 * n, cudaMemcpyHostToDevice));
-  launch_bsdf_sample(dm.as<GpuMaterial>(), dwo, dn, du, front ? dfr : nullptr, n, dok, dwi, dw, 0);
-  CK(cudaGetLastError());
-  CK(cudaMemcpy(ok, dok, 4 * n, cudaMemcpyDeviceToHost));
-  CK(cudaMemcpy(wi, dwi, 24 * n, cudaMemcpyDeviceToHost));
-  CK(cudaMemcpy(weight, dw, 24 * n, cudaMemcpyDeviceToHost));
-  return LT_OK;
+  lt_staged::Staged q;
+  const size_t v3 = 24 * (size_t)n;
+  const int im = q.add(mats.data(), nullptr, sizeof(GpuMaterial) * n);
+  const int io = q.add(wo, nullptr, v3), in = q.add(normal, nullptr, v3), iu = q.add(u, nullptr, v3);
+  const int ifr = front ? q.add(front, nullptr, 4 * (size_t)n) : -1;
+  const int iok = q.add(nullptr, ok, 4 * (size_t)n), iwi = q.add(nullptr, wi, v3);
+  const int iw = q.add(nullptr, weight, v3);
+  RET(q.begin());
+  launch_bsdf_sample(q.dev<GpuMaterial>(im), q.dev<double>(io), q.dev<double>(in),
+                     q.dev<double>(iu), ifr >= 0 ? q.dev<int32_t>(ifr) : nullptr, n,
+                     q.dev<int32_t>(iok), q.dev<double>(iwi), q.dev<double>(iw), q.stream());
+  return q.finish();
 }
 
 extern "C" int lt_occluded_batch_host(lt_scene *s, const double *origins, const double *dirs,

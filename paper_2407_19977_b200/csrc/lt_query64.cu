@@ -531,7 +531,8 @@ void launch_display64(int op, const double *in, int64_t n, double *out, uint8_t 
 // ------------------------------------------------------------------ C-ABI
 // Host-buffer entry points (include/luxb200.h).  Every call stages its
 // arrays through one per-device scratch buffer (grow-only, serialized by a
-// mutex) and runs on the legacy default stream, synchronously.
+// mutex) and runs synchronously on a per-device non-blocking stream, so a
+// query never waits for (or blocks) render work on other streams.
 
 #include <cuda_runtime.h>
 
@@ -540,88 +541,10 @@ void launch_display64(int op, const double *in, int64_t n, double *out, uint8_t 
 
 #include "lt_internal.h"
 
-namespace {
-
-struct Scratch {
-  std::mutex mu;
-  void *p = nullptr;
-  size_t bytes = 0;
-};
-
-Scratch &scratch_for(int dev) {
-  static std::mutex g_mu;
-  static std::vector<Scratch *> g;
-  std::lock_guard<std::mutex> lk(g_mu);
-  if ((int)g.size() <= dev) g.resize(dev + 1, nullptr);
-  if (!g[dev]) g[dev] = new Scratch();  // process lifetime
-  return *g[dev];
-}
-
-// One staged call: inputs are copied in, outputs copied back after the
-// kernel; `add` returns the device pointer of each array.
-struct Staged {
-  struct Arr {
-    const void *in;
-    void *out;
-    size_t bytes, off;
-  };
-  std::vector<Arr> arrs;
-  size_t total = 0;
-  Scratch *sc = nullptr;
-  std::unique_lock<std::mutex> lk;
-  int add(const void *in, void *out, size_t bytes) {
-    arrs.push_back(Arr{in, out, bytes, total});
-    total += (bytes + 255) / 256 * 256;
-    return (int)arrs.size() - 1;
-  }
-  int begin() {
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess) return lt_fail(LT_ERR_CUDA, "no CUDA device");
-    sc = &scratch_for(dev);
-    lk = std::unique_lock<std::mutex>(sc->mu);
-    if (sc->bytes < total) {
-      if (sc->p) cudaFree(sc->p);
-      sc->p = nullptr;
-      sc->bytes = 0;
-      const cudaError_t e = cudaMalloc(&sc->p, std::max<size_t>(total, 1 << 20));
-      if (e != cudaSuccess)
-        return lt_fail(LT_ERR_NOMEM, "query scratch: %s", cudaGetErrorString(e));
-      sc->bytes = std::max<size_t>(total, 1 << 20);
-    }
-    for (const Arr &a : arrs)
-      if (a.in && a.bytes) {
-        const cudaError_t e = cudaMemcpy(ptr(a), a.in, a.bytes, cudaMemcpyHostToDevice);
-        if (e != cudaSuccess) return lt_fail(LT_ERR_CUDA, "query upload: %s", cudaGetErrorString(e));
-      }
-    return LT_OK;
-  }
-  char *ptr(const Arr &a) const { return static_cast<char *>(sc->p) + a.off; }
-  template <class T>
-  T *dev(int i) const {
-    return reinterpret_cast<T *>(ptr(arrs[i]));
-  }
-  int finish() {
-    cudaError_t e = cudaGetLastError();
-    if (e == cudaSuccess) e = cudaDeviceSynchronize();
-    if (e != cudaSuccess) return lt_fail(LT_ERR_CUDA, "query kernel: %s", cudaGetErrorString(e));
-    for (const Arr &a : arrs)
-      if (a.out && a.bytes) {
-        e = cudaMemcpy(a.out, ptr(a), a.bytes, cudaMemcpyDeviceToHost);
-        if (e != cudaSuccess) return lt_fail(LT_ERR_CUDA, "query download: %s", cudaGetErrorString(e));
-      }
-    return LT_OK;
-  }
-};
-
-#define Q_RET(expr)             \
-  do {                          \
-    const int r_ = (expr);      \
-    if (r_ != LT_OK) return r_; \
-  } while (0)
-
-}  // namespace
+#include "lt_staged.h"
 
 using namespace lt;
+using lt_staged::Staged;
 
 extern "C" int lt_ray_triangle_batch(const double *origins, const double *dirs,
                                      const double *t_min, const double *t_max, const double *v0,
@@ -649,7 +572,7 @@ extern "C" int lt_ray_triangle_batch(const double *origins, const double *dirs,
                         s.dev<double>(i1), s.dev<double>(iv[0]), s.dev<double>(iv[1]),
                         s.dev<double>(iv[2]), s.dev<double>(iv[3]), s.dev<double>(iv[4]),
                         s.dev<double>(iv[5]), n, s.dev<int32_t>(iok), s.dev<double>(it),
-                        s.dev<double>(ig), s.dev<double>(isn), s.dev<int32_t>(ifr), 0);
+                        s.dev<double>(ig), s.dev<double>(isn), s.dev<int32_t>(ifr), s.stream());
   return s.finish();
 }
 
@@ -675,7 +598,7 @@ extern "C" int lt_hit_frame_batch(const double *dirs, const double *v0, const do
   launch_hit_frame64(s.dev<double>(id), s.dev<double>(iv[0]), s.dev<double>(iv[1]),
                      s.dev<double>(iv[2]), s.dev<double>(iv[3]), s.dev<double>(iv[4]),
                      s.dev<double>(iv[5]), s.dev<double>(iuv), n, s.dev<double>(ig),
-                     s.dev<double>(isn), s.dev<int32_t>(ifr), 0);
+                     s.dev<double>(isn), s.dev<int32_t>(ifr), s.stream());
   return s.finish();
 }
 
@@ -696,7 +619,7 @@ extern "C" int lt_ray_aabb_batch(const double *origins, const double *dirs, cons
   Q_RET(s.begin());
   launch_ray_aabb64(s.dev<double>(io), s.dev<double>(id), s.dev<double>(i0), s.dev<double>(i1),
                     s.dev<double>(il), s.dev<double>(ih), n, s.dev<int32_t>(iok),
-                    s.dev<double>(it), 0);
+                    s.dev<double>(it), s.stream());
   return s.finish();
 }
 
@@ -712,7 +635,8 @@ extern "C" int lt_bsdf64_eval_batch(const double *params, const double *wo, cons
   const int iff = s.add(nullptr, f, v3), ipdf = s.add(nullptr, pdf, 8 * n);
   Q_RET(s.begin());
   launch_bsdf64(0, s.dev<double>(ip), s.dev<double>(io), s.dev<double>(ii), s.dev<double>(in),
-                nullptr, n, nullptr, s.dev<double>(iff), nullptr, s.dev<double>(ipdf), nullptr, 0);
+                nullptr, n, nullptr, s.dev<double>(iff), nullptr, s.dev<double>(ipdf), nullptr,
+                s.stream());
   return s.finish();
 }
 
@@ -734,7 +658,7 @@ extern "C" int lt_bsdf64_sample_batch(const double *params, const double *wo,
   Q_RET(s.begin());
   launch_bsdf64(1, s.dev<double>(ip), s.dev<double>(io), nullptr, s.dev<double>(in),
                 s.dev<double>(iu), n, s.dev<int32_t>(iok), s.dev<double>(iwi), s.dev<double>(iw),
-                s.dev<double>(ipdf), s.dev<int32_t>(isp), 0);
+                s.dev<double>(ipdf), s.dev<int32_t>(isp), s.stream());
   return s.finish();
 }
 
@@ -753,7 +677,7 @@ extern "C" int lt_microfacet_batch(int32_t op, const double *a, const double *b,
   Q_RET(s.begin());
   launch_microfacet64(op, s.dev<double>(ia), s.dev<double>(ib),
                       ic >= 0 ? s.dev<double>(ic) : nullptr, in >= 0 ? s.dev<double>(in) : nullptr,
-                      n, s.dev<double>(iout), 0);
+                      n, s.dev<double>(iout), s.stream());
   return s.finish();
 }
 
@@ -768,6 +692,6 @@ extern "C" int lt_display_batch(int32_t op, const double *in, int64_t n, double 
   const int io = op < 3 ? s.add(nullptr, out, 8 * vals) : s.add(nullptr, out_u8, vals);
   Q_RET(s.begin());
   launch_display64(op, s.dev<double>(ii), n, op < 3 ? s.dev<double>(io) : nullptr,
-                   op == 3 ? s.dev<uint8_t>(io) : nullptr, 0);
+                   op == 3 ? s.dev<uint8_t>(io) : nullptr, s.stream());
   return s.finish();
 }
