@@ -155,6 +155,63 @@ int lt_build_bvh_device(int32_t device, const double *v0, const double *v1, cons
 /* ---- scene residency: replaces the per-call `_scene_arrays` packing
  * (integrator.py:284-291); flattens the host BVH into the HBM layout ---- */
 int lt_scene_create(const lt_scene_desc *desc, int32_t device, lt_scene **out);
+
+/* ---- glTF ingest on the device: flatten_scene (scene.py:519-596) fed from
+ * the GLB's own float32 / integer accessors, uploaded as raw bytes (the GLB
+ * stores float32, procgen.py:123) instead of the host's float64 world-space
+ * soup.  The host keeps the cheap part -- JSON, accessor validation, the node
+ * walk and its 4x4 products, material resolution (scene.py:251-490) -- and
+ * hands over one record per primitive and one per (node, primitive)
+ * instance in flatten_scene's visit order.  The device decodes the
+ * accessors, generates smooth normals where NORMAL is absent
+ * (scene.py:493-508: the per-vertex sums in np.add.at's order), applies the
+ * transforms with the rounding numpy's BLAS product uses (one fused
+ * multiply-add chain per output, k = 0, 1, 2), computes the extent, drops
+ * degenerate triangles and normalises the normals -- the reference's
+ * float64 arithmetic step for step, so the arrays are bit-identical to
+ * load_scene's. ---- */
+typedef struct lt_gltf_primitive {
+  /* POSITION: float32 VEC3 at buffers[pos_buffer] + pos_offset, pos_stride bytes apart */
+  int32_t pos_buffer, pos_stride;
+  int64_t pos_offset, n_vertices;
+  /* NORMAL: float32 VEC3; nrm_buffer = -1: none (smooth normals are generated) */
+  int32_t nrm_buffer, nrm_stride;
+  int64_t nrm_offset;
+  /* indices: idx_bytes = 1 / 2 / 4 (u8 / u16 / u32); idx_buffer = -1: 0..n_indices-1 */
+  int32_t idx_buffer, idx_stride, idx_bytes, reserved;
+  int64_t idx_offset, n_indices;  /* n_indices % 3 == 0, every index < n_vertices */
+} lt_gltf_primitive;
+
+typedef struct lt_gltf_instance {
+  int32_t primitive, material;    /* material: slot in the scene's material table */
+  double linear[9];               /* world[:3, :3], row-major */
+  double translation[3];          /* world[:3, 3] */
+  double normal_matrix[9];        /* np.linalg.inv(linear).T, row-major */
+} lt_gltf_instance;
+
+typedef struct lt_gltf_desc {
+  int32_t n_buffers;
+  const uint8_t *const *buffers;  /* host bytes of each glTF buffer */
+  const int64_t *buffer_bytes;
+  int32_t n_primitives;
+  const lt_gltf_primitive *primitives;
+  int32_t n_instances;
+  const lt_gltf_instance *instances;
+} lt_gltf_desc;
+
+/* flatten_scene on `device` with the arrays copied back: v0..n2 (cap,3)
+ * float64 and material_index (cap,), cap >= the instances' total triangle
+ * count; *n_kept / *n_dropped as SceneDescription.degenerate_dropped.  An
+ * all-degenerate scene returns LT_ERR_INVALID "empty scene". */
+int lt_gltf_flatten(const lt_gltf_desc *gltf, int32_t device, int64_t cap, double *v0,
+                    double *v1, double *v2, double *n0, double *n1, double *n2,
+                    int32_t *material_index, int64_t *n_kept, int64_t *n_dropped);
+/* the same flatten feeding lt_scene_create without leaving the device: the
+ * triangle arrays never exist on the host, the BVH is built on the device.
+ * `scene` supplies the materials and environment; its triangle and BVH
+ * fields must be 0 / NULL. */
+int lt_scene_create_gltf(const lt_gltf_desc *gltf, const lt_scene_desc *scene, int32_t device,
+                         lt_scene **out, int64_t *n_kept, int64_t *n_dropped);
 int lt_scene_destroy(lt_scene *scene);
 int lt_scene_info_get(const lt_scene *scene, lt_scene_info *info);
 

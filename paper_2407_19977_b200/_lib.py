@@ -98,6 +98,34 @@ class RenderStats(C.Structure):
     ]
 
 
+class GltfPrimitive(C.Structure):
+    _fields_ = [
+        ("pos_buffer", C.c_int32), ("pos_stride", C.c_int32),
+        ("pos_offset", C.c_int64), ("n_vertices", C.c_int64),
+        ("nrm_buffer", C.c_int32), ("nrm_stride", C.c_int32),
+        ("nrm_offset", C.c_int64),
+        ("idx_buffer", C.c_int32), ("idx_stride", C.c_int32), ("idx_bytes", C.c_int32),
+        ("reserved", C.c_int32),
+        ("idx_offset", C.c_int64), ("n_indices", C.c_int64),
+    ]
+
+
+class GltfInstance(C.Structure):
+    _fields_ = [
+        ("primitive", C.c_int32), ("material", C.c_int32),
+        ("linear", C.c_double * 9), ("translation", C.c_double * 3),
+        ("normal_matrix", C.c_double * 9),
+    ]
+
+
+class GltfDesc(C.Structure):
+    _fields_ = [
+        ("n_buffers", C.c_int32), ("buffers", C.POINTER(_u8p)), ("buffer_bytes", _lp),
+        ("n_primitives", C.c_int32), ("primitives", C.POINTER(GltfPrimitive)),
+        ("n_instances", C.c_int32), ("instances", C.POINTER(GltfInstance)),
+    ]
+
+
 # (name, restype, argtypes) for every symbol the header declares
 SIGNATURES = {
     "lt_abi_version": (C.c_int, []),
@@ -108,6 +136,10 @@ SIGNATURES = {
     "lt_build_bvh_device": (C.c_int, [C.c_int32, _dp, _dp, _dp, C.c_int64, C.c_int32, C.c_int32,
                                       _dp, _dp, _ip, _ip, _ip, _ip, _ip, _lp, _lp, _lp]),
     "lt_scene_create": (C.c_int, [C.POINTER(SceneDesc), C.c_int32, C.POINTER(C.c_void_p)]),
+    "lt_scene_create_gltf": (C.c_int, [C.POINTER(GltfDesc), C.POINTER(SceneDesc), C.c_int32,
+                                       C.POINTER(C.c_void_p), _lp, _lp]),
+    "lt_gltf_flatten": (C.c_int, [C.POINTER(GltfDesc), C.c_int32, C.c_int64, _dp, _dp, _dp, _dp,
+                                  _dp, _dp, _ip, _lp, _lp]),
     "lt_scene_destroy": (C.c_int, [C.c_void_p]),
     "lt_scene_info_get": (C.c_int, [C.c_void_p, C.POINTER(SceneInfo)]),
     "lt_intersect_batch": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_float,

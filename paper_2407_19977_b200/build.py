@@ -27,11 +27,13 @@ NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas"
 CXX_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-fno-fast-math", "-Wall",
              f"-I{INCLUDE}", f"-I{CSRC}"]
 
-CU_SOURCES = ["lt_kernels.cu", "lt_api.cu", "lt_bvh_gpu.cu", "lt_query64.cu"]
+CU_SOURCES = ["lt_kernels.cu", "lt_api.cu", "lt_bvh_gpu.cu", "lt_query64.cu", "lt_ingest.cu"]
 # per-source extra nvcc flags: the BVH build must round every float64 operation
 # like the reference (no FMA contraction)
-# (and the float64 query kernels reproduce the reference's roundings)
-CU_EXTRA = {"lt_bvh_gpu.cu": ["-fmad=false"], "lt_query64.cu": ["-fmad=false"]}
+# (and the float64 query kernels and the glTF flatten reproduce the
+# reference's roundings)
+CU_EXTRA = {"lt_bvh_gpu.cu": ["-fmad=false"], "lt_query64.cu": ["-fmad=false"],
+            "lt_ingest.cu": ["-fmad=false"]}
 CPP_SOURCES = ["lt_bvh_build.cpp"]
 HEADERS = ["lt_device.cuh", "lt_material.cuh", "lt_traverse.cuh", "lt_kernels.h",
            "lt_internal.h", "lt_staged.h"]

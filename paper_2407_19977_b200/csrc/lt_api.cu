@@ -506,6 +506,20 @@ static void parallel_for(int64_t n, F f) {
   for (auto &x : th) x.join();
 }
 
+// materials + environment of a description (all creation paths)
+static int validate_shading(const lt_scene_desc *d) {
+  if (d->n_materials < 1 || !d->base_weight || !d->base_color || !d->base_metalness ||
+      !d->specular_weight || !d->specular_color || !d->specular_roughness ||
+      !d->specular_ior || !d->emission_luminance || !d->emission_color)
+    return lt_fail(LT_ERR_INVALID, "material arrays must be non-null");
+  if (d->env_kind < LT_ENV_UNIFORM || d->env_kind > LT_ENV_LATLONG)
+    return lt_fail(LT_ERR_INVALID, "unknown environment kind %d", d->env_kind);
+  if (d->env_kind == LT_ENV_LATLONG &&
+      (!d->env_texels || d->env_width < 1 || d->env_height < 1))
+    return lt_fail(LT_ERR_INVALID, "lat-long environment needs texels and a size");
+  return LT_OK;
+}
+
 static int validate_desc(const lt_scene_desc *d) {
   if (!d) return lt_fail(LT_ERR_INVALID, "null scene description");
   if (d->n_triangles < 1) return lt_fail(LT_ERR_INVALID, "empty scene");
@@ -522,16 +536,7 @@ static int validate_desc(const lt_scene_desc *d) {
                       !d->right_child || !d->first_triangle || !d->triangle_count ||
                       !d->triangle_order))
     return lt_fail(LT_ERR_INVALID, "bvh arrays must be non-null");
-  if (d->n_materials < 1 || !d->base_weight || !d->base_color || !d->base_metalness ||
-      !d->specular_weight || !d->specular_color || !d->specular_roughness ||
-      !d->specular_ior || !d->emission_luminance || !d->emission_color)
-    return lt_fail(LT_ERR_INVALID, "material arrays must be non-null");
-  if (d->env_kind < LT_ENV_UNIFORM || d->env_kind > LT_ENV_LATLONG)
-    return lt_fail(LT_ERR_INVALID, "unknown environment kind %d", d->env_kind);
-  if (d->env_kind == LT_ENV_LATLONG &&
-      (!d->env_texels || d->env_width < 1 || d->env_height < 1))
-    return lt_fail(LT_ERR_INVALID, "lat-long environment needs texels and a size");
-  return LT_OK;
+  return validate_shading(d);
 }
 
 // The O(n) index checks of a description (material indices, triangle
@@ -847,7 +852,12 @@ static int device_layout(lt_scene *s, const double *bmin, const double *bmax,
   return LT_OK;
 }
 
-static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s) {
+// gltf != NULL: the triangle arrays come from lt_ingest_run on the scene's
+// stream (the description's triangle / BVH fields are unused), the BVH is
+// built on the device
+static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s,
+                             const lt_gltf_desc *gltf = nullptr, int64_t *n_kept = nullptr,
+                             int64_t *n_dropped = nullptr) {
   PhaseTimer pt;
   s->device = device;
   CK(cudaSetDevice(device));
@@ -882,13 +892,12 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
     b->ast = s->stream;
   }
   cudaStream_t st = s->stream;
-  const int64_t n = d->n_triangles;
+  int64_t n = d->n_triangles;
   // no host BVH (n_nodes == 0): build the reference's tree (leaf size 4, 12
   // bins, build_bvh's defaults) on the device from the uploaded vertices and
   // lay it out without a host round trip
-  const bool build_here = d->n_nodes == 0;
-  int64_t nn = d->n_nodes;
-  s->n_tris = n;
+  const bool build_here = gltf || d->n_nodes == 0;
+  int64_t nn = gltf ? 0 : d->n_nodes;
   pt.mark("stream + attributes");
 
   // --- uploads.  Small scenes: every array through one pinned staging
@@ -910,9 +919,41 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
   int32_t root_first;
   double root_lo[3], root_hi[3];
   const size_t kSmallUpload = size_t(4) << 20;
-  TmpBuf t_all;
+  TmpBuf t_all, t_raw;
   Workspace &W = *s->ws;
   std::unique_lock<std::mutex> create_lk(W.create_mu);
+  // --- glTF ingest: the buffers' raw bytes up (through the pinned ring),
+  // flatten_scene on the device; its output stands in for the uploads below
+  struct IngestGuard {
+    lt_ingest_out o{};
+    cudaStream_t st;
+    ~IngestGuard() { lt_ingest_free(&o, st); }  // stream-ordered, after the flatten reads it
+  } ing{{}, st};
+  if (gltf) {
+    std::vector<int64_t> at(std::max<int32_t>(1, gltf->n_buffers));
+    size_t raw_total = 0;
+    for (int32_t b = 0; b < gltf->n_buffers; ++b) {
+      at[b] = (int64_t)raw_total;
+      raw_total += ((size_t)gltf->buffer_bytes[b] + 255) / 256 * 256;
+    }
+    RET(t_raw.alloc(raw_total, st));
+    std::vector<CopyItem> raw_items;
+    for (int32_t b = 0; b < gltf->n_buffers; ++b)
+      if (gltf->buffer_bytes[b] > 0)
+        raw_items.push_back(CopyItem{t_raw.as<char>() + at[b], gltf->buffers[b],
+                                     (size_t)gltf->buffer_bytes[b]});
+    RET(ensure_ring(W));
+    RET(staged_h2d(W, device, raw_items, st));
+    pt.mark("glTF buffers staged");
+    RET(lt_ingest_run(gltf, t_raw.as<uint8_t>(), at.data(), st, &ing.o));
+    pt.mark("device flatten_scene");
+    n = ing.o.n_kept;
+    if (n_kept) *n_kept = ing.o.n_kept;
+    if (n_dropped) *n_dropped = ing.o.n_dropped;
+    for (int k = 0; k < 6; ++k) t_v[k].set_view(ing.o.v[k]);
+    t_mat.set_view(ing.o.mat);
+  }
+  s->n_tris = n;
   struct Item {
     TmpBuf *dst;
     const void *src;
@@ -920,8 +961,10 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
     bool tri;  // a triangle array (uploaded after the BVH arrays)
   };
   std::vector<Item> items;
-  for (int k = 0; k < 6; ++k) items.push_back({&t_v[k], src[k], 24 * (size_t)n, true});
-  items.push_back({&t_mat, d->material_index, 4 * (size_t)n, true});
+  if (!gltf) {
+    for (int k = 0; k < 6; ++k) items.push_back({&t_v[k], src[k], 24 * (size_t)n, true});
+    items.push_back({&t_mat, d->material_index, 4 * (size_t)n, true});
+  }
   if (!build_here) {
     items.push_back({&t_order, d->triangle_order, 4 * (size_t)n, false});
     items.push_back({&t_bmin, d->bounds_min, 24 * (size_t)nn, false});
@@ -939,7 +982,9 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
   }
   const bool small_upload = total <= kSmallUpload;
   char *base = nullptr;
-  if (small_upload) {
+  if (total == 0) {
+    // (glTF ingest: nothing to upload)
+  } else if (small_upload) {
     RET(t_all.alloc(total, st));
     std::lock_guard<std::mutex> lk(W.upload_mu);
     if (W.stage_ev)
@@ -1071,7 +1116,7 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
   }
   // index checks on host threads while the DMA runs; nothing on the device
   // has read an index yet (the device build reads only vertices)
-  if (int rc = validate_indices(d)) {
+  if (int rc = gltf ? LT_OK : validate_indices(d)) {
     join_triangles();
     cudaStreamSynchronize(st);
     if (W.upload_st) cudaStreamSynchronize(W.upload_st);
@@ -1225,6 +1270,82 @@ extern "C" int lt_scene_create(const lt_scene_desc *desc, int32_t device, lt_sce
     return rc;
   }
   *out = s;
+  return LT_OK;
+}
+
+static int check_device(int32_t device) {
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return lt_fail(LT_ERR_CUDA, "no CUDA device available");
+  if (device < 0 || device >= ndev)
+    return lt_fail(LT_ERR_INVALID, "device %d out of range [0, %d)", device, ndev);
+  return LT_OK;
+}
+
+extern "C" int lt_scene_create_gltf(const lt_gltf_desc *gltf, const lt_scene_desc *desc,
+                                    int32_t device, lt_scene **out, int64_t *n_kept,
+                                    int64_t *n_dropped) {
+  if (!out) return lt_fail(LT_ERR_INVALID, "null output handle");
+  *out = nullptr;
+  if (!desc) return lt_fail(LT_ERR_INVALID, "null scene description");
+  if (desc->n_triangles != 0 || desc->n_nodes != 0 || desc->v0 || desc->material_index ||
+      desc->bounds_min || desc->triangle_order)
+    return lt_fail(LT_ERR_INVALID, "lt_scene_create_gltf: triangle and BVH fields must be empty");
+  RET(validate_shading(desc));
+  int64_t n_tris = 0;
+  RET(lt_ingest_check(gltf, desc->n_materials, &n_tris));
+  if (n_tris == 0) return lt_fail(LT_ERR_INVALID, "empty scene");
+  RET(check_device(device));
+  DeviceGuard g(device);
+  lt_scene *s = new lt_scene();
+  int rc = scene_create_impl(desc, device, s, gltf, n_kept, n_dropped);
+  if (rc != LT_OK) {
+    std::string msg = g_last_error;
+    destroy_scene(s);
+    g_last_error = msg;
+    return rc;
+  }
+  *out = s;
+  return LT_OK;
+}
+
+extern "C" int lt_gltf_flatten(const lt_gltf_desc *gltf, int32_t device, int64_t cap, double *v0,
+                               double *v1, double *v2, double *n0, double *n1, double *n2,
+                               int32_t *material_index, int64_t *n_kept, int64_t *n_dropped) {
+  int64_t n_tris = 0;
+  RET(lt_ingest_check(gltf, 0, &n_tris));
+  if (n_tris == 0) return lt_fail(LT_ERR_INVALID, "empty scene");
+  if (cap < n_tris) return lt_fail(LT_ERR_INVALID, "capacity %lld < %lld triangles",
+                                   (long long)cap, (long long)n_tris);
+  if (!v0 || !v1 || !v2 || !n0 || !n1 || !n2 || !material_index || !n_kept || !n_dropped)
+    return lt_fail(LT_ERR_INVALID, "output arrays must be non-null");
+  RET(check_device(device));
+  DeviceGuard g(device);
+  // one upload, kernels and download on the query stream, serialized by its
+  // scratch (lt_staged.h) for the raw bytes
+  lt_staged::Staged S;
+  std::vector<int> ids(std::max<int32_t>(1, gltf->n_buffers));
+  for (int32_t b = 0; b < gltf->n_buffers; ++b)
+    ids[b] = S.add(gltf->buffers[b], nullptr, (size_t)gltf->buffer_bytes[b]);
+  RET(S.begin());
+  std::vector<int64_t> at(ids.size(), 0);
+  const char *base = S.dev<char>(0);
+  for (int32_t b = 0; b < gltf->n_buffers; ++b) at[b] = S.dev<char>(ids[b]) - base;
+  struct Guard {
+    lt_ingest_out o{};
+    cudaStream_t st;
+    ~Guard() { lt_ingest_free(&o, st); }
+  } ing{{}, S.stream()};
+  RET(lt_ingest_run(gltf, reinterpret_cast<const uint8_t *>(base), at.data(), S.stream(), &ing.o));
+  const int64_t k = ing.o.n_kept;
+  double *dst[6] = {v0, v1, v2, n0, n1, n2};
+  for (int a = 0; a < 6; ++a)
+    CK(cudaMemcpyAsync(dst[a], ing.o.v[a], 24 * (size_t)k, cudaMemcpyDeviceToHost, S.stream()));
+  CK(cudaMemcpyAsync(material_index, ing.o.mat, 4 * (size_t)k, cudaMemcpyDeviceToHost,
+                     S.stream()));
+  CK(cudaStreamSynchronize(S.stream()));
+  *n_kept = k;
+  *n_dropped = ing.o.n_dropped;
   return LT_OK;
 }
 

@@ -27,3 +27,20 @@ struct lt_gpu_tree {
 int lt_gpu_tree_build(const double *dv0, const double *dv1, const double *dv2, int64_t n,
                       int32_t leaf_size, int32_t bins, void *stream, lt_gpu_tree *out);
 void lt_gpu_tree_free(lt_gpu_tree *t);
+
+// glTF ingest on the device (lt_ingest.cu): flatten_scene's triangle soup in
+// one stream-ordered allocation `mem` (v[0..5] (n_kept,3) float64, mat).
+struct lt_ingest_out {
+  double *v[6];
+  int32_t *mat;
+  int64_t n_total, n_kept, n_dropped;
+  void *mem;
+};
+// Structural checks of a description (ranges inside their buffers, ids,
+// counts); n_materials <= 0 skips the material-slot check.  *n_out_tris =
+// the instances' total triangle count.
+int lt_ingest_check(const lt_gltf_desc *g, int32_t n_materials, int64_t *n_out_tris);
+// d_raw: the glTF buffers on the device, buffer b at d_raw + buf_at[b].
+int lt_ingest_run(const lt_gltf_desc *g, const uint8_t *d_raw, const int64_t *buf_at,
+                  void *stream, lt_ingest_out *out);
+void lt_ingest_free(lt_ingest_out *o, void *stream);

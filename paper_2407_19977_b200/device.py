@@ -29,6 +29,31 @@ def _c32(a) -> np.ndarray:
     return np.ascontiguousarray(a, dtype=np.int32)
 
 
+def _shading_desc(d, materials, environment, keep) -> int:
+    """Material table + environment fields of an lt_scene_desc; returns the
+    material count."""
+    def p64(a):
+        arr = _c64(a)
+        keep.append(arr)
+        return arr.ctypes.data_as(C.POINTER(C.c_double))
+
+    table = pack_material_table(materials)
+    d.n_materials = len(table["base_weight"])
+    for name, arr in table.items():
+        setattr(d, name, p64(arr))
+    kind, a, b = environment_pack(environment)
+    d.env_kind = kind
+    d.env_a[:] = [float(x) for x in a]
+    d.env_b[:] = [float(x) for x in b]
+    if kind == _lib.LT_ENV_LATLONG:
+        tex = np.ascontiguousarray(environment.texels, dtype=np.float32)
+        keep.append(tex)
+        d.env_height, d.env_width = int(tex.shape[0]), int(tex.shape[1])
+        d.env_texels = tex.ctypes.data_as(C.POINTER(C.c_float))
+        d.env_scale = float(environment.scale)
+    return d.n_materials
+
+
 class DeviceScene:
     """Owns one lt_scene on one GPU.  Not thread-safe; one per device."""
 
@@ -83,25 +108,38 @@ class DeviceScene:
             d.first_triangle = p32(bvh.first_triangle)
             d.triangle_count = p32(bvh.triangle_count)
             d.triangle_order = p32(bvh.triangle_order)
-        table = pack_material_table(materials)
-        self.n_materials = len(table["base_weight"])
-        d.n_materials = self.n_materials
-        for name, arr in table.items():
-            setattr(d, name, p64(arr))
-        kind, a, b = environment_pack(environment)
-        d.env_kind = kind
-        d.env_a[:] = [float(x) for x in a]
-        d.env_b[:] = [float(x) for x in b]
-        if kind == _lib.LT_ENV_LATLONG:
-            tex = np.ascontiguousarray(environment.texels, dtype=np.float32)
-            keep.append(tex)
-            d.env_height, d.env_width = int(tex.shape[0]), int(tex.shape[1])
-            d.env_texels = tex.ctypes.data_as(C.POINTER(C.c_float))
-            d.env_scale = float(environment.scale)
+        self.n_materials = _shading_desc(d, materials, environment, keep)
         handle = C.c_void_p()
         t0 = time.perf_counter()
         _lib.check(_lib.lib().lt_scene_create(C.byref(d), int(device), C.byref(handle)))
         self.create_ms = (time.perf_counter() - t0) * 1e3
+        self._adopt(handle, device, n)
+
+    @classmethod
+    def from_gltf(cls, gltf, keep, materials, environment, camera, device: int = 0):
+        """Scene from a glTF description (`_lib.GltfDesc`, whose arrays `keep`
+        holds alive) flattened on the device by lt_scene_create_gltf: the
+        triangle soup never exists on the host.  Sets `degenerate_dropped`."""
+        _lib.require_gpu()
+        self = cls.__new__(cls)
+        self.handle = None
+        self.bvh = None
+        d = _lib.SceneDesc()
+        keep = list(keep)
+        self.n_materials = _shading_desc(d, materials, environment, keep)
+        handle = C.c_void_p()
+        kept, dropped = C.c_int64(0), C.c_int64(0)
+        t0 = time.perf_counter()
+        _lib.check(_lib.lib().lt_scene_create_gltf(C.byref(gltf), C.byref(d), int(device),
+                                                   C.byref(handle), C.byref(kept),
+                                                   C.byref(dropped)))
+        self.create_ms = (time.perf_counter() - t0) * 1e3
+        self._adopt(handle, device, kept.value)
+        self.degenerate_dropped = dropped.value
+        self.camera = camera
+        return self
+
+    def _adopt(self, handle, device, n) -> None:
         self.handle = handle
         self.device = int(device)
         self.n_triangles = n

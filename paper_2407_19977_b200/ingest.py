@@ -6,12 +6,22 @@ float64 triangle arrays bit for bit (the world transform, smooth normals,
 degenerate filter and normalisation are the same numpy operations in the
 same order) and the same `SceneError` messages.
 
-Host code: ingest produces the arrays `DeviceScene` uploads; the GPU work
-starts at `lt_scene_create`.
+Two ways to the device:
+  * `load_scene` (host, numpy) -> SceneDescription -> `DeviceScene` uploads
+    the float64 soup (the reference's path);
+  * `load_device_scene` / `load_scene_gpu` (lt_ingest.cu): the host parses
+    the JSON, validates the accessors and walks the nodes (cheap); the GLB's
+    raw float32 / integer bytes are uploaded once and the device decodes
+    them, generates smooth normals, applies the transforms, filters
+    degenerates and normalises -- the same float64 arithmetic in the same
+    order, so the arrays equal load_scene's bit for bit -- and (for
+    load_device_scene) builds the BVH and the render layout without the
+    soup ever reaching the host.
 """
 from __future__ import annotations
 
 import base64
+import contextlib
 import json
 import math
 import struct
@@ -252,8 +262,8 @@ class _GltfReader:
         acc = self.doc.get("accessors", [])
         return acc[idx] if idx < len(acc) else {}
 
-    def read(self, idx: int) -> np.ndarray:
-        """(count, width) array of an accessor, strided views gathered."""
+    def locate(self, idx: int) -> "_Located":
+        """Where an accessor's elements lie (validated as read() validates)."""
         accessors = self.doc.get("accessors", [])
         if not 0 <= idx < len(accessors):
             raise SceneError(f"accessor {idx} does not exist")
@@ -267,12 +277,13 @@ class _GltfReader:
             raise SceneError(f"accessor {idx}: unsupported type {acc.get('type')!r}")
         dt = np.dtype(COMPONENT_DTYPE[ctype])
         width = TYPE_WIDTH[acc["type"]]
+        elem = dt.itemsize * width
         count = int(acc.get("count", 0))
         if count == 0:
-            return np.zeros((0, width), dtype=dt)
+            return _Located(None, 0, elem, 0, width, dt)
         view_idx = acc.get("bufferView")
         if view_idx is None:
-            return np.zeros((count, width), dtype=dt)
+            return _Located(None, 0, elem, count, width, dt)     # all zeros
         views = self.doc.get("bufferViews", [])
         if not 0 <= view_idx < len(views):
             raise SceneError(f"accessor {idx}: bufferView {view_idx} does not exist")
@@ -281,7 +292,6 @@ class _GltfReader:
         if not 0 <= buf_idx < len(self.buffers):
             raise SceneError(f"accessor {idx}: buffer {buf_idx} does not exist")
         raw = self.buffers[buf_idx]
-        elem = dt.itemsize * width
         stride = int(view.get("byteStride", 0)) or elem
         first = int(view.get("byteOffset", 0)) + int(acc.get("byteOffset", 0))
         last = first + stride * (count - 1) + elem
@@ -289,11 +299,35 @@ class _GltfReader:
         if last > len(raw) or last > view_end:
             raise SceneError(f"accessor {idx}: data range [{first}, {last}) overruns its "
                              "buffer view")
-        if stride == elem:
-            return np.frombuffer(raw, dtype=dt, count=count * width, offset=first).reshape(
-                count, width)
-        rows = np.lib.stride_tricks.as_strided(np.frombuffer(raw, dtype=np.uint8)[first:],
-                                               shape=(count, elem), strides=(stride, 1))
+        return _Located(raw, first, stride, count, width, dt)
+
+    def read(self, idx: int) -> np.ndarray:
+        """(count, width) array of an accessor, strided views gathered."""
+        return self.locate(idx).array()
+
+
+@dataclass
+class _Located:
+    """An accessor's elements: `count` rows of `width` x `dtype`, `stride`
+    bytes apart from byte `first` of `data` (None: all zeros)."""
+    data: bytes | None
+    first: int
+    stride: int
+    count: int
+    width: int
+    dtype: np.dtype
+
+    def array(self) -> np.ndarray:
+        dt, width, count = self.dtype, self.width, self.count
+        if self.data is None:
+            return np.zeros((count, width), dtype=dt)
+        elem = dt.itemsize * width
+        if self.stride == elem:
+            return np.frombuffer(self.data, dtype=dt, count=count * width,
+                                 offset=self.first).reshape(count, width)
+        rows = np.lib.stride_tricks.as_strided(
+            np.frombuffer(self.data, dtype=np.uint8)[self.first:], shape=(count, elem),
+            strides=(self.stride, 1))
         return rows.copy().view(dt).reshape(count, width)
 
 
@@ -328,7 +362,21 @@ def node_matrix(node: dict, index: int) -> np.ndarray:
     return m
 
 
-def _primitive(reader: _GltfReader, prim: dict, where: str, materials: list) -> GltfPrimitive:
+@dataclass
+class GltfPrimitiveRef:
+    """A primitive as located accessors (the device ingest's input): no
+    float64 widening on the host."""
+    positions: _Located
+    normals: _Located | None
+    indices: _Located | None          # None: 0 .. n-1
+    n_indices: int
+    material_name: str | None
+    material_fallback: OpenPbrParams | None
+
+
+def _primitive_ref(reader: _GltfReader, prim: dict, where: str, materials: list):
+    """The checks of scene.py:251-351 in the reference's order; returns the
+    located primitive and its index values (None when implicit)."""
     mode = prim.get("mode", 4)
     if mode != 4:
         raise SceneError(f"{where}: unsupported primitive mode {mode}; only TRIANGLES (4) is "
@@ -339,25 +387,29 @@ def _primitive(reader: _GltfReader, prim: dict, where: str, materials: list) -> 
     spec = reader.accessor_spec(attrs["POSITION"])
     if spec.get("componentType") != 5126 or spec.get("type") != "VEC3":
         raise SceneError(f"{where}: POSITION must be a float32 VEC3 accessor")
-    positions = reader.read(attrs["POSITION"]).astype(np.float64)
+    positions = reader.locate(attrs["POSITION"])
     normals = None
     if "NORMAL" in attrs:
         spec = reader.doc["accessors"][attrs["NORMAL"]]
         if spec.get("componentType") != 5126 or spec.get("type") != "VEC3":
             raise SceneError(f"{where}: NORMAL must be a float32 VEC3 accessor")
-        normals = reader.read(attrs["NORMAL"]).astype(np.float64)
-        if normals.shape != positions.shape:
+        normals = reader.locate(attrs["NORMAL"])
+        if normals.count != positions.count:
             raise SceneError(f"{where}: NORMAL count differs from POSITION count")
+    values = indices = None
     if "indices" in prim:
         spec = reader.accessor_spec(prim["indices"])
         if spec.get("componentType") not in INDEX_COMPONENTS or spec.get("type") != "SCALAR":
             raise SceneError(f"{where}: indices must be a scalar u8/u16/u32 accessor")
-        indices = reader.read(prim["indices"]).astype(np.int64).ravel()
+        indices = reader.locate(prim["indices"])
+        values = indices.array().ravel()
+        n_indices = values.size
     else:
-        indices = np.arange(positions.shape[0], dtype=np.int64)
-    if indices.size % 3 != 0:
-        raise SceneError(f"{where}: index count {indices.size} is not a multiple of 3")
-    if indices.size and (indices.min() < 0 or indices.max() >= positions.shape[0]):
+        n_indices = positions.count
+    if n_indices % 3 != 0:
+        raise SceneError(f"{where}: index count {n_indices} is not a multiple of 3")
+    if values is not None and values.size and (values.min() < 0 or
+                                               values.max() >= positions.count):
         raise SceneError(f"{where}: index out of range")
     name = fallback = None
     if "material" in prim:
@@ -374,12 +426,35 @@ def _primitive(reader: _GltfReader, prim: dict, where: str, materials: list) -> 
         fallback = OpenPbrParams(base_color=tuple(unit(c) for c in base[:3]),
                                  base_metalness=unit(pbr.get("metallicFactor", 1.0)),
                                  specular_roughness=unit(pbr.get("roughnessFactor", 1.0)))
-    return GltfPrimitive(positions, normals, indices, name, fallback)
+    return GltfPrimitiveRef(positions, normals, indices, n_indices, name, fallback), values
+
+
+def _primitive(reader: _GltfReader, prim: dict, where: str, materials: list) -> GltfPrimitive:
+    ref, values = _primitive_ref(reader, prim, where, materials)
+    positions = ref.positions.array().astype(np.float64)
+    normals = ref.normals.array().astype(np.float64) if ref.normals is not None else None
+    indices = values.astype(np.int64) if values is not None else \
+        np.arange(positions.shape[0], dtype=np.int64)
+    return GltfPrimitive(positions, normals, indices, ref.material_name, ref.material_fallback)
+
+
+def _primitive_located(reader, prim, where, materials) -> GltfPrimitiveRef:
+    return _primitive_ref(reader, prim, where, materials)[0]
 
 
 def load_gltf(path) -> GltfDocument:
     """Mesh-space geometry plus the node hierarchy of a .gltf / .glb file
     (scene.py:384-490)."""
+    return _read_document(path, _primitive)
+
+
+def load_gltf_located(path) -> GltfDocument:
+    """load_gltf with every primitive left as located accessors
+    (GltfPrimitiveRef): the same checks and errors, no float64 arrays."""
+    return _read_document(path, _primitive_located)
+
+
+def _read_document(path, primitive) -> GltfDocument:
     path = Path(path)
     if not path.is_file():
         raise SceneError(f"scene file not found: {path}")
@@ -389,7 +464,7 @@ def load_gltf(path) -> GltfDocument:
     meshes = []
     for mi, mesh in enumerate(doc.get("meshes", [])):
         name = mesh.get("name", f"mesh_{mi}")
-        prims = [_primitive(reader, prim, f"mesh {mi} ({name!r}) primitive {pi}", materials)
+        prims = [primitive(reader, prim, f"mesh {mi} ({name!r}) primitive {pi}", materials)
                  for pi, prim in enumerate(mesh.get("primitives", []))]
         meshes.append(GltfMesh(name, prims))
     nodes = []
@@ -430,22 +505,11 @@ def generate_smooth_normals(positions: np.ndarray, indices: np.ndarray) -> np.nd
     return acc / length
 
 
-def flatten_scene(doc: GltfDocument, materials: MaterialMap, camera: CameraConfig,
-                  environment: EnvironmentConfig) -> SceneDescription:
-    """World-space triangle soup: node transforms baked in, materials
-    resolved (config name -> glTF fallback -> default), degenerate triangles
-    dropped (scene.py:519-596)."""
-    parts = []
-    table: dict = {}
-    params_list: list = []
-
-    def material_slot(params) -> int:
-        if params not in table:
-            table[params] = len(params_list)
-            params_list.append(params)
-        return table[params]
-
-    def walk(idx: int, parent: np.ndarray, path: tuple) -> None:
+def _instances(doc: GltfDocument):
+    """(world, linear, to_normals, primitive) per mesh primitive of every node
+    in flatten_scene's depth-first visit order, with its cycle / singular
+    transform checks (scene.py:527-560)."""
+    def walk(idx: int, parent: np.ndarray, path: tuple):
         if idx in path:
             raise SceneError(f"node {idx}: cycle in node hierarchy")
         node = doc.nodes[idx]
@@ -456,24 +520,52 @@ def flatten_scene(doc: GltfDocument, materials: MaterialMap, camera: CameraConfi
                 raise SceneError(f"node {idx} ({node.name!r}): singular transform")
             to_normals = np.linalg.inv(linear).T
             for prim in doc.meshes[node.mesh].primitives:
-                world_pos = prim.positions @ linear.T + world[:3, 3]
-                local_n = prim.normals if prim.normals is not None else \
-                    generate_smooth_normals(prim.positions, prim.indices)
-                world_n = local_n @ to_normals.T
-                params = materials.resolve(prim.material_name) if prim.material_name else None
-                if params is None:
-                    params = prim.material_fallback
-                if params is None:
-                    params = materials.default
-                slot = material_slot(params)
-                ix = prim.indices
-                parts.append(tuple(world_pos[ix[k::3]] for k in range(3)) +
-                             tuple(world_n[ix[k::3]] for k in range(3)) + (slot,))
+                yield world, linear, to_normals, prim
         for child in node.children:
-            walk(child, world, path + (idx,))
+            yield from walk(child, world, path + (idx,))
 
     for root in doc.roots:
-        walk(root, np.eye(4), ())
+        yield from walk(root, np.eye(4), ())
+
+
+class _MaterialSlots:
+    """Material resolution (config name -> glTF fallback -> default) and the
+    first-use slot table of flatten_scene."""
+
+    def __init__(self, materials: MaterialMap):
+        self.materials = materials
+        self.table: dict = {}
+        self.params_list: list = []
+
+    def slot(self, prim) -> int:
+        params = self.materials.resolve(prim.material_name) if prim.material_name else None
+        if params is None:
+            params = prim.material_fallback
+        if params is None:
+            params = self.materials.default
+        if params not in self.table:
+            self.table[params] = len(self.params_list)
+            self.params_list.append(params)
+        return self.table[params]
+
+
+def flatten_scene(doc: GltfDocument, materials: MaterialMap, camera: CameraConfig,
+                  environment: EnvironmentConfig) -> SceneDescription:
+    """World-space triangle soup: node transforms baked in, materials
+    resolved (config name -> glTF fallback -> default), degenerate triangles
+    dropped (scene.py:519-596)."""
+    parts = []
+    slots = _MaterialSlots(materials)
+    for world, linear, to_normals, prim in _instances(doc):
+        world_pos = prim.positions @ linear.T + world[:3, 3]
+        local_n = prim.normals if prim.normals is not None else \
+            generate_smooth_normals(prim.positions, prim.indices)
+        world_n = local_n @ to_normals.T
+        slot = slots.slot(prim)
+        ix = prim.indices
+        parts.append(tuple(world_pos[ix[k::3]] for k in range(3)) +
+                     tuple(world_n[ix[k::3]] for k in range(3)) + (slot,))
+    params_list = slots.params_list
     if not parts or sum(p[0].shape[0] for p in parts) == 0:
         raise SceneError("empty scene")
     v0, v1, v2, n0, n1, n2 = (np.vstack([p[k] for p in parts]) for k in range(6))
@@ -502,6 +594,154 @@ def load_scene(scene_path, config_path) -> SceneDescription:
     config = load_render_config(config_path)
     return flatten_scene(load_gltf(scene_path), config.materials, config.camera,
                          config.environment)
+
+
+# ------------------------------------------------------------ device ingest
+
+@contextlib.contextmanager
+def _scene_errors():
+    """The device flatten's all-degenerate verdict as the reference's
+    SceneError("empty scene") (scene.py:582)."""
+    try:
+        yield
+    except ValueError as exc:
+        if str(exc) == "empty scene":
+            raise SceneError("empty scene") from None
+        raise
+
+
+def gltf_device_desc(doc: GltfDocument, materials: MaterialMap):
+    """The lt_gltf_desc of a located document (load_gltf_located): the
+    buffers' raw bytes, one record per primitive, one per (node, primitive)
+    instance in flatten_scene's visit order with its world matrix,
+    inverse-transpose (computed here with the reference's numpy calls) and
+    material slot.  Returns (desc, keep-alive list, material list, total
+    triangles); raises the reference's "empty scene" for a scene with no
+    triangles."""
+    import ctypes as C
+
+    from . import _lib
+    keep: list = []
+    buffers: list = []
+    buffer_ids: dict = {}
+
+    def buffer_of(loc: _Located) -> tuple[int, int, int]:
+        if loc.data is None:        # an accessor without a bufferView: zeros
+            data, first, stride = bytes(loc.count * loc.width * loc.dtype.itemsize), 0, \
+                loc.width * loc.dtype.itemsize
+        else:
+            data, first, stride = loc.data, loc.first, loc.stride
+        key = id(data)
+        if key not in buffer_ids:
+            buffer_ids[key] = len(buffers)
+            buffers.append(data)
+        return buffer_ids[key], first, stride
+
+    prim_ids: dict = {}
+    prims: list = []
+
+    def prim_record(prim: GltfPrimitiveRef) -> int:
+        key = id(prim)
+        if key in prim_ids:
+            return prim_ids[key]
+        r = _lib.GltfPrimitive()
+        r.pos_buffer, r.pos_offset, r.pos_stride = buffer_of(prim.positions)
+        r.n_vertices = prim.positions.count
+        if prim.normals is not None:
+            r.nrm_buffer, r.nrm_offset, r.nrm_stride = buffer_of(prim.normals)
+        else:
+            r.nrm_buffer, r.nrm_offset, r.nrm_stride = -1, 0, 12
+        if prim.indices is not None:
+            r.idx_buffer, r.idx_offset, r.idx_stride = buffer_of(prim.indices)
+            r.idx_bytes = prim.indices.dtype.itemsize
+        else:
+            r.idx_buffer, r.idx_offset, r.idx_stride, r.idx_bytes = -1, 0, 4, 4
+        r.n_indices = prim.n_indices
+        prim_ids[key] = len(prims)
+        prims.append(r)
+        keep.append(prim)
+        return prim_ids[key]
+
+    slots = _MaterialSlots(materials)
+    instances = []
+    total = 0
+    for world, linear, to_normals, prim in _instances(doc):
+        rec = _lib.GltfInstance()
+        rec.primitive = prim_record(prim)
+        rec.material = slots.slot(prim)
+        rec.linear[:] = [float(x) for x in np.ascontiguousarray(linear).ravel()]
+        rec.translation[:] = [float(x) for x in world[:3, 3]]
+        rec.normal_matrix[:] = [float(x) for x in np.ascontiguousarray(to_normals).ravel()]
+        instances.append(rec)
+        total += prim.n_indices // 3
+    if not instances or total == 0:
+        raise SceneError("empty scene")
+    desc = _lib.GltfDesc()
+    desc.n_buffers = len(buffers)
+    bufs = [np.frombuffer(b, dtype=np.uint8) if len(b) else np.zeros(1, np.uint8)
+            for b in buffers]
+    ptrs = (C.POINTER(C.c_uint8) * max(1, len(bufs)))(
+        *[b.ctypes.data_as(C.POINTER(C.c_uint8)) for b in bufs])
+    sizes = np.array([len(b) for b in buffers], dtype=np.int64)
+    prim_arr = (_lib.GltfPrimitive * len(prims))(*prims)
+    inst_arr = (_lib.GltfInstance * len(instances))(*instances)
+    desc.buffers = ptrs
+    desc.buffer_bytes = sizes.ctypes.data_as(C.POINTER(C.c_int64))
+    desc.n_primitives = len(prims)
+    desc.primitives = prim_arr
+    desc.n_instances = len(instances)
+    desc.instances = inst_arr
+    keep += [buffers, bufs, ptrs, sizes, prim_arr, inst_arr]
+    return desc, keep, slots.params_list, total
+
+
+def flatten_scene_device(doc: GltfDocument, materials: MaterialMap, camera: CameraConfig,
+                         environment: EnvironmentConfig, device: int = 0) -> SceneDescription:
+    """flatten_scene (scene.py:519-596) on the GPU from a located document:
+    the same SceneDescription bit for bit (lt_gltf_flatten), copied back to
+    the host."""
+    import ctypes as C
+
+    from . import _lib
+    _lib.require_gpu()
+    desc, keep, params_list, total = gltf_device_desc(doc, materials)
+    out = [np.empty((total, 3)) for _ in range(6)]
+    mat = np.empty(total, dtype=np.int32)
+    kept, dropped = C.c_int64(0), C.c_int64(0)
+    dp = C.POINTER(C.c_double)
+    with _scene_errors():
+        _lib.check(_lib.lib().lt_gltf_flatten(
+            C.byref(desc), int(device), total, *[a.ctypes.data_as(dp) for a in out],
+            mat.ctypes.data_as(C.POINTER(C.c_int32)), C.byref(kept), C.byref(dropped)))
+    k = kept.value
+    tris = TriangleBuffer(*[a[:k] for a in out], mat[:k])
+    return SceneDescription(tris, params_list, camera, environment, dropped.value)
+
+
+def load_scene_gpu(scene_path, config_path, device: int = 0) -> SceneDescription:
+    """load_scene with the flatten on the GPU: the host reads the file and
+    walks the nodes, the device decodes the float32 accessors and builds the
+    world-space soup; the result is load_scene's, bit for bit."""
+    config = load_render_config(config_path)
+    return flatten_scene_device(load_gltf_located(scene_path), config.materials, config.camera,
+                                config.environment, device)
+
+
+def load_device_scene(scene_path, config_path, device: int = 0):
+    """glTF file + render config straight to a resident DeviceScene: the
+    GLB's float32 / integer bytes are the only geometry uploaded, the
+    flattened soup and the BVH are built on the device
+    (lt_scene_create_gltf).  `render_progressive(ds, settings)` renders it;
+    `ds.degenerate_dropped` and `ds.camera` are set."""
+    from .device import DeviceScene
+    config = load_render_config(config_path)
+    doc = load_gltf_located(scene_path)
+    desc, keep, params_list, _ = gltf_device_desc(doc, config.materials)
+    with _scene_errors():
+        ds = DeviceScene.from_gltf(desc, keep, params_list, config.environment, config.camera,
+                                   device)
+    ds.materials = params_list
+    return ds
 
 
 # ------------------------------------------------------------ GLB writer

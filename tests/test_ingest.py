@@ -95,6 +95,32 @@ def test_material_map_wildcards():
         MaterialMap([("a*b", a)])
 
 
+@pytest.mark.parametrize("name", FIXTURES)
+def test_device_ingest_description(name):
+    """The host half of the device ingest (lt_gltf_desc): one record per
+    primitive, one instance per (node, primitive) in visit order, the
+    reference's pre-filter triangle count and material table."""
+    from paper_2407_19977_b200.ingest import (gltf_device_desc, load_gltf, load_gltf_located,
+                                              load_render_config, load_scene)
+    cfg = load_render_config(DIR / "config.json")
+    desc, keep, mats, total = gltf_device_desc(load_gltf_located(DIR / name), cfg.materials)
+    sd = load_scene(DIR / name, DIR / "config.json")
+    assert total == len(sd.triangles.v0) + sd.degenerate_dropped
+    assert mats == sd.materials
+    doc = load_gltf(DIR / name)
+    assert desc.n_primitives == sum(len(m.primitives) for m in doc.meshes)
+    for i in range(desc.n_instances):
+        inst = desc.instances[i]
+        assert 0 <= inst.primitive < desc.n_primitives and 0 <= inst.material < len(mats)
+        lin = np.array(inst.linear[:]).reshape(3, 3)
+        assert np.array_equal(np.array(inst.normal_matrix[:]).reshape(3, 3),
+                              np.linalg.inv(lin).T)
+    for i in range(desc.n_primitives):
+        p = desc.primitives[i]
+        assert p.n_indices % 3 == 0 and p.idx_bytes in (1, 2, 4)
+        assert p.pos_offset + p.pos_stride * (p.n_vertices - 1) + 12 <= desc.buffer_bytes[p.pos_buffer]
+
+
 @pytest.mark.gpu
 def test_ingested_scene_renders_like_the_oracle():
     """A GLB scene loaded here, rendered on the GPU, per-sample against the

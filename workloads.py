@@ -116,6 +116,7 @@ class Scene:
     camera: Camera
     environment: Environment
     degenerate_dropped: int = 0
+    parts: list | None = None     # MeshBuilder parts (indexed meshes), for write_gltf
 
 
 # ------------------------------------------------------------------ meshes
@@ -296,7 +297,7 @@ def cornell_box(width: int = 64, height: int = 64, variant: str = "diffuse") -> 
         mb.add_flat(box_tris((-0.5, 0.0, 0.25), (-0.125, 0.375, 0.625)), 6)   # glass block
     cam = Camera(position=(0.0, 1.0, 3.75), look_at=(0.0, 1.0, 0.0),
                        vertical_fov_deg=40.0, width=width, height=height)
-    return Scene(mb.build(), mats, cam, Environment.uniform((0.0, 0.0, 0.0)))
+    return Scene(mb.build(), mats, cam, Environment.uniform((0.0, 0.0, 0.0)), parts=mb.parts)
 
 
 def sphere_on_plane(n_triangles: int = 70_000, width: int = 1920, height: int = 1080,
@@ -314,7 +315,7 @@ def sphere_on_plane(n_triangles: int = 70_000, width: int = 1920, height: int = 
     cam = Camera(position=(0.0, 1.5, 4.75), look_at=(0.0, 1.0, 0.0),
                        vertical_fov_deg=40.0, width=width, height=height)
     env = environment or Environment.gradient(**BENCH_ENVIRONMENT)
-    return Scene(mb.build(), mats, cam, env)
+    return Scene(mb.build(), mats, cam, env, parts=mb.parts)
 
 
 def pushbutton(width: int = 1920, height: int = 1080, extended: bool = True,
@@ -403,7 +404,7 @@ def pushbutton(width: int = 1920, height: int = 1080, extended: bool = True,
     if env is None:
         env = Environment.latlong(synthetic_hdr(), 1.0) if extended else \
             Environment.gradient(**BENCH_ENVIRONMENT)
-    return Scene(mb.build(), mats, cam, env)
+    return Scene(mb.build(), mats, cam, env, parts=mb.parts)
 
 
 def synthetic_hdr(width: int = 1024, height: int = 512, sun_dir=(0.45, 0.6, 0.35),
@@ -432,6 +433,70 @@ def synthetic_hdr(width: int = 1024, height: int = 512, sun_dir=(0.45, 0.6, 0.35
     img = img + (cosang >= core)[..., None] * sun_radiance * np.array([1.0, 0.95, 0.85])
     img = img + halo[..., None] * np.array([2.0, 1.8, 1.4])
     return np.ascontiguousarray(img, dtype=np.float32)
+
+
+def write_gltf(scene: Scene, glb_path, config_path, normals: bool = True) -> None:
+    """The scene as a GLB + render config that `load_scene` reads: one mesh
+    per MeshBuilder part (float32 positions, float32 normals unless
+    `normals` is False -- then the loader generates smooth normals -- and
+    u32 indices), material "m<k>" bound in the config to the scene's k-th
+    material, one identity node per mesh.  A lat-long environment is written
+    as uniform white (the config format has no maps)."""
+    import json
+    import struct
+    from dataclasses import asdict
+    blobs, views, accessors, meshes, nodes, used = [], [], [], [], [], {}
+    offset = 0
+
+    def add_blob(arr, ctype, kind, count):
+        nonlocal offset
+        data = arr.tobytes()
+        views.append({"buffer": 0, "byteOffset": offset, "byteLength": len(data)})
+        blobs.append(data + b"\x00" * (-len(data) % 4))
+        offset += len(blobs[-1])
+        accessors.append({"bufferView": len(views) - 1, "componentType": ctype,
+                          "count": int(count), "type": kind})
+        return len(accessors) - 1
+
+    for pos, idx, nrm, mat in scene.parts:
+        attrs = {"POSITION": add_blob(np.asarray(pos, np.float32), 5126, "VEC3", len(pos))}
+        if normals:
+            attrs["NORMAL"] = add_blob(np.asarray(nrm, np.float32), 5126, "VEC3", len(pos))
+        ind = add_blob(np.asarray(idx, np.uint32), 5125, "SCALAR", idx.size)
+        used.setdefault(mat, len(used))
+        meshes.append({"primitives": [{"attributes": attrs, "indices": ind,
+                                       "material": used[mat]}]})
+        nodes.append({"mesh": len(meshes) - 1})
+    binary = b"".join(blobs)
+    doc = {"asset": {"version": "2.0"}, "buffers": [{"byteLength": len(binary)}],
+           "bufferViews": views, "accessors": accessors, "meshes": meshes, "nodes": nodes,
+           "scenes": [{"nodes": list(range(len(nodes)))}], "scene": 0,
+           "materials": [{"name": f"m{m}"} for m in used]}
+    js = json.dumps(doc).encode()
+    js += b" " * (-len(js) % 4)
+    with open(glb_path, "wb") as f:
+        f.write(struct.pack("<III", 0x46546C67, 2, 28 + len(js) + len(binary)))
+        f.write(struct.pack("<II", len(js), 0x4E4F534A) + js)
+        f.write(struct.pack("<II", len(binary), 0x004E4942) + binary)
+    cam, env = scene.camera, scene.environment
+    if env.kind == "gradient":
+        env_doc = {"type": "gradient", "zenith": [float(x) for x in env.zenith],
+                   "horizon": [float(x) for x in env.horizon]}
+    elif env.kind == "uniform":
+        env_doc = {"type": "uniform", "radiance": [float(x) for x in env.radiance]}
+    else:
+        env_doc = {"type": "uniform", "radiance": [1.0, 1.0, 1.0]}
+    config = {"camera": {"position": [float(x) for x in cam.position],
+                         "look_at": [float(x) for x in cam.look_at],
+                         "up": [float(x) for x in cam.up],
+                         "vertical_fov_deg": float(cam.vertical_fov_deg),
+                         "width": int(cam.width), "height": int(cam.height)},
+              "environment": env_doc,
+              "materials": {f"m{m}": {k: (list(v) if isinstance(v, tuple) else v)
+                                      for k, v in asdict(scene.materials[m]).items()}
+                            for m in used}}
+    with open(config_path, "w") as f:
+        json.dump(config, f)
 
 
 def scene_by_name(name: str, **kw) -> Scene:
