@@ -26,7 +26,7 @@ from .integrator import (RenderResult, RenderSettings, environment_radiance,
                          trace_radiance, trace_radiance_batch)
 from .procgen import bumpy_sphere, bumpy_sphere_glb, icosphere, icosphere_glb
 from .ingest import (MaterialMap, RenderConfig, flatten_scene, generate_smooth_normals, load_gltf,
-                     load_render_config, load_scene, save_glb)
+                     load_render_config, load_scene, save_glb, load_device_scene, load_scene_gpu)
 
 __version__ = "0.1.0"
 
@@ -49,5 +49,5 @@ __all__ = [
     "trace_radiance_batch",
     "bumpy_sphere", "bumpy_sphere_glb", "icosphere", "icosphere_glb",
     "MaterialMap", "RenderConfig", "flatten_scene", "generate_smooth_normals", "load_gltf",
-    "load_render_config", "load_scene", "save_glb",
+    "load_render_config", "load_scene", "save_glb", "load_device_scene", "load_scene_gpu",
 ]
