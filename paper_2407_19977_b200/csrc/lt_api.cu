@@ -63,6 +63,11 @@ namespace {
 #define LT_MAX_BATCH_LOG2 28
 #endif
 constexpr int64_t kMaxBatchPaths = int64_t(1) << LT_MAX_BATCH_LOG2;
+// Passes of at most this many paths run as one fused launch per batch
+// (k_path_small) instead of the wavefront: 2x faster at 1-2 M paths (a
+// 1080p 1-spp progressive update: 2.21 -> 1.08 ms), even at ~8 M, 1.5x
+// slower at full frames (profiles/r02_fused_small.jsonl, _scale.jsonl).
+constexpr int64_t kFusedMaxPaths = int64_t(1) << 22;
 
 // Device buffer.  With `ast` set the memory comes stream-ordered from the
 // device's default mempool (cudaMallocAsync / cudaFreeAsync on `ast`), so a
@@ -1576,6 +1581,15 @@ static int render_impl(lt_scene *s, const lt_render_params *p, float *accum, uin
   // a small pass (< 1 M paths) runs on one lane: a second lane would only
   // add launches and a stream fork / join to a few-microsecond frame
   const bool small = n_local * p->sample_count < (int64_t(1) << 20);
+  // the fused one-launch path for passes too small to fill the GPU (no
+  // per-launch counters / timing / material sort requested); LT_FUSED_MAX
+  // overrides the path-count threshold (0 disables)
+  const int64_t fused_max = [] {
+    const char *e = std::getenv("LT_FUSED_MAX");
+    return e ? (int64_t)std::atoll(e) : kFusedMaxPaths;
+  }();
+  const bool fused = n_local * p->sample_count <= fused_max &&
+                     !(p->flags & (LT_FLAG_COUNT | LT_FLAG_SORT_MATERIALS));
   const int n_lanes =
       small ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(s->n_lanes, n_local));
   struct Batch {
@@ -1631,7 +1645,7 @@ static int render_impl(lt_scene *s, const lt_render_params *p, float *accum, uin
     Lane &ln = s->ws->lane[b.lane];
     cudaStream_t ls = fork ? W.lane_st[b.lane] : st;
     int32_t *ctr = ln.counters.as<int32_t>();
-    CK(cudaMemsetAsync(ctr, 0, sizeof(int32_t) * (2 * (size_t)p->max_depth + 2), ls));
+    if (!fused) CK(cudaMemsetAsync(ctr, 0, sizeof(int32_t) * (2 * (size_t)p->max_depth + 2), ls));
     RaygenArgs ra{};
     std::memcpy(ra.cam, p->camera, sizeof(ra.cam));
     ra.width = p->width;
@@ -1643,10 +1657,21 @@ static int render_impl(lt_scene *s, const lt_render_params *p, float *accum, uin
     ra.pix_list = pix_list;
     ra.n_paths = b.np * b.ns;
     ra.t_min = t_min;
-    // raygen writes only the ray records; the depth-0 shade regenerates
-    // throughput / radiance / PCG state
-    launch_raygen(ra, path_arrays(ln), ln.q_o[0].as<float4>(), ln.q_d[0].as<float4>(), ctr, ls);
-    RET(run_bounces(s, ln, p->max_depth, p->rr_start, t_min, p->flags, ls, &ra, ra.n_paths));
+    if (fused) {
+      // (LT_FLAG_PROFILE times the fused launch as the pass's trace time)
+      if (p->flags & LT_FLAG_PROFILE) RET(record_event(s, ls));
+      launch_path_small(s->view, ra, p->max_depth, p->rr_start, path_arrays(ln),
+                        s->ray_ctr.as<unsigned long long>(), ls);
+      if (p->flags & LT_FLAG_PROFILE) RET(record_event(s, ls));
+      s->stats.kernel_launches += 1;
+      s->stats.trace_launches += 1;
+    } else {
+      // raygen writes only the ray records; the depth-0 shade regenerates
+      // throughput / radiance / PCG state
+      launch_raygen(ra, path_arrays(ln), ln.q_o[0].as<float4>(), ln.q_d[0].as<float4>(), ctr,
+                    ls);
+      RET(run_bounces(s, ln, p->max_depth, p->rr_start, t_min, p->flags, ls, &ra, ra.n_paths));
+    }
     AccumArgs aa{b.np, b.pc0, b.ns, pix_list};
     launch_accumulate(aa, ln.S.as<float4>(), accum, valid, invalid, ls);
     s->stats.kernel_launches += 2;

@@ -435,6 +435,108 @@ __device__ __forceinline__ int dir_bin(const float4 &d) {
   return (d.x < 0.f ? 1 : 0) | (d.y < 0.f ? 2 : 0) | (d.z < 0.f ? 4 : 0);
 }
 
+// One path segment of _trace (integrator.py:160-226) after its closest-hit
+// query h = (t, u, v, k): miss -> environment; hit -> emission; the final
+// segment stops; otherwise hit frame, 3 draws, BSDF sample, throughput and
+// Russian roulette (4th draw).  Returns true when the path continues with
+// the ray (out_o, out_d) and throughput Tn.  `inc_of()` yields the PCG
+// increment, asked for only when the segment draws.  Shared by the
+// wavefront shade kernel and the fused small-pass kernel, so both round
+// identically.
+struct Segment {
+  bool wrote_l = false;    // L changed and the path ends here
+  bool scattered = false;  // the draws ran (state advanced)
+  uint64_t st_out;         // PCG state after the segment's draws
+  float4 Tn;               // throughput of the continuation
+  float4 out_o, out_d;     // the continuation ray (path id / t_min in .w)
+  int cls = 0;             // material class (LT_FLAG_COUNT statistics)
+};
+template <class IncFn>
+__device__ __forceinline__ bool shade_segment(const SceneView &sc, int32_t depth,
+                                              int32_t max_depth, int32_t rr_start, float t_min,
+                                              bool want_cls, int32_t p, const float4 &h, f3 o,
+                                              f3 d, const float4 &T, float4 &L, uint64_t state,
+                                              IncFn inc_of, Segment &sg) {
+  const int32_t k = __float_as_int(h.w);
+  sg.st_out = state;
+  if (k < 0) {
+    const f3 e = env_radiance(sc, d);
+    L.x += T.x * e.x;
+    L.y += T.y * e.y;
+    L.z += T.z * e.z;
+    sg.wrote_l = true;
+    return false;
+  }
+  // issue every random load of this hit before using any of them: one
+  // 64 B shading record (geometric normal + material, vertex normals)
+  LT_ASSERT(k < sc.n_tris);
+  const int64_t k4 = 4 * (int64_t)k;
+  const bool scatter = depth != max_depth - 1;
+  const float4 s0 = __ldg(&sc.shade[k4]);
+  float4 s1{}, s2{}, s3{};
+  uint64_t inc = 0;
+  if (scatter) {
+    s1 = __ldg(&sc.shade[k4 + 1]);
+    s2 = __ldg(&sc.shade[k4 + 2]);
+    s3 = __ldg(&sc.shade[k4 + 3]);
+    inc = inc_of();
+  }
+  const int32_t mi = __float_as_int(s0.w);
+  LT_ASSERT(mi >= 0 && mi < sc.n_mats);
+  const GpuMaterial &mt = sc.mats[mi];
+  if (want_cls)
+    sg.cls = !scatter ? 1
+                      : (mt.flags & MAT_DIFFUSE_ONLY)
+                            ? 2
+                            : (mt.flags & (MAT_COAT | MAT_GLASS))
+                                  ? 3 + (int)(mt.flags & (MAT_COAT | MAT_GLASS))
+                                  : 3;
+  if (mt.flags & MAT_EMISSIVE) {
+    L.x += T.x * mt.el * mt.ec[0];
+    L.y += T.y * mt.el * mt.ec[1];
+    L.z += T.z * mt.el * mt.ec[2];
+    sg.wrote_l = true;
+  }
+  if (!scatter) return false;
+  f3 g, sn;
+  bool front;
+  hit_frame(d, mk(s0.x, s0.y, s0.z), mk(s1.x, s1.y, s1.z), mk(s2.x, s2.y, s2.z),
+            mk(s3.x, s3.y, s3.z), h.y, h.z, g, sn, front);
+  const float u_lobe = unit_f32(state, inc);
+  const float u1 = unit_f32(state, inc);
+  const float u2 = unit_f32(state, inc);
+  f3 wi, w;
+  bool alive = sample_material(-d, sn, mt, front, u_lobe, u1, u2, wi, w);
+  float4 Tn = T;
+  if (alive) {
+    Tn.x *= w.x;
+    Tn.y *= w.y;
+    Tn.z *= w.z;
+    if (Tn.x <= 0.f && Tn.y <= 0.f && Tn.z <= 0.f) alive = false;
+  }
+  if (alive && depth >= rr_start) {
+    float pr = fmaxf(fmaxf(Tn.x, Tn.y), Tn.z);
+    pr = fminf(fmaxf(pr, LT_RR_MIN_F), 1.f);
+    const float u_rr = unit_f32(state, inc);
+    if (u_rr >= pr) {
+      alive = false;
+    } else {
+      Tn.x /= pr;
+      Tn.y /= pr;
+      Tn.z /= pr;
+    }
+  }
+  sg.scattered = true;
+  sg.st_out = state;
+  if (!alive) return false;
+  sg.wrote_l = false;  // (the continuation's record carries L)
+  sg.Tn = Tn;
+  const float t = h.x;
+  sg.out_o = make_float4(o.x + t * d.x, o.y + t * d.y, o.z + t * d.z, __int_as_float(p));
+  sg.out_d = make_float4(wi.x, wi.y, wi.z, t_min);
+  return true;
+}
+
 // One bounce of _trace (integrator.py:160-226) for every queued path:
 // miss -> environment; hit -> emission; final segment stops; otherwise hit
 // frame, 3 draws, BSDF sample, throughput, Russian roulette (4th draw), and
@@ -467,7 +569,6 @@ __global__ void __launch_bounds__(kShadeThreads, LT_SHADE_MIN_BLOCKS)
       // queue entries and path state stream through (evict-first) so the
       // L2 keeps the triangle / shading records
       const float4 h = __ldcs(&hits[q]);
-      const int32_t k = __float_as_int(h.w);
       int32_t p;
       f3 o, d;
       float4 T, L;
@@ -496,94 +597,22 @@ __global__ void __launch_bounds__(kShadeThreads, LT_SHADE_MIN_BLOCKS)
         ld_path(pa.S, p, T, L, st0);
         rs.x = st0;
       }
-      bool wrote_l = false;
-      bool scattered = false;
-      uint64_t st_out = rs.x;  // the PCG state after this bounce's draws
-      cls = 0;  // miss
-      if (k < 0) {
-        const f3 e = env_radiance(sc, d);
-        L.x += T.x * e.x;
-        L.y += T.y * e.y;
-        L.z += T.z * e.z;
-        wrote_l = true;
-      } else {
-        // issue every random load of this hit before using any of them: one
-        // 64 B shading record (geometric normal + material, vertex normals)
-        LT_ASSERT(k < sc.n_tris);
-        const int64_t k4 = 4 * (int64_t)k;
-        const bool scatter = sa.depth != sa.max_depth - 1;
-        const float4 s0 = __ldg(&sc.shade[k4]);
-        float4 s1{}, s2{}, s3{};
-        if (scatter) {
-          s1 = __ldg(&sc.shade[k4 + 1]);
-          s2 = __ldg(&sc.shade[k4 + 2]);
-          s3 = __ldg(&sc.shade[k4 + 3]);
-          if (!primary) rs.y = pa.inc ? __ldg(&pa.inc[p]) : path_inc(ra, p);
-        }
-        const int32_t mi = __float_as_int(s0.w);
-        LT_ASSERT(mi >= 0 && mi < sc.n_mats);
-        const GpuMaterial &mt = sc.mats[mi];
-        if (sa.warp_ctr)
-          cls = !scatter ? 1
-                         : (mt.flags & MAT_DIFFUSE_ONLY)
-                               ? 2
-                               : (mt.flags & (MAT_COAT | MAT_GLASS)) ? 3 + (int)(mt.flags &
-                                                                            (MAT_COAT | MAT_GLASS))
-                                                                     : 3;
-        if (mt.flags & MAT_EMISSIVE) {
-          L.x += T.x * mt.el * mt.ec[0];
-          L.y += T.y * mt.el * mt.ec[1];
-          L.z += T.z * mt.el * mt.ec[2];
-          wrote_l = true;
-        }
-        if (scatter) {
-          f3 g, sn;
-          bool front;
-          hit_frame(d, mk(s0.x, s0.y, s0.z), mk(s1.x, s1.y, s1.z), mk(s2.x, s2.y, s2.z),
-                    mk(s3.x, s3.y, s3.z), h.y, h.z, g, sn, front);
-          uint64_t state = rs.x;
-          const uint64_t inc = rs.y;
-          const float u_lobe = unit_f32(state, inc);
-          const float u1 = unit_f32(state, inc);
-          const float u2 = unit_f32(state, inc);
-          f3 wi, w;
-          bool alive = sample_material(-d, sn, mt, front, u_lobe, u1, u2, wi, w);
-          float4 Tn = T;
-          if (alive) {
-            Tn.x *= w.x;
-            Tn.y *= w.y;
-            Tn.z *= w.z;
-            if (Tn.x <= 0.f && Tn.y <= 0.f && Tn.z <= 0.f) alive = false;
-          }
-          if (alive && sa.depth >= sa.rr_start) {
-            float pr = fmaxf(fmaxf(Tn.x, Tn.y), Tn.z);
-            pr = fminf(fmaxf(pr, LT_RR_MIN_F), 1.f);
-            const float u_rr = unit_f32(state, inc);
-            if (u_rr >= pr) {
-              alive = false;
-            } else {
-              Tn.x /= pr;
-              Tn.y /= pr;
-              Tn.z /= pr;
-            }
-          }
-          scattered = true;
-          st_out = state;
-          if (alive) {
-            st_path(pa.S, p, Tn, L, state);
-            wrote_l = false;  // (the record is current)
-            const float t = h.x;
-            out_o = make_float4(o.x + t * d.x, o.y + t * d.y, o.z + t * d.z, __int_as_float(p));
-            out_d = make_float4(wi.x, wi.y, wi.z, sa.t_min);
-            emit = true;
-          }
-        }
+      Segment sg;
+      emit = shade_segment(
+          sc, sa.depth, sa.max_depth, sa.rr_start, sa.t_min, sa.warp_ctr != nullptr, p, h, o, d,
+          T, L, rs.x,
+          [&]() -> uint64_t {
+            return primary ? rs.y : pa.inc ? __ldg(&pa.inc[p]) : path_inc(ra, p);
+          },
+          sg);
+      cls = sg.cls;
+      if (emit) {
+        st_path(pa.S, p, sg.Tn, L, sg.st_out);
+        out_o = sg.out_o;
+        out_d = sg.out_d;
       }
-      // a path that ends here leaves its radiance in the record (the
-      // accumulation reads it); the primary launch writes every path's
-      // record once (raygen does not clear it)
-      // (an explicit path -- pa.inc set -- also reports its final PCG state)
-      if (!emit && (wrote_l || primary || (scattered && pa.inc))) st_path(pa.S, p, T, L, st_out);
+      if (!emit && (sg.wrote_l || primary || (sg.scattered && pa.inc)))
+        st_path(pa.S, p, T, L, sg.st_out);
     }
     if (sa.warp_ctr) {
       // shading divergence: distinct material classes among a warp's lanes
@@ -645,6 +674,45 @@ __global__ void __launch_bounds__(kShadeThreads, LT_SHADE_MIN_BLOCKS)
       }
     }
   }
+}
+
+// Fused small pass: one thread runs a whole (pixel, sample) path -- the
+// camera ray, then per segment the per-thread closest-hit traversal
+// (traverse<true>: the wide layout, leaf test and tie rule of k_trace) and
+// shade_segment -- and leaves its radiance in the path record for
+// k_accumulate.  For passes too small to fill the GPU, where the
+// wavefront's two dependent launches per segment are the cost (C1: 16 K
+// paths); results are bit-identical to the wavefront path.
+__global__ void __launch_bounds__(kShadeThreads)
+    k_path_small(SceneView sc, RaygenArgs ra, int32_t max_depth, int32_t rr_start, PathArrays pa,
+                 unsigned long long *__restrict__ ray_ctr) {
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  unsigned rays = 0;
+  if (p < ra.n_paths) {
+    f3 o, d;
+    uint64_t state, inc;
+    primary_ray(ra, p, o, d, state, inc);
+    float4 T = make_float4(1.f, 1.f, 1.f, 0.f), L = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int32_t depth = 0; depth < max_depth; ++depth) {
+      const HitRec hr =
+          traverse<true, false>(sc, o, d, ra.t_min, __int_as_float(0x7f800000), nullptr, nullptr);
+      ++rays;
+      const float4 h = make_float4(hr.t, hr.u, hr.v, __int_as_float(hr.k));
+      Segment sg;
+      const bool cont = shade_segment(sc, depth, max_depth, rr_start, ra.t_min, false,
+                                      (int32_t)p, h, o, d, T, L, state,
+                                      [&]() -> uint64_t { return inc; }, sg);
+      state = sg.st_out;
+      if (!cont) break;
+      T = sg.Tn;
+      o = mk(sg.out_o.x, sg.out_o.y, sg.out_o.z);
+      d = mk(sg.out_d.x, sg.out_d.y, sg.out_d.z);
+    }
+    st_path(pa.S, p, T, L, state);
+  }
+  // closest-hit queries of the pass (ray_ctr[0], as k_trace counts them)
+  for (int off = 16; off > 0; off >>= 1) rays += __shfl_xor_sync(kFull, rays, off);
+  if ((threadIdx.x & 31) == 0 && rays) atomicAdd(ray_ctr, (unsigned long long)rays);
 }
 
 // ------------------------------------------------------------------ device layout
@@ -1227,6 +1295,14 @@ cudaError_t launch_shade(const SceneView &sc, const ShadeArgs &sa, const PathArr
   }
   return cudaLaunchKernelEx(&cfg, k_shade, sc, s2, ra, pa, q_o, q_d, hits, count_in, n_o, n_d,
                             count_out);
+}
+
+void launch_path_small(const SceneView &sc, const RaygenArgs &ra, int32_t max_depth,
+                       int32_t rr_start, const PathArrays &pa, unsigned long long *ray_ctr,
+                       cudaStream_t st) {
+  if (ra.n_paths <= 0) return;
+  const int grid = (int)((ra.n_paths + kShadeThreads - 1) / kShadeThreads);
+  k_path_small<<<grid, kShadeThreads, 0, st>>>(sc, ra, max_depth, rr_start, pa, ray_ctr);
 }
 
 void launch_accumulate(const AccumArgs &aa, const float4 *S, float *accum, uint32_t *valid,

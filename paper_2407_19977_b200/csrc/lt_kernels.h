@@ -127,6 +127,11 @@ void launch_collapse_all(const double *bmin, const double *bmax, const int32_t *
                          const int32_t *right, const int32_t *count, int32_t *fifo,
                          int32_t *wide_children, int32_t *wide_of, int32_t *n_wide,
                          cudaStream_t st);
+// a whole render batch in one launch (small passes): path records for
+// launch_accumulate, closest-hit count into ray_ctr[0]
+void launch_path_small(const SceneView &sc, const RaygenArgs &ra, int32_t max_depth,
+                       int32_t rr_start, const PathArrays &pa, unsigned long long *ray_ctr,
+                       cudaStream_t st);
 void launch_accumulate(const AccumArgs &aa, const float4 *S, float *accum, uint32_t *valid,
                        uint32_t *invalid, cudaStream_t st);
 void launch_pack_rays_f32(const float *o, const float *d, int64_t n, float t_min, float t_max,

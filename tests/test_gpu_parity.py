@@ -18,7 +18,7 @@ import pytest
 
 import workloads as wl
 
-from conftest import agreement_tiers, golden_scene, record_parity
+from conftest import SCENES, agreement_tiers, golden_scene, record_parity
 
 pytestmark = pytest.mark.gpu
 
@@ -271,8 +271,11 @@ def test_traversal_schedule_does_not_change_results(knobs, monkeypatch):
     threshold), the lane count and the queue ordering change which lane
     traces which ray and when -- never a result: closest hits are a
     lexicographic minimum over (t, triangle index) and per-pixel samples
-    accumulate in index order (scene knobs are read at scene creation)."""
+    accumulate in index order (scene knobs are read at scene creation).
+    (The wavefront path is forced: this frame is small enough for the fused
+    kernel.)"""
     m = lb()
+    monkeypatch.setenv("LT_FUSED_MAX", "0")
     g = golden_scene("sphere20k")
     st = m.RenderSettings(samples_per_pixel=5, max_depth=6, seed=11)
     plain = m.render_progressive(device_scene(g), st).image
@@ -280,6 +283,57 @@ def test_traversal_schedule_does_not_change_results(knobs, monkeypatch):
         monkeypatch.setenv(k, v)
     other = m.render_progressive(device_scene(g), st).image
     assert np.array_equal(plain, other)
+
+
+def fused_and_wavefront(ds, camera, st, monkeypatch, **kw):
+    """One pass through the fused small-pass kernel and one through the
+    wavefront (LT_FUSED_MAX selects): accumulators and ray counts."""
+    from paper_2407_19977_b200.integrator import Accumulator, render_pass_device
+    out = []
+    for limit in ("1000000000", "0"):
+        monkeypatch.setenv("LT_FUSED_MAX", limit)
+        acc = Accumulator(camera.width, camera.height, ds.device)
+        render_pass_device(ds, camera, st, acc, 0, st.samples_per_pixel, **kw)
+        out.append((acc.sum.cpu().numpy().view(np.uint32), acc.valid.cpu().numpy(),
+                    acc.invalid.cpu().numpy(), ds.stats()))
+    return out
+
+
+@pytest.mark.parametrize("name", SCENES)
+def test_fused_small_pass_equals_wavefront(name, monkeypatch):
+    """k_path_small (one thread per path: camera ray, per-thread traversal,
+    the shared shade_segment) against the wavefront raygen -> (k_trace ->
+    k_shade)* on every golden scene: bit-identical accumulators, the same
+    closest-hit count; the fused pass is one kernel launch."""
+    m = lb()
+    g = golden_scene(name)
+    ds = device_scene(g)
+    for st in (m.RenderSettings(samples_per_pixel=6, max_depth=8, seed=3),
+               m.RenderSettings(samples_per_pixel=3, max_depth=3, rr_start_depth=0, seed=9)):
+        (fs, fv, fi, fst), (ws, wv, wi, wst) = fused_and_wavefront(ds, g.camera, st, monkeypatch)
+        assert np.array_equal(fs, ws) and np.array_equal(fv, wv) and np.array_equal(fi, wi)
+        assert fst["rays"] == wst["rays"] > 0
+        assert fst["trace_launches"] == 1 < wst["trace_launches"]
+
+
+@pytest.mark.parametrize("variant", ["mixed", "extended"])
+def test_fused_small_pass_equals_wavefront_extensions(variant, monkeypatch):
+    """The same on the Cornell boxes with metal / glossy dielectric and coat /
+    glass boxes, a sharded pass, and the lat-long environment."""
+    m = lb()
+    sc = wl.cornell_box(40, 40, variant)
+    ds = m.DeviceScene(sc, m.build_bvh(sc.triangles))
+    st = m.RenderSettings(samples_per_pixel=8, max_depth=8, seed=21)
+    (fs, fv, _, _), (ws, wv, _, _) = fused_and_wavefront(ds, sc.camera, st, monkeypatch)
+    assert np.array_equal(fs, ws) and np.array_equal(fv, wv)
+    (fs, fv, _, _), (ws, wv, _, _) = fused_and_wavefront(ds, sc.camera, st, monkeypatch,
+                                                           shard=(1, 3, 8))
+    assert np.array_equal(fs, ws) and np.array_equal(fv, wv)
+    env = m.EnvironmentConfig.latlong(wl.synthetic_hdr(64, 32), 1.0)
+    sc2 = m.SceneDescription(sc.triangles, sc.materials, sc.camera, env)
+    ds2 = m.DeviceScene(sc2, m.build_bvh(sc.triangles))
+    (fs, _, _, _), (ws, _, _, _) = fused_and_wavefront(ds2, sc.camera, st, monkeypatch)
+    assert np.array_equal(fs, ws)
 
 
 @pytest.mark.parametrize("name", ["cornell_c2", "sphere20k"])
