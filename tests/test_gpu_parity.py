@@ -336,6 +336,20 @@ def test_fused_small_pass_equals_wavefront_extensions(variant, monkeypatch):
     assert np.array_equal(fs, ws)
 
 
+@pytest.mark.parametrize("scene_name", ["pushbutton", "sphere70k"])
+def test_fused_small_pass_equals_wavefront_at_scale(scene_name, monkeypatch):
+    """The fused pass on the 1.06 M-triangle C4 scene (coat, glass, lat-long
+    sky) and the 70 k C3 scene at 480x270, 2 spp: bit-identical to the
+    wavefront."""
+    m = lb()
+    sc = wl.scene_by_name(scene_name, width=480, height=270)
+    ds = m.DeviceScene(sc)
+    st = m.RenderSettings(samples_per_pixel=2, max_depth=8, seed=17)
+    (fs, fv, fi, fst), (ws, wv, wi, wst) = fused_and_wavefront(ds, sc.camera, st, monkeypatch)
+    assert np.array_equal(fs, ws) and np.array_equal(fv, wv) and np.array_equal(fi, wi)
+    assert fst["rays"] == wst["rays"]
+
+
 @pytest.mark.parametrize("name", ["cornell_c2", "sphere20k"])
 def test_material_sorted_shading_does_not_change_results(name):
     """LT_FLAG_SORT_MATERIALS (the hit queue shaded in material-class order
