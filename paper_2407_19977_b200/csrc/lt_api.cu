@@ -420,6 +420,10 @@ struct WorkspaceLease {
 };
 
 struct lt_scene {
+  // serializes the host calls that use the scene's scratch buffers, stats
+  // and pixel-list cache (render passes, ray queries) across host threads;
+  // taken before the device's workspace lease, never after it
+  mutable std::recursive_mutex mu;
   int device = 0;
   int sm_count = 0;
   cudaStream_t stream = nullptr;
@@ -1691,6 +1695,7 @@ extern "C" int lt_render_pass(lt_scene *s, const lt_render_params *params, float
                               uint32_t *valid, uint32_t *invalid, void *stream) {
   if (!s) return lt_fail(LT_ERR_INVALID, "null scene");
   DeviceGuard g(s->device);
+  std::lock_guard<std::recursive_mutex> scene_lk(s->mu);
   return render_impl(s, params, accum_sum, valid, invalid, (cudaStream_t)stream);
 }
 
@@ -1698,6 +1703,7 @@ extern "C" int lt_render_stats_get(const lt_scene *cs, lt_render_stats *out) {
   if (!cs || !out) return lt_fail(LT_ERR_INVALID, "null argument");
   lt_scene *s = const_cast<lt_scene *>(cs);
   DeviceGuard g(s->device);
+  std::lock_guard<std::recursive_mutex> scene_lk(s->mu);
   if (s->ray_ctr.p) {
     unsigned long long c[6] = {0, 0, 0, 0, 0, 0};
     CK(cudaMemcpy(c, s->ray_ctr.p, sizeof(c), cudaMemcpyDeviceToHost));
@@ -1741,6 +1747,7 @@ extern "C" int lt_render_pass_host(lt_scene *s, const lt_render_params *p, doubl
   RET(validate_render(p));
   if (!accum_mean || !valid || !invalid) return lt_fail(LT_ERR_INVALID, "null output buffer");
   DeviceGuard g(s->device);
+  std::lock_guard<std::recursive_mutex> scene_lk(s->mu);
   const int64_t npx = (int64_t)p->width * p->height;
   RET(s->s_a.ensure(12 * npx));
   RET(s->s_b.ensure(4 * npx));
@@ -1799,6 +1806,7 @@ extern "C" int lt_intersect_batch(lt_scene *s, const float *origins, const float
   if (n == 0) return LT_OK;
   if (!origins || !dirs || !idx || !t) return lt_fail(LT_ERR_INVALID, "null ray buffer");
   DeviceGuard g(s->device);
+  std::lock_guard<std::recursive_mutex> scene_lk(s->mu);
   cudaStream_t st = (cudaStream_t)stream;
   RET(s->s_d.ensure(16 * n));
   RET(s->s_e.ensure(16 * n));
@@ -1833,6 +1841,7 @@ static int hits_host(lt_scene *s, const double *origins, const double *dirs, int
   if (n == 0) return LT_OK;
   if (!origins || !dirs || !idx || !t) return lt_fail(LT_ERR_INVALID, "null ray buffer");
   DeviceGuard g(s->device);
+  std::lock_guard<std::recursive_mutex> scene_lk(s->mu);
   cudaStream_t st = s->stream;
   RET(upload_rays_f64(s, origins, dirs, n, t_min, t_max, st));
   if (brute) {
@@ -1880,6 +1889,7 @@ extern "C" int lt_traversal_counts_host(lt_scene *s, const double *origins, cons
   if (n == 0) return LT_OK;
   if (!origins || !dirs || !nodes || !tests) return lt_fail(LT_ERR_INVALID, "null buffer");
   DeviceGuard g(s->device);
+  std::lock_guard<std::recursive_mutex> scene_lk(s->mu);
   cudaStream_t st = s->stream;
   RET(upload_rays_f64(s, origins, dirs, n, t_min, t_max, st));
   int32_t *d_nodes = nullptr, *d_tests = nullptr;
@@ -1908,6 +1918,7 @@ extern "C" int lt_trace_paths_host(lt_scene *s, const double *origins, const dou
   if (!(t_min > 0.0)) return lt_fail(LT_ERR_INVALID, "t_min must be positive");
   if (n >= (int64_t(1) << 31)) return lt_fail(LT_ERR_INVALID, "too many paths");
   DeviceGuard g(s->device);
+  std::lock_guard<std::recursive_mutex> scene_lk(s->mu);
   cudaStream_t st = s->stream;
   s->stats = lt_render_stats{};
   s->ev_used = 0;
@@ -2040,6 +2051,7 @@ extern "C" int lt_occluded_batch_host(lt_scene *s, const double *origins, const 
   if (n == 0) return LT_OK;
   if (!origins || !dirs || !occluded) return lt_fail(LT_ERR_INVALID, "null buffer");
   DeviceGuard g(s->device);
+  std::lock_guard<std::recursive_mutex> scene_lk(s->mu);
   cudaStream_t st = s->stream;
   RET(upload_rays_f64(s, origins, dirs, n, t_min, t_max, st));
   RET(s->s_b.ensure(std::max<int64_t>(16, 4 * n)));

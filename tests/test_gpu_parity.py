@@ -871,3 +871,52 @@ def test_degenerate_triangles_against_oracle():
     assert int(np.sum(idx != ref_i)) <= 2
     same = (idx == ref_i) & (ref_i >= 0)
     assert np.all(np.abs(t[same] - ref_t[same]) <= 2e-5 * np.maximum(1.0, ref_t[same]))
+
+
+def test_concurrent_threads_render_like_sequential():
+    """Host threads rendering on one device at the same time -- different
+    scenes and the same scene -- and issuing different ray queries against
+    one shared scene in between (the scene lock serializes its scratch; the
+    per-device workspace lease orders the passes) give exactly the
+    sequential results."""
+    import threading
+    m = lb()
+    scenes = [wl.cornell_box(48, 40, "mixed"), wl.scene_by_name("sphere70k", width=96, height=54),
+              wl.cornell_box(40, 40, "extended")]
+    dss = [m.DeviceScene(sc) for sc in scenes]
+    st = m.RenderSettings(samples_per_pixel=6, max_depth=6, seed=31)
+    want = [m.render_progressive(ds, st).image for ds in dss]
+    g = golden_scene("glossy")
+    gds = device_scene(g)
+    o, d = g["rays_o"], g["rays_d"]
+    rng = np.random.default_rng(5)
+    perms = [rng.permutation(len(o)) for _ in range(4)]
+    want_idx = [m.intersect_scene_batch(g.triangles, g.bvh, o[pm], d[pm], scene=gds)[0]
+                for pm in perms]
+    errors, done = [], []
+    # threads 0-2: their own scene; 3-4: scene 0 as well (same-scene passes)
+    plan = [0, 1, 2, 0, 0]
+
+    def worker(w):
+        k = plan[w]
+        try:
+            for rep in range(4):
+                img = m.render_progressive(dss[k], st).image
+                if not np.array_equal(img, want[k]):
+                    errors.append(f"worker {w} scene {k} rep {rep} differs")
+                q = (w + rep) % len(perms)
+                idx, _ = m.intersect_scene_batch(g.triangles, g.bvh, o[perms[q]], d[perms[q]],
+                                                 scene=gds)
+                if not np.array_equal(idx, want_idx[q]):
+                    errors.append(f"worker {w} query {q} differs")
+            done.append(w)
+        except Exception as exc:  # noqa: BLE001
+            errors.append(repr(exc))
+
+    threads = [threading.Thread(target=worker, args=(w,)) for w in range(len(plan))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join(timeout=300)
+    assert not errors, errors
+    assert sorted(done) == list(range(len(plan)))
