@@ -555,15 +555,12 @@ __global__ void __launch_bounds__(kShadeThreads, LT_SHADE_MIN_BLOCKS)
   const int n = *count_in;
   const int lane = threadIdx.x & 31;
   __shared__ int s_cnt[LT_DIR_BINS], s_off[LT_DIR_BINS], s_base;
-  if (sa.octant_sort) {
-    for (int b = threadIdx.x; b < LT_DIR_BINS; b += blockDim.x) s_cnt[b] = 0;
-    __syncthreads();
-  }
-  for (int base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
-    const int qi = base + threadIdx.x;
-    bool emit = false;
-    float4 out_o, out_d;
-    int cls = -1;  // material class of the lane's hit (LT_FLAG_COUNT statistics)
+  // this block iteration's continuation rays, staged for the grouped append
+  __shared__ float4 s_ro[LT_SHADE_ITEMS * kShadeThreads], s_rd[LT_SHADE_ITEMS * kShadeThreads];
+  for (int b = threadIdx.x; b < LT_DIR_BINS; b += blockDim.x) s_cnt[b] = 0;
+  __syncthreads();
+  // one queue entry: the segment, its path record, the continuation ray
+  auto process = [&](int qi, bool &emit, float4 &out_o, float4 &out_d, int &cls) {
     if (qi < n) {
       const int q = sa.perm ? __ldg(&sa.perm[qi]) : qi;
       // queue entries and path state stream through (evict-first) so the
@@ -614,65 +611,67 @@ __global__ void __launch_bounds__(kShadeThreads, LT_SHADE_MIN_BLOCKS)
       if (!emit && (sg.wrote_l || primary || (sg.scattered && pa.inc)))
         st_path(pa.S, p, T, L, sg.st_out);
     }
-    if (sa.warp_ctr) {
-      // shading divergence: distinct material classes among a warp's lanes
-      const unsigned act = __ballot_sync(kFull, cls >= 0);
-      if (act) {
-        const unsigned same = __match_any_sync(kFull, cls);
-        const bool first_of_class = cls >= 0 && __ffs(same & act) - 1 == lane;
-        const int distinct = __popc(__ballot_sync(kFull, first_of_class));
-        if (lane == __ffs(act) - 1) {
-          atomicAdd(&sa.warp_ctr[0], 1ull);
-          atomicAdd(&sa.warp_ctr[1], distinct > 1 ? 1ull : 0ull);
-          atomicAdd(&sa.warp_ctr[2], (unsigned long long)distinct);
+  };
+  // LT_SHADE_ITEMS consecutive 128-entry ranges per block iteration; their
+  // continuation rays are staged in shared memory (8 KB per block at 2, so
+  // a shade CTA still fits beside the trace CTAs of the other lane) and
+  // appended as one contiguous range of the next queue per block, laid out
+  // by direction octant (counting sort), so a trace warp fetches rays with
+  // nearby origins and similar directions; with octant_sort off the range
+  // keeps shading order.  (s_cnt is zeroed before the loop and re-zeroed by
+  // thread 0 once it has read the counts: two barriers per iteration.)
+  // One instance of the segment code per kernel: every ordering option
+  // runs the same arithmetic.
+  const int span = LT_SHADE_ITEMS * kShadeThreads;
+  for (int base = blockIdx.x * span; base < n; base += gridDim.x * span) {
+    int bins[LT_SHADE_ITEMS], ranks[LT_SHADE_ITEMS];
+#pragma unroll 1
+    for (int it = 0; it < LT_SHADE_ITEMS; ++it) {
+      bool emit = false;
+      float4 out_o, out_d;
+      int cls = -1;  // material class of the lane's hit (LT_FLAG_COUNT statistics)
+      process(base + it * kShadeThreads + threadIdx.x, emit, out_o, out_d, cls);
+      if (sa.warp_ctr) {
+        // shading divergence: distinct material classes among a warp's lanes
+        const unsigned act = __ballot_sync(kFull, cls >= 0);
+        if (act) {
+          const unsigned same = __match_any_sync(kFull, cls);
+          const bool first_of_class = cls >= 0 && __ffs(same & act) - 1 == lane;
+          const int distinct = __popc(__ballot_sync(kFull, first_of_class));
+          if (lane == __ffs(act) - 1) {
+            atomicAdd(&sa.warp_ctr[0], 1ull);
+            atomicAdd(&sa.warp_ctr[1], distinct > 1 ? 1ull : 0ull);
+            atomicAdd(&sa.warp_ctr[2], (unsigned long long)distinct);
+          }
         }
+      }
+      bins[it] = -1;
+      if (emit) {
+        bins[it] = sa.octant_sort ? dir_bin(out_d) : 0;
+        ranks[it] = atomicAdd(&s_cnt[bins[it]], 1);
+        s_ro[it * kShadeThreads + threadIdx.x] = out_o;
+        s_rd[it * kShadeThreads + threadIdx.x] = out_d;
       }
     }
-    if (sa.octant_sort) {
-      // block-aggregated append grouped by direction: one contiguous range
-      // of the next queue per block, laid out bin by bin (counting sort), so
-      // a trace warp fetches rays with nearby origins and similar
-      // directions (higher SIMT efficiency for incoherent bounces)
-      // (s_cnt is zeroed before the loop and re-zeroed by thread 0 once it
-      // has read the counts: two barriers per block iteration)
-      int bin = 0, rank = 0;
-      if (emit) {
-        bin = dir_bin(out_d);
-        rank = atomicAdd(&s_cnt[bin], 1);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int run = 0;
+      for (int b = 0; b < LT_DIR_BINS; ++b) {
+        s_off[b] = run;
+        run += s_cnt[b];
+        s_cnt[b] = 0;
       }
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        int run = 0;
-        for (int b = 0; b < LT_DIR_BINS; ++b) {
-          s_off[b] = run;
-          run += s_cnt[b];
-          s_cnt[b] = 0;
-        }
-        s_base = run ? atomicAdd(count_out, run) : 0;
-      }
-      __syncthreads();
-      if (emit) {
-        const int slot = s_base + s_off[bin] + rank;
+      s_base = run ? atomicAdd(count_out, run) : 0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int it = 0; it < LT_SHADE_ITEMS; ++it)
+      if (bins[it] >= 0) {
+        const int slot = s_base + s_off[bins[it]] + ranks[it];
         LT_ASSERT(slot < sa.cap);
-        __stcs(&n_o[slot], out_o);
-        __stcs(&n_d[slot], out_d);
+        __stcs(&n_o[slot], s_ro[it * kShadeThreads + threadIdx.x]);
+        __stcs(&n_d[slot], s_rd[it * kShadeThreads + threadIdx.x]);
       }
-    } else {
-      // warp-aggregated append to the next queue
-      const unsigned mask = __ballot_sync(kFull, emit);
-      if (mask) {
-        const int leader = __ffs(mask) - 1;
-        int slot0 = 0;
-        if (lane == leader) slot0 = atomicAdd(count_out, __popc(mask));
-        slot0 = __shfl_sync(kFull, slot0, leader);
-        if (emit) {
-          const int slot = slot0 + __popc(mask & ((1u << lane) - 1u));
-          LT_ASSERT(slot < sa.cap);
-          __stcs(&n_o[slot], out_o);
-          __stcs(&n_d[slot], out_d);
-        }
-      }
-    }
   }
 }
 

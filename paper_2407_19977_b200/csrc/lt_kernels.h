@@ -26,6 +26,13 @@ constexpr int kShadeThreads = LT_SHADE_THREADS;
 #ifndef LT_NODE_STEPS
 #define LT_NODE_STEPS 3
 #endif
+// queue entries per shade thread and block iteration: their continuation
+// rays are appended as one octant-grouped range of LT_SHADE_ITEMS x 128
+// (2: -3.8 % C4 step time, the next trace gains from the wider grouping;
+// profiles/r02_shade_items2.jsonl)
+#ifndef LT_SHADE_ITEMS
+#define LT_SHADE_ITEMS 2
+#endif
 #ifndef LT_SHADE_MIN_BLOCKS
 #define LT_SHADE_MIN_BLOCKS 8
 #endif
