@@ -25,6 +25,8 @@ from .integrator import (RenderResult, RenderSettings, environment_radiance,
                          generate_camera_ray, render_image, render_pass, render_progressive,
                          trace_radiance, trace_radiance_batch)
 from .procgen import bumpy_sphere, bumpy_sphere_glb, icosphere, icosphere_glb
+from .harness import (BenchmarkReport, BenchRow, auto_framing_camera, format_ms,
+                      load_benchmark_scene, run_benchmark, summarize_runs)
 from .ingest import (MaterialMap, RenderConfig, flatten_scene, generate_smooth_normals, load_gltf,
                      load_render_config, load_scene, save_glb, load_device_scene, load_scene_gpu)
 
@@ -50,4 +52,6 @@ __all__ = [
     "bumpy_sphere", "bumpy_sphere_glb", "icosphere", "icosphere_glb",
     "MaterialMap", "RenderConfig", "flatten_scene", "generate_smooth_normals", "load_gltf",
     "load_render_config", "load_scene", "save_glb", "load_device_scene", "load_scene_gpu",
+    "BenchRow", "BenchmarkReport", "auto_framing_camera", "format_ms", "load_benchmark_scene",
+    "run_benchmark", "summarize_runs",
 ]

@@ -147,7 +147,9 @@ REFERENCE_ALL = [   # luxtrace/__init__.py:40-65
     "tonemap_to_u8", "write_linear_dump", "write_png",
     "bumpy_sphere", "bumpy_sphere_glb", "icosphere", "icosphere_glb", "save_glb",
     "set_worker_count", "thread_cap",
-]   # (the benchmark harness names are out of scope)
+    "BenchRow", "BenchmarkReport", "auto_framing_camera", "format_ms", "load_benchmark_scene",
+    "run_benchmark", "summarize_runs",
+]
 
 
 def test_reference_api_names_exported():
