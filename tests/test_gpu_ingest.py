@@ -232,3 +232,118 @@ def test_device_ingest_errors(tmp_path):
                                     C.byref(dr))
     assert rc == _lib.LT_ERR_INVALID
     assert "outside its buffer" in _lib.lib().lt_last_error().decode()
+
+
+def random_gltf(rng, path):
+    """A random small GLB: 1-3 meshes of 1-2 primitives with u8 / u16 / u32
+    or implicit indices, interleaved (strided) or packed float32 positions,
+    optional normals, degenerate and empty primitives, and a node tree with
+    TRS / matrix / identity nodes, instancing and nested children."""
+    blobs, views, accessors = [], [], []
+    binary = b""
+
+    def add_view(data: bytes, stride=None):
+        nonlocal binary
+        v = {"buffer": 0, "byteOffset": len(binary), "byteLength": len(data)}
+        if stride:
+            v["byteStride"] = stride
+        views.append(v)
+        binary += data + b"\x00" * (-len(data) % 4)
+        return len(views) - 1
+
+    meshes = []
+    for _ in range(int(rng.integers(1, 4))):
+        prims = []
+        for _ in range(int(rng.integers(1, 3))):
+            nv = int(rng.integers(3, 40))
+            pos = rng.uniform(-2, 2, (nv, 3)).astype(np.float32)
+            if rng.uniform() < 0.2:
+                pos[1] = pos[0]                      # a degenerate corner pair
+            nrm = rng.normal(size=(nv, 3)).astype(np.float32) if rng.uniform() < 0.5 else None
+            attrs = {}
+            if nrm is not None and rng.uniform() < 0.5:
+                v = add_view(np.concatenate([pos, nrm], axis=1).tobytes(), stride=24)
+                accessors.append({"bufferView": v, "componentType": 5126, "count": nv,
+                                  "type": "VEC3"})
+                attrs["POSITION"] = len(accessors) - 1
+                accessors.append({"bufferView": v, "byteOffset": 12, "componentType": 5126,
+                                  "count": nv, "type": "VEC3"})
+                attrs["NORMAL"] = len(accessors) - 1
+            else:
+                v = add_view(pos.tobytes())
+                accessors.append({"bufferView": v, "componentType": 5126, "count": nv,
+                                  "type": "VEC3"})
+                attrs["POSITION"] = len(accessors) - 1
+                if nrm is not None:
+                    v = add_view(nrm.tobytes())
+                    accessors.append({"bufferView": v, "componentType": 5126, "count": nv,
+                                      "type": "VEC3"})
+                    attrs["NORMAL"] = len(accessors) - 1
+            prim = {"attributes": attrs}
+            kind = rng.integers(0, 4)
+            if kind < 3:
+                nt = int(rng.integers(0, 30))
+                idx = rng.integers(0, nv, 3 * nt)
+                dt, ct = [(np.uint8, 5121), (np.uint16, 5123), (np.uint32, 5125)][kind]
+                v = add_view(idx.astype(dt).tobytes())
+                accessors.append({"bufferView": v, "componentType": ct, "count": int(idx.size),
+                                  "type": "SCALAR"})
+                prim["indices"] = len(accessors) - 1
+            elif nv % 3:
+                accessors[attrs["POSITION"]]["count"] = nv - nv % 3   # implicit triangles
+                if "NORMAL" in attrs:
+                    accessors[attrs["NORMAL"]]["count"] = nv - nv % 3
+            prims.append(prim)
+        meshes.append({"primitives": prims})
+
+    def quat():
+        q = rng.normal(size=4)
+        return [float(x) for x in q / np.linalg.norm(q)]
+
+    nodes = []
+    n_nodes = int(rng.integers(1, 7))
+    for i in range(n_nodes):
+        node = {}
+        r = rng.uniform()
+        if r < 0.35:
+            node.update(translation=[float(x) for x in rng.uniform(-3, 3, 3)], rotation=quat(),
+                        scale=[float(x) for x in rng.uniform(0.2, 2.0, 3)])
+        elif r < 0.6:
+            m = np.eye(4)
+            m[:3, :3] = rng.normal(size=(3, 3))
+            m[:3, 3] = rng.uniform(-2, 2, 3)
+            node["matrix"] = [float(x) for x in m.T.ravel()]
+        if rng.uniform() < 0.8:
+            node["mesh"] = int(rng.integers(0, len(meshes)))
+        kids = [j for j in range(i + 1, n_nodes) if rng.uniform() < 0.3]
+        if kids:
+            node["children"] = kids
+        nodes.append(node)
+    children = {c for n in nodes for c in n.get("children", [])}
+    doc = {"asset": {"version": "2.0"}, "buffers": [{"byteLength": len(binary)}],
+           "bufferViews": views, "accessors": accessors, "meshes": meshes, "nodes": nodes,
+           "scenes": [{"nodes": [i for i in range(n_nodes) if i not in children]}]}
+    path.write_bytes(_glb(doc, binary))
+
+
+def test_device_ingest_fuzz(tmp_path):
+    """60 random documents: whatever load_scene returns or raises,
+    load_scene_gpu returns the same arrays bit for bit or raises the same
+    SceneError."""
+    from paper_2407_19977_b200.ingest import load_scene, load_scene_gpu
+    rng = np.random.default_rng(2024)
+    compared = 0
+    for case in range(60):
+        glb = tmp_path / f"r{case}.glb"
+        random_gltf(rng, glb)
+        try:
+            want = load_scene(glb, DIR / "config.json")
+        except Exception as exc:  # noqa: BLE001
+            with pytest.raises(type(exc)) as ei:
+                load_scene_gpu(glb, DIR / "config.json")
+            assert str(ei.value) == str(exc), case
+            continue
+        got = load_scene_gpu(glb, DIR / "config.json")
+        assert_same_scene(got, want)
+        compared += 1
+    assert compared >= 40
