@@ -189,6 +189,7 @@ struct Lane {
   int64_t cap = 0;
   int32_t depth_cap = 0;
   DevBuf q_o[2], q_d[2], hits, S, inc, counters;
+  DevBuf rng;  // per-batch PCG tables (launch_rng_tables)
   // LT_FLAG_SORT_MATERIALS: per-entry class, the class-grouped slot order,
   // class totals + cursors
   DevBuf cls, perm, cls_ctr;
@@ -1592,6 +1593,10 @@ static int render_impl(lt_scene *s, const lt_render_params *p, float *accum, uin
     const char *e = std::getenv("LT_FUSED_MAX");
     return e ? (int64_t)std::atoll(e) : kFusedMaxPaths;
   }();
+  const bool rng_tables = [] {
+    const char *e = std::getenv("LT_RNG_TABLES");
+    return !(e && e[0] == '0');
+  }();
   const bool fused = n_local * p->sample_count <= fused_max &&
                      !(p->flags & (LT_FLAG_COUNT | LT_FLAG_SORT_MATERIALS));
   const int n_lanes =
@@ -1661,6 +1666,17 @@ static int render_impl(lt_scene *s, const lt_render_params *p, float *accum, uin
     ra.pix_list = pix_list;
     ra.n_paths = b.np * b.ns;
     ra.t_min = t_min;
+    if (rng_tables) {
+      // the batch's PCG increments (per pixel) and seeding terms (per
+      // sample) once, instead of three mix64 per path in raygen and again
+      // in the depth-0 shade
+      RET(ln.rng.ensure(sizeof(uint64_t) * (size_t)(b.np + b.ns)));
+      uint64_t *tab = ln.rng.as<uint64_t>();
+      ra.inc_tab = tab;
+      ra.init_tab = tab + b.np;
+      launch_rng_tables(ra, b.ns, tab, tab + b.np, ls);
+      s->stats.kernel_launches += 1;
+    }
     if (fused) {
       // (LT_FLAG_PROFILE times the fused launch as the pass's trace time)
       if (p->flags & LT_FLAG_PROFILE) RET(record_event(s, ls));

@@ -145,6 +145,16 @@ __global__ void k_flatten_tris(const double *__restrict__ v0, const double *__re
 // two jitter draws, float64 pinhole direction; returns the PCG state after
 // the two draws.  Raygen writes the ray record the depth-0 trace and shade
 // read; the depth-0 shade regenerates only the PCG state (primary_rng).
+// seed_stream (rng.py:70-78) from the batch tables: st = 0 -> inc after the
+// first step, + init_state, one more step -- the same 64-bit arithmetic
+__device__ __forceinline__ void seed_from_tables(const RaygenArgs &ra, int64_t i, int64_t s_local,
+                                                 uint64_t &state, uint64_t &inc) {
+  inc = __ldg(&ra.inc_tab[i]);
+  uint64_t st = inc + __ldg(&ra.init_tab[s_local]);
+  (void)pcg_next(st, inc);
+  state = st;
+}
+
 __device__ __forceinline__ void primary_ray(const RaygenArgs &ra, int64_t p, f3 &o, f3 &d,
                                             uint64_t &state, uint64_t &inc) {
   // batch-local path index and pixel count are < 2^31 (int32 queues): a
@@ -153,9 +163,13 @@ __device__ __forceinline__ void primary_ray(const RaygenArgs &ra, int64_t p, f3 
   const int64_t i = p - s_local * ra.n_pix;
   const int64_t pix = ra.pix_list ? (int64_t)ra.pix_list[ra.pix_offset + i] : ra.pix_offset + i;
   const int64_t sample = ra.sample_base + s_local;
-  const int64_t py = pix / ra.width;
+  // (pixel indices are < 2^31: a 32-bit division, not the 64-bit routine)
+  const int64_t py = (int64_t)((uint32_t)pix / (uint32_t)ra.width);
   const int64_t px = pix - py * ra.width;
-  seed_stream((uint64_t)pix, (uint64_t)sample, ra.seed, state, inc);
+  if (ra.inc_tab)
+    seed_from_tables(ra, i, s_local, state, inc);
+  else
+    seed_stream((uint64_t)pix, (uint64_t)sample, ra.seed, state, inc);
   const double jx = unit_f64(state, inc);
   const double jy = unit_f64(state, inc);
   d = camera_dir(ra.cam, (double)px, (double)py, jx, jy, ra.width, ra.height);
@@ -168,8 +182,13 @@ __device__ __forceinline__ void primary_rng(const RaygenArgs &ra, int64_t p, uin
                                             uint64_t &inc) {
   const int64_t s_local = (int64_t)((uint32_t)p / (uint32_t)ra.n_pix);
   const int64_t i = p - s_local * ra.n_pix;
-  const int64_t pix = ra.pix_list ? (int64_t)ra.pix_list[ra.pix_offset + i] : ra.pix_offset + i;
-  seed_stream((uint64_t)pix, (uint64_t)(ra.sample_base + s_local), ra.seed, state, inc);
+  if (ra.inc_tab) {
+    seed_from_tables(ra, i, s_local, state, inc);
+  } else {
+    const int64_t pix =
+        ra.pix_list ? (int64_t)ra.pix_list[ra.pix_offset + i] : ra.pix_offset + i;
+    seed_stream((uint64_t)pix, (uint64_t)(ra.sample_base + s_local), ra.seed, state, inc);
+  }
   (void)pcg_next(state, inc);
   (void)pcg_next(state, inc);
 }
@@ -179,6 +198,8 @@ __device__ __forceinline__ void primary_rng(const RaygenArgs &ra, int64_t p, uin
 __device__ __forceinline__ uint64_t path_inc(const RaygenArgs &ra, int64_t p) {
   const int64_t s_local = (int64_t)((uint32_t)p / (uint32_t)ra.n_pix);
   const int64_t i = p - s_local * ra.n_pix;
+  // (not ra.inc_tab: a random 8 B table load measured slower here than the
+  // hash, profiles/r02_rng_tables3.jsonl)
   const int64_t pix = ra.pix_list ? (int64_t)ra.pix_list[ra.pix_offset + i] : ra.pix_offset + i;
   return (mix64((uint64_t)pix) << 1) | 1ULL;
 }
@@ -201,6 +222,17 @@ __device__ __forceinline__ void st_path(float4 *__restrict__ S, int64_t p, const
                "f"(T.x), "f"(T.y), "f"(T.z), "f"(L.x), "f"(L.y), "f"(L.z),
                "f"(__uint_as_float((uint32_t)state)), "f"(__uint_as_float((uint32_t)(state >> 32)))
                : "memory");
+}
+
+__global__ void k_rng_tables(RaygenArgs ra, int64_t n_samples, uint64_t *__restrict__ inc_tab,
+                             uint64_t *__restrict__ init_tab) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t < ra.n_pix) {
+    const int64_t pix =
+        ra.pix_list ? (int64_t)ra.pix_list[ra.pix_offset + t] : ra.pix_offset + t;
+    inc_tab[t] = (mix64((uint64_t)pix) << 1) | 1ULL;
+  }
+  if (t < n_samples) init_tab[t] = mix64(ra.seed ^ mix64((uint64_t)(ra.sample_base + t)));
 }
 
 // Primary rays of a render batch: only the 16 B direction record is written
@@ -1216,6 +1248,13 @@ void launch_flatten_tris(const double *v0, const double *v1, const double *v2, c
                          float4 *shade, cudaStream_t st) {
   k_flatten_tris<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(v0, v1, v2, n0, n1, n2, mat_index,
                                                               order, leaf_end, n, tris, shade);
+}
+
+void launch_rng_tables(const RaygenArgs &ra, int64_t n_samples, uint64_t *inc_tab,
+                       uint64_t *init_tab, cudaStream_t st) {
+  const int64_t n = ra.n_pix > n_samples ? ra.n_pix : n_samples;
+  if (n <= 0) return;
+  k_rng_tables<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(ra, n_samples, inc_tab, init_tab);
 }
 
 void launch_raygen(const RaygenArgs &ra, const PathArrays &pa, float4 *q_o, float4 *q_d,

@@ -57,6 +57,11 @@ struct RaygenArgs {
   const int32_t *pix_list;  // local -> global pixel (NULL: identity)
   int64_t n_paths;       // n_pix * samples in this batch
   float t_min;
+  // optional per-batch tables (launch_rng_tables): the PCG increment of
+  // batch pixel i and the seeding term mix64(seed ^ mix64(sample)) of
+  // batch sample s -- the same values seed_stream derives per path
+  const uint64_t *inc_tab;
+  const uint64_t *init_tab;
 };
 
 struct ShadeArgs {
@@ -95,6 +100,9 @@ void launch_flatten_tris(const double *v0, const double *v1, const double *v2, c
                          const double *n1, const double *n2, const int32_t *mat_index,
                          const int32_t *order, const uint8_t *leaf_end, int64_t n, float4 *tris,
                          float4 *shade, cudaStream_t st);
+// fill ra.inc_tab[0 .. n_pix) and ra.init_tab[0 .. n_samples) for a batch
+void launch_rng_tables(const RaygenArgs &ra, int64_t n_samples, uint64_t *inc_tab,
+                       uint64_t *init_tab, cudaStream_t st);
 void launch_raygen(const RaygenArgs &ra, const PathArrays &pa, float4 *q_o, float4 *q_d,
                    int32_t *count0, cudaStream_t st);
 void launch_raygen_explicit(const double *o, const double *d, const uint64_t *state,
