@@ -70,8 +70,12 @@ def emitted_radiance(params) -> np.ndarray:
 
 
 def pack_materials(materials):
-    """The reference's 9-array SoA packing (material.py:68-92), same order."""
-    t = pack_material_table(materials)
+    """The reference's 9-array SoA packing (material.py:68-92), same order
+    (fresh, writable arrays, as the reference returns)."""
+    mats = list(materials)
+    if not mats:
+        raise ValueError("scene has no materials")
+    t = _pack_material_table(mats)
     return (t["base_weight"], t["base_color"], t["base_metalness"], t["specular_weight"],
             t["specular_color"], t["specular_roughness"], t["specular_ior"],
             t["emission_luminance"], t["emission_color"])
@@ -83,12 +87,31 @@ _SCALARS = ("base_weight", "base_metalness", "specular_weight", "specular_roughn
 _COLORS = ("base_color", "specular_color", "emission_color", "coat_color", "transmission_color")
 
 
+_TABLES: dict = {}
+
+
 def pack_material_table(materials) -> dict[str, np.ndarray]:
     """All material arrays (reference + extension) keyed by field name;
-    (k,) or (k, 3) float64, C-contiguous."""
+    (k,) or (k, 3) float64, C-contiguous.  Memoized for hashable (frozen)
+    material objects; the arrays are shared, read-only."""
     mats = list(materials)
     if not mats:
         raise ValueError("scene has no materials")
+    try:
+        key = tuple(mats)
+        hit = _TABLES.get(key)
+    except TypeError:           # unhashable material objects: no memo
+        return _pack_material_table(mats)
+    if hit is None:
+        if len(_TABLES) >= 64:
+            _TABLES.clear()
+        hit = _TABLES[key] = _pack_material_table(mats)
+        for a in hit.values():
+            a.flags.writeable = False
+    return hit
+
+
+def _pack_material_table(mats) -> dict[str, np.ndarray]:
     out = {}
     for name in _SCALARS:
         out[name] = np.array([float(getattr(m, name, EXTENSION_DEFAULTS.get(name, 0.0)))

@@ -105,9 +105,29 @@ class SceneDescription:
     degenerate_dropped: int = 0
 
 
+_CAMERA_PACKS: dict = {}
+
+
 def camera_pack(camera) -> np.ndarray:
     """[position, forward, right, up, tan(fov/2), aspect] -- the 14 doubles of
-    _camera_pack (integrator.py:75-83), same numpy operations."""
+    _camera_pack (integrator.py:75-83), same numpy operations.  Memoized by
+    the camera's values (a dozen small numpy calls cost ~0.1 ms, a visible
+    share of a small render call); a copy is returned."""
+    try:
+        key = (tuple(float(x) for x in camera.position),
+               tuple(float(x) for x in camera.look_at), tuple(float(x) for x in camera.up),
+               float(camera.vertical_fov_deg), int(camera.width), int(camera.height))
+    except (TypeError, ValueError):
+        return _camera_pack(camera)
+    hit = _CAMERA_PACKS.get(key)
+    if hit is None:
+        if len(_CAMERA_PACKS) >= 64:
+            _CAMERA_PACKS.clear()
+        hit = _CAMERA_PACKS[key] = _camera_pack(camera)
+    return hit.copy()
+
+
+def _camera_pack(camera) -> np.ndarray:
     position = np.asarray(camera.position, dtype=np.float64)
     forward = normalize(np.asarray(camera.look_at, dtype=np.float64) - position)
     right = normalize(np.cross(forward, np.asarray(camera.up, dtype=np.float64)))
