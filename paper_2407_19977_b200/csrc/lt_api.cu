@@ -179,7 +179,14 @@ constexpr int kLanes = 4;          // upper bound; LT_LANES picks 1..kLanes (def
 constexpr int kDefaultLanes = 2;
 // pinned staging ring for pageable scene arrays: kRingWorkers host threads,
 // two kRingSlot slots each
-constexpr int kRingWorkers = 6;
+#ifndef LT_RING_WORKERS
+#define LT_RING_WORKERS 6
+#endif
+#ifndef LT_BVH_WORKERS
+#define LT_BVH_WORKERS 2
+#endif
+constexpr int kRingWorkers = LT_RING_WORKERS;
+constexpr int kBvhWorkers = LT_BVH_WORKERS;  // of them staging the BVH arrays
 constexpr int kRingSlots = 2 * kRingWorkers;
 constexpr size_t kRingSlot = size_t(4) << 20;
 // resident buffers of destroyed scenes kept for reuse
@@ -975,6 +982,10 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
     for (int k = 0; k < 6; ++k) items.push_back({&t_v[k], src[k], 24 * (size_t)n, true});
     items.push_back({&t_mat, d->material_index, 4 * (size_t)n, true});
   }
+  // the lat-long texels travel with the triangle arrays (on the side stream
+  // when there is one), not after the layout
+  const int64_t env_np = d->env_kind == LT_ENV_LATLONG ? (int64_t)d->env_width * d->env_height : 0;
+  if (env_np) items.push_back({&t_env, d->env_texels, sizeof(float) * 3 * (size_t)env_np, true});
   if (!build_here) {
     items.push_back({&t_order, d->triangle_order, 4 * (size_t)n, false});
     items.push_back({&t_bmin, d->bounds_min, 24 * (size_t)nn, false});
@@ -1099,7 +1110,8 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
       RET(ensure_ring(W));
       CK(cudaEventCreateWithFlags(&tri_done, cudaEventDisableTiming));
       tri_thread = std::thread([&, tri_items = copies(true)]() {
-        tri_rc = staged_h2d(W, device, tri_items, W.upload_st, 2, kRingWorkers - 2);
+        tri_rc = staged_h2d(W, device, tri_items, W.upload_st, kBvhWorkers,
+                            kRingWorkers - kBvhWorkers);
         if (tri_rc == LT_OK) {
           const cudaError_t e = cudaEventRecord(tri_done, W.upload_st);
           if (e != cudaSuccess)
@@ -1107,7 +1119,7 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
         }
         if (tri_rc != LT_OK) tri_msg = g_last_error;
       });
-      RET(staged_h2d(W, device, copies(false), st, 0, 2));
+      RET(staged_h2d(W, device, copies(false), st, 0, kBvhWorkers));
       pt.mark("BVH arrays staged");
     }
     g_bmin = t_bmin.as<double>();
@@ -1197,15 +1209,11 @@ static int scene_create_impl(const lt_scene_desc *d, int32_t device, lt_scene *s
     for (int i = 0; i < d->n_materials; ++i) build_material(d, i, mats[i]);
     if ((rc = upload(s->mats, mats.data(), mats.size(), st))) break;
     // environment
-    if (d->env_kind == LT_ENV_LATLONG) {
-      const int64_t np = (int64_t)d->env_width * d->env_height;
-      // float3 texels as given; widened to float4 records on the device
-      const size_t env_bytes = sizeof(float) * 3 * (size_t)np;
-      if ((rc = t_env.alloc(env_bytes, st))) break;
-      if ((rc = ensure_ring(W))) break;
-      if ((rc = staged_h2d(W, device, {CopyItem{t_env.p, d->env_texels, env_bytes}}, st))) break;
-      if ((rc = s->env.ensure((size_t)np * 16))) break;
-      launch_expand_rgb(t_env.as<float>(), np, s->env.as<float4>(), st);
+    if (env_np) {
+      // float3 texels as given (uploaded with the triangle arrays), widened
+      // to float4 records on the device
+      if ((rc = s->env.ensure((size_t)env_np * 16))) break;
+      launch_expand_rgb(t_env.as<float>(), env_np, s->env.as<float4>(), st);
     }
     pt.mark("materials + env");
     e = cudaStreamSynchronize(st);
