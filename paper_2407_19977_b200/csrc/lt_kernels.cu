@@ -573,9 +573,9 @@ __device__ __forceinline__ bool shade_segment(const SceneView &sc, int32_t depth
 // miss -> environment; hit -> emission; final segment stops; otherwise hit
 // frame, 3 draws, BSDF sample, throughput, Russian roulette (4th draw), and
 // the continuation ray is appended to the next queue: one atomic per block
-// iteration, the block's rays laid out by direction octant (or, with
-// ShadeArgs.octant_sort off, warp ballot + one atomic per warp).  With
-// ShadeArgs.perm the queue is shaded in material-class order.
+// iteration (LT_SHADE_ITEMS x 128 entries), the block's rays laid out by
+// direction octant (with ShadeArgs.octant_sort off, in shading order).
+// With ShadeArgs.perm the queue is shaded in material-class order.
 __global__ void __launch_bounds__(kShadeThreads, LT_SHADE_MIN_BLOCKS)
     k_shade(SceneView sc, ShadeArgs sa, RaygenArgs ra, PathArrays pa,
             const float4 *__restrict__ q_o, const float4 *__restrict__ q_d,
