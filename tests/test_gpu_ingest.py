@@ -323,18 +323,30 @@ def random_gltf(rng, path):
     doc = {"asset": {"version": "2.0"}, "buffers": [{"byteLength": len(binary)}],
            "bufferViews": views, "accessors": accessors, "meshes": meshes, "nodes": nodes,
            "scenes": [{"nodes": [i for i in range(n_nodes) if i not in children]}]}
-    path.write_bytes(_glb(doc, binary))
+    if path.suffix == ".gltf":
+        # a .gltf with its buffer in an external .bin file (the URI resolved
+        # next to the document) or inline as a base64 data URI
+        if rng.uniform() < 0.5:
+            (path.parent / (path.stem + ".bin")).write_bytes(binary)
+            doc["buffers"][0]["uri"] = path.stem + ".bin"
+        else:
+            import base64
+            doc["buffers"][0]["uri"] = ("data:application/octet-stream;base64," +
+                                        base64.b64encode(binary).decode())
+        path.write_text(json.dumps(doc))
+    else:
+        path.write_bytes(_glb(doc, binary))
 
 
 def test_device_ingest_fuzz(tmp_path):
-    """60 random documents: whatever load_scene returns or raises,
-    load_scene_gpu returns the same arrays bit for bit or raises the same
-    SceneError."""
+    """60 random documents (a third of them .gltf with an external .bin or a
+    data-URI buffer): whatever load_scene returns or raises, load_scene_gpu
+    returns the same arrays bit for bit or raises the same SceneError."""
     from paper_2407_19977_b200.ingest import load_scene, load_scene_gpu
     rng = np.random.default_rng(2024)
     compared = 0
     for case in range(60):
-        glb = tmp_path / f"r{case}.glb"
+        glb = tmp_path / (f"r{case}.gltf" if case % 3 == 2 else f"r{case}.glb")
         random_gltf(rng, glb)
         try:
             want = load_scene(glb, DIR / "config.json")
